@@ -1,0 +1,171 @@
+"""Double-precision CPU oracle for TNRD/TRDPD inference -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this package.  The product path
+(paper_1510_02930_b200) never imports it and shares no code with it.
+
+The arithmetic lives in tnrd_oracle.c (plain C, double, OpenMP over rows);
+this module compiles it with gcc and exposes it through ctypes.  Every C
+function cites the PAPER.md / SPEC.md passage it follows.
+
+Parity pins (tests/test_oracle_pins.py) tie each function to something other
+than itself: brute-force dense matrices, scipy.ndimage.convolve, closed forms,
+scalar minimisation of Eq.10, invariants.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "tnrd_oracle.c")
+_LIB = os.path.join(_HERE, "libtnrd_oracle.so")
+_lock = threading.Lock()
+_lib = None
+
+BOUNDARY_EXPLICIT = 0  # R1: symmetric-extension rotated-kernel convolution (P l.302-311)
+BOUNDARY_ADJOINT = 1   # R2: exact transpose K^T (P l.298-301; S l.57-65)
+PHI_RBF = 0
+PHI_LINEAR = 1
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle shared library with gcc (-O2, OpenMP, IEEE math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c99", "-Wall",
+               "-o", _LIB, _SRC, "-lm"]
+        subprocess.run(cmd, check=True)
+    return _LIB
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = ctypes.CDLL(_LIB)
+            dp = ctypes.POINTER(ctypes.c_double)
+            i = ctypes.c_int
+            L.oracle_rot180.argtypes = [i, dp, dp]
+            L.oracle_conv2d_sym.argtypes = [i, i, dp, i, dp, dp]
+            L.oracle_conv2d_adjoint.argtypes = [i, i, dp, i, dp, dp]
+            L.oracle_phi.argtypes = [i, dp, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double]
+            L.oracle_phi.restype = ctypes.c_double
+            L.oracle_prox.argtypes = [ctypes.c_double] * 3
+            L.oracle_prox.restype = ctypes.c_double
+            L.oracle_stage.argtypes = [i, i, dp, dp, i, i, i, dp, dp, dp, dp, dp, ctypes.c_double,
+                                       i, i, dp, dp]
+            L.oracle_denoise.argtypes = [i, i, dp, i, i, i, i, dp, dp, dp, dp, dp, dp, i, i, dp]
+            _lib = L
+    return _lib
+
+
+def _d(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def rot180(k) -> np.ndarray:
+    k = _d(k)
+    out = np.empty_like(k)
+    lib().oracle_rot180(k.shape[0], _p(k), _p(out))
+    return out
+
+
+def conv2d_sym(x, k) -> np.ndarray:
+    x, k = _d(x), _d(k)
+    out = np.empty_like(x)
+    lib().oracle_conv2d_sym(x.shape[0], x.shape[1], _p(x), k.shape[0], _p(k), _p(out))
+    return out
+
+
+def conv2d_adjoint(y, k) -> np.ndarray:
+    y, k = _d(y), _d(k)
+    out = np.empty_like(y)
+    lib().oracle_conv2d_adjoint(y.shape[0], y.shape[1], _p(y), k.shape[0], _p(k), _p(out))
+    return out
+
+
+def phi(w, mu0: float, step: float, gamma: float, z) -> np.ndarray:
+    w = _d(w)
+    L = lib()
+    zz = np.asarray(z, dtype=np.float64)
+    out = np.array([L.oracle_phi(w.shape[0], _p(w), float(mu0), float(step), float(gamma), float(v))
+                    for v in zz.ravel()])
+    return out.reshape(zz.shape)
+
+
+def prox(ut, lam, f) -> np.ndarray:
+    ut, lam, f = np.broadcast_arrays(np.asarray(ut, np.float64), np.asarray(lam, np.float64),
+                                     np.asarray(f, np.float64))
+    L = lib()
+    out = np.array([L.oracle_prox(float(a), float(b), float(c))
+                    for a, b, c in zip(ut.ravel(), lam.ravel(), f.ravel())])
+    return out.reshape(ut.shape)
+
+
+def _model_arrays(model):
+    return (_d(model.filters), _d(model.rbf_w), _d(model.rbf_mu0), _d(model.rbf_step),
+            _d(model.rbf_gamma), _d(model.lam))
+
+
+def stage(u, f, model, t: int = 0, boundary: int = BOUNDARY_EXPLICIT, phi_mode: int = PHI_RBF,
+          return_u_tilde: bool = False):
+    """One stage of Eq.13 with params[t]."""
+    u, f = _d(u), _d(f)
+    H, W = u.shape
+    filt, w, mu0, step, gam, lam = _model_arrays(model)
+    Nk, m, M = filt.shape[1], filt.shape[2], w.shape[2]
+    out = np.empty_like(u)
+    ut = np.empty_like(u)
+    lib().oracle_stage(H, W, _p(u), _p(f), Nk, m, M, _p(_d(filt[t])), _p(_d(w[t])),
+                       _p(_d(mu0[t])), _p(_d(step[t])), _p(_d(gam[t])), float(lam[t]),
+                       boundary, phi_mode, _p(out), _p(ut))
+    return (out, ut) if return_u_tilde else out
+
+
+def denoise(f, model, boundary: int = BOUNDARY_EXPLICIT, phi_mode: int = PHI_RBF) -> np.ndarray:
+    """u_T for one image f [H][W] (or a batch [B][H][W], looped)."""
+    f = _d(f)
+    if f.ndim == 3:
+        return np.stack([denoise(fi, model, boundary, phi_mode) for fi in f])
+    H, W = f.shape
+    filt, w, mu0, step, gam, lam = _model_arrays(model)
+    T, Nk, m, M = filt.shape[0], filt.shape[1], filt.shape[2], w.shape[2]
+    out = np.empty_like(f)
+    lib().oracle_denoise(H, W, _p(f), T, Nk, m, M, _p(filt), _p(w), _p(mu0), _p(step), _p(gam),
+                         _p(lam), boundary, phi_mode, _p(out))
+    return out
+
+
+def denoise_window(f, model, y0: int, y1: int, x0: int, x1: int,
+                   boundary: int = BOUNDARY_EXPLICIT) -> np.ndarray:
+    """u_T on the window [y0,y1) x [x0,x1) of a large image, computed exactly on a
+    crop with a 2rT dependency margin (pin P12: the output depends on the input
+    only within radius 2rT; crop edges on true image edges need no margin)."""
+    f = np.asarray(f)
+    H, W = f.shape
+    R = 2 * (model.k // 2) * model.T
+    cy0, cy1 = max(0, y0 - R), min(H, y1 + R)
+    cx0, cx1 = max(0, x0 - R), min(W, x1 + R)
+    u = denoise(f[cy0:cy1, cx0:cx1], model, boundary)
+    return u[y0 - cy0:y1 - cy0, x0 - cx0:x1 - cx0]
+
+
+def psnr(u, clean, peak: float) -> float:
+    """10 log10(peak^2 / MSE), unclamped (S l.374 after the 255/peak rescale)."""
+    mse = float(np.mean((np.asarray(u, np.float64) - np.asarray(clean, np.float64)) ** 2))
+    return float("inf") if mse == 0 else 10.0 * np.log10(peak * peak / mse)
+
+
+def num_threads() -> int:
+    v = os.environ.get("OMP_NUM_THREADS")
+    return int(v) if v else (os.cpu_count() or 1)

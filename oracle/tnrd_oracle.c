@@ -1,0 +1,167 @@
+/*
+ * TNRD / TRDPD Poisson-denoising ORACLE -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, double-precision CPU implementation of the inference pass of
+ * Feng & Chen, "Fast and Accurate Poisson Denoising with Optimized Nonlinear
+ * Diffusion" (arXiv 1510.02930).  Citations "P l.N" are lines of PAPER.md,
+ * "S l.N" lines of SPEC.md.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  It shares no code, header or
+ * constant with the CUDA path (paper_1510_02930_b200/csrc) and never calls it.
+ *
+ * Conventions (DESIGN.md §2 lists every reading):
+ *   - images are row-major [H][W] (S l.22-27), u in R^N (P l.101-102);
+ *   - "*" is true 2-D convolution (P l.137, l.142-144; S l.50);
+ *   - symmetric boundary = half-sample mirror, edge pixel duplicated
+ *     (P l.302 "symmetric boundary condition"; S l.73);
+ *   - stage s = 0..T-1 uses params[s] for k, phi and lambda (P Eq.13 l.328-332).
+ */
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define EXPORT __attribute__((visibility("default")))
+
+/* Half-sample symmetric extension index: x -> [0, n).  Folds repeatedly so
+ * that it is defined for any x (S l.73: pad value at -1 equals value at 0). */
+static long mirror_index(long x, long n) {
+    long period = 2 * n;
+    long m = x % period;
+    if (m < 0) m += period;
+    return m < n ? m : period - 1 - m;
+}
+
+/* rot180: kbar[i][j] = k[m-1-i][m-1-j]  (P l.143-144 "rotating the kernel k_i
+ * 180 degrees"; S l.40). */
+EXPORT void oracle_rot180(int m, const double *k, double *kbar) {
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j)
+            kbar[i * m + j] = k[(m - 1 - i) * m + (m - 1 - j)];
+}
+
+/* conv2d_sym: out(p,q) = sum_{a,b=-r..r} k[a+r][b+r] * E(x)(p-a, q-b), E the
+ * symmetric extension (P l.137 "k_i * u", l.302 symmetric boundary; S l.47-55). */
+EXPORT void oracle_conv2d_sym(int H, int W, const double *x, int m, const double *k, double *out) {
+    int r = m / 2;
+#pragma omp parallel for schedule(static)
+    for (int p = 0; p < H; ++p) {
+        for (int q = 0; q < W; ++q) {
+            double s = 0.0;
+            for (int a = -r; a <= r; ++a) {
+                long pp = mirror_index((long)p - a, H);
+                for (int b = -r; b <= r; ++b) {
+                    long qq = mirror_index((long)q - b, W);
+                    s += k[(a + r) * m + (b + r)] * x[pp * W + qq];
+                }
+            }
+            out[(long)p * W + q] = s;
+        }
+    }
+}
+
+/* conv2d_adjoint: the exact transpose K^T of conv2d_sym (P l.295-301 "K_i^T";
+ * S l.57-65: scatter-add of reflected contributions).  Boundary reading R2. */
+EXPORT void oracle_conv2d_adjoint(int H, int W, const double *y, int m, const double *k, double *out) {
+    int r = m / 2;
+    memset(out, 0, sizeof(double) * (size_t)H * W);
+    for (int p = 0; p < H; ++p)
+        for (int q = 0; q < W; ++q)
+            for (int a = -r; a <= r; ++a) {
+                long pp = mirror_index((long)p - a, H);
+                for (int b = -r; b <= r; ++b) {
+                    long qq = mirror_index((long)q - b, W);
+                    out[pp * W + qq] += k[(a + r) * m + (b + r)] * y[(long)p * W + q];
+                }
+            }
+}
+
+/* Influence function phi(z) = sum_{j<M} w_j exp(-(z - mu_j)^2 / (2 gamma^2)),
+ * mu_j = mu0 + j*step: Gaussian-RBF mixture on uniform centres
+ * (P l.145-146 phi "not restricted to be of a certain kind"; S l.104-107, l.140;
+ * BASELINE.json north_star).  Direct sum over all M terms. */
+EXPORT double oracle_phi(int M, const double *w, double mu0, double step, double gamma, double z) {
+    double s = 0.0;
+    for (int j = 0; j < M; ++j) {
+        double d = z - (mu0 + j * step);
+        s += w[j] * exp(-(d * d) / (2.0 * gamma * gamma));
+    }
+    return s;
+}
+
+/* Poisson proximal map, P Eq.12 (l.318-322) with tau = 1 (l.333):
+ *   u = (ut - lam + sqrt((ut - lam)^2 + 4 lam f)) / 2.
+ * For ut - lam < 0 the algebraically equal form 2 lam f / (sqrt(.) - (ut - lam))
+ * avoids cancellation (S l.215); f = 0 then gives exactly max(ut - lam, 0) (S l.183). */
+EXPORT double oracle_prox(double ut, double lam, double f) {
+    double delta = ut - lam;
+    double sigma = sqrt(delta * delta + 4.0 * lam * f);
+    if (delta >= 0.0) return 0.5 * (delta + sigma);
+    if (f == 0.0) return 0.0;
+    return 2.0 * lam * f / (sigma - delta);
+}
+
+/* One diffusion stage, P Eq.13 (l.326-333):
+ *   ut = u - sum_i kbar_i * phi_i(k_i * u),   u_next = prox_lambda(ut).
+ * boundary 0 (R1, default): the second convolution is the explicit rotated-kernel
+ *   convolution with the symmetric boundary (P l.302-311 "revise the above
+ *   formulation as explicit convolutions").
+ * boundary 1 (R2): the exact transpose K_i^T (P l.298-301; S l.57-65).
+ * phi_mode 0: RBF phi;  phi_mode 1: linear phi_i(z) = w[i][0] * z (oracle-only
+ *   switch used to pin linear diffusion, BASELINE.json north_star).
+ * Filters are taken in ascending i (S l.219). */
+EXPORT void oracle_stage(int H, int W, const double *u, const double *f,
+                         int Nk, int m, int M,
+                         const double *filters, /* [Nk][m][m] */
+                         const double *rbf_w,   /* [Nk][M] */
+                         const double *mu0, const double *step, const double *gamma, /* [Nk] */
+                         double lam, int boundary, int phi_mode,
+                         double *u_next, double *u_tilde_out /* may be NULL */) {
+    size_t N = (size_t)H * W;
+    double *v = (double *)malloc(sizeof(double) * N);
+    double *d = (double *)calloc(N, sizeof(double));
+    double *t = (double *)malloc(sizeof(double) * N);
+    double *kbar = (double *)malloc(sizeof(double) * m * m);
+    for (int i = 0; i < Nk; ++i) {
+        const double *k = filters + (size_t)i * m * m;
+        oracle_conv2d_sym(H, W, u, m, k, v);                      /* v = k_i * u     */
+#pragma omp parallel for schedule(static)
+        for (long p = 0; p < (long)N; ++p)                        /* w = phi_i(v)    */
+            v[p] = phi_mode == 1 ? rbf_w[(size_t)i * M] * v[p]
+                                 : oracle_phi(M, rbf_w + (size_t)i * M, mu0[i], step[i], gamma[i], v[p]);
+        if (boundary == 1) {
+            oracle_conv2d_adjoint(H, W, v, m, k, t);              /* t = K_i^T w     */
+        } else {
+            oracle_rot180(m, k, kbar);
+            oracle_conv2d_sym(H, W, v, m, kbar, t);               /* t = kbar_i * w  */
+        }
+        for (size_t p = 0; p < N; ++p) d[p] += t[p];
+    }
+    for (size_t p = 0; p < N; ++p) {
+        double ut = u[p] - d[p];                                  /* tau = 1, l.333  */
+        if (u_tilde_out) u_tilde_out[p] = ut;
+        u_next[p] = oracle_prox(ut, lam, f[p]);
+    }
+    free(v); free(d); free(t); free(kbar);
+}
+
+/* Inference pass: u_0 = f (P l.136 "u_0 = I_0", l.148 "I_0 ... can be set as f"),
+ * then T stages of Eq.13.  No floor or clamp (P never clamps; S l.228). */
+EXPORT void oracle_denoise(int H, int W, const double *f, int T, int Nk, int m, int M,
+                           const double *filters, const double *rbf_w, const double *mu0,
+                           const double *step, const double *gamma, const double *lam,
+                           int boundary, int phi_mode, double *u_out) {
+    size_t N = (size_t)H * W;
+    double *a = (double *)malloc(sizeof(double) * N);
+    double *b = (double *)malloc(sizeof(double) * N);
+    memcpy(a, f, sizeof(double) * N);
+    for (int s = 0; s < T; ++s) {
+        oracle_stage(H, W, a, f, Nk, m, M,
+                     filters + (size_t)s * Nk * m * m, rbf_w + (size_t)s * Nk * M,
+                     mu0 + (size_t)s * Nk, step + (size_t)s * Nk, gamma + (size_t)s * Nk,
+                     lam[s], boundary, phi_mode, b, NULL);
+        double *tmp = a; a = b; b = tmp;
+    }
+    memcpy(u_out, a, sizeof(double) * N);
+    free(a); free(b);
+}

@@ -1,0 +1,380 @@
+"""Pins P1-P16: tie the double-precision oracle to what the paper
+and the mathematics fix, independently of the oracle's own code.
+
+Every check compares the oracle with something it does not share code with:
+golden values (tests/golden, cited), dense brute-force matrices built here from
+numpy.pad index maps, scipy routines, closed forms, scalar minimisation of
+Eq.10, and structural invariants of Eq.13.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import scipy.integrate
+import scipy.ndimage
+import scipy.optimize
+import scipy.signal
+
+import oracle
+from oracle.fp32_emulation import denoise_f32
+from synth import Model, make_model, make_problem, zero_model
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    rows = []
+    with open(os.path.join(GOLD, name)) as fh:
+        for line in fh:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                rows.append([float(x) for x in line.split()])
+    return rows
+
+
+def _dense_conv_matrix(H, W, k):
+    """K with (K x)(p,q) = sum_{a,b} k[a+r][b+r] x_ext(p-a, q-b), x_ext the half-sample
+    symmetric extension, built from numpy.pad(mode='symmetric') of an index map."""
+    m = k.shape[0]
+    r = m // 2
+    idx = np.pad(np.arange(H * W).reshape(H, W), r, mode="symmetric")
+    K = np.zeros((H * W, H * W))
+    for p in range(H):
+        for q in range(W):
+            for a in range(-r, r + 1):
+                for b in range(-r, r + 1):
+                    K[p * W + q, idx[p - a + r, q - b + r]] += k[a + r, b + r]
+    return K
+
+
+def _rng(seed=0):
+    return np.random.default_rng(seed)
+
+
+# ---------------------------------------------------------------- P1 rot180
+def test_p1_rot180_golden_and_involution():
+    rows = _golden("rot180_3x3.txt")
+    k, expect = np.array(rows[:3]), np.array(rows[3:])
+    assert np.array_equal(oracle.rot180(k), expect)
+    for m in (3, 5, 7):
+        k = _rng(m).standard_normal((m, m))
+        assert np.array_equal(oracle.rot180(oracle.rot180(k)), k)
+        assert np.array_equal(oracle.rot180(k), np.rot90(k, 2))
+
+
+# ---------------------------------------------------------------- P2 conv
+@pytest.mark.parametrize("H,W,m", [(5, 5, 3), (7, 11, 5), (12, 9, 7), (16, 20, 7), (3, 4, 7)])
+def test_p2_conv_dense_bruteforce(H, W, m):
+    rng = _rng(H * 100 + W + m)
+    x, k = rng.standard_normal((H, W)), rng.standard_normal((m, m))
+    K = _dense_conv_matrix(H, W, k)
+    got = oracle.conv2d_sym(x, k).ravel()
+    assert np.max(np.abs(got - K @ x.ravel())) < 1e-12
+
+
+@pytest.mark.parametrize("m", [3, 5, 7, 9])
+def test_p2_conv_matches_scipy_reflect(m):
+    rng = _rng(m)
+    x, k = rng.standard_normal((40, 33)), rng.standard_normal((m, m))
+    ref = scipy.ndimage.convolve(x, k, mode="reflect")  # 'reflect' = half-sample symmetric
+    assert np.max(np.abs(oracle.conv2d_sym(x, k) - ref)) < 1e-12
+
+
+def test_p2_conv_delta_and_constant():
+    rng = _rng(1)
+    x = rng.standard_normal((13, 17))
+    d = np.zeros((5, 5))
+    d[2, 2] = 1.0
+    assert np.array_equal(oracle.conv2d_sym(x, d), x)
+    k = rng.standard_normal((7, 7))
+    c = np.full((10, 12), 2.5)
+    assert np.max(np.abs(oracle.conv2d_sym(c, k) - 2.5 * k.sum())) < 1e-12
+    # a shifted delta is a shift (true convolution: output(p) = x(p - 1))
+    s = np.zeros((3, 3))
+    s[1, 2] = 1.0  # offset b = +1
+    y = oracle.conv2d_sym(x, s)
+    assert np.array_equal(y[:, 1:], x[:, :-1])
+    assert np.array_equal(y[:, 0], x[:, 0])  # mirror: x(-1) = x(0)
+
+
+# ---------------------------------------------------------------- P3 adjoint (R2)
+@pytest.mark.parametrize("m", [3, 5, 7, 9])
+def test_p3_adjoint_inner_product(m):
+    for draw in range(20):
+        rng = _rng(1000 * m + draw)
+        H, W = rng.integers(m, 24, size=2)
+        x, y = rng.standard_normal((H, W)), rng.standard_normal((H, W))
+        k = rng.standard_normal((m, m))
+        lhs = np.sum(oracle.conv2d_sym(x, k) * y)
+        rhs = np.sum(x * oracle.conv2d_adjoint(y, k))
+        assert abs(lhs - rhs) < 1e-10 * max(1.0, abs(lhs))
+
+
+def test_p3_adjoint_is_dense_transpose():
+    rng = _rng(3)
+    H, W, m = 9, 8, 5
+    y, k = rng.standard_normal((H, W)), rng.standard_normal((m, m))
+    K = _dense_conv_matrix(H, W, k)
+    assert np.max(np.abs(oracle.conv2d_adjoint(y, k).ravel() - K.T @ y.ravel())) < 1e-12
+
+
+# ---------------------------------------------------------------- P4 R1 vs R2
+@pytest.mark.parametrize("m", [3, 7])
+def test_p4_r1_r2_differ_only_in_outer_band(m):
+    r = m // 2
+    rng = _rng(40 + m)
+    y, k = rng.standard_normal((30, 26)), rng.standard_normal((m, m))
+    r1 = oracle.conv2d_sym(y, oracle.rot180(k))
+    r2 = oracle.conv2d_adjoint(y, k)
+    assert np.max(np.abs(r1[r:-r, r:-r] - r2[r:-r, r:-r])) < 1e-12
+    # and R1's interior is the correlation with k (scipy)
+    corr = scipy.ndimage.correlate(y, k, mode="reflect")
+    assert np.max(np.abs(r1 - corr)) < 1e-12
+    band = np.ones_like(y, bool)
+    band[r:-r, r:-r] = False
+    assert np.max(np.abs(r1 - r2)[band]) > 1e-3  # they genuinely differ at the edge
+
+
+# ---------------------------------------------------------------- P5 phi
+def test_p5_phi_golden():
+    for row in _golden("phi_examples.txt"):
+        M = int(row[0])
+        mu0, step, gamma, z, expect = row[1:6]
+        w = np.array(row[6:6 + M])
+        got = oracle.phi(w, mu0, step, gamma, z)
+        assert abs(got - expect) < 1e-14, (row, got)
+
+
+def test_p5_phi_linearity_bound_and_integral():
+    rng = _rng(5)
+    M, mu0, step, gamma = 63, -12.0, 24.0 / 62, 24.0 / 62
+    w1, w2 = rng.standard_normal(M), rng.standard_normal(M)
+    z = rng.uniform(-15, 15, size=50)
+    p1, p2 = oracle.phi(w1, mu0, step, gamma, z), oracle.phi(w2, mu0, step, gamma, z)
+    assert np.max(np.abs(oracle.phi(w1 + 2 * w2, mu0, step, gamma, z) - (p1 + 2 * p2))) < 1e-12
+    assert np.all(np.abs(p1) <= np.abs(w1).sum() + 1e-12)
+    # Gaussian mixture integral: int phi = sqrt(2 pi) gamma sum_j w_j  (quadrature, independent)
+    val, _ = scipy.integrate.quad(lambda t: float(oracle.phi(w1, mu0, step, gamma, t)),
+                                  -40, 40, limit=400)
+    assert abs(val - math.sqrt(2 * math.pi) * gamma * w1.sum()) < 1e-8
+
+
+def test_p5_phi_centre_indexing():
+    """One-hot weights on centre j peak exactly at mu0 + j*step (catches index/spacing errors)."""
+    M, mu0, step, gamma = 7, -3.0, 1.0, 0.4
+    for j in range(M):
+        w = np.zeros(M)
+        w[j] = 1.0
+        assert oracle.phi(w, mu0, step, gamma, mu0 + j * step) == 1.0
+        # half maximum at distance gamma*sqrt(2 ln 2)
+        h = gamma * math.sqrt(2 * math.log(2))
+        assert abs(oracle.phi(w, mu0, step, gamma, mu0 + j * step + h) - 0.5) < 1e-14
+
+
+# ---------------------------------------------------------------- P6 prox
+def test_p6_prox_golden():
+    for ut, lam, f, expect in _golden("prox_examples.txt"):
+        assert abs(oracle.prox(ut, lam, f) - expect) < 1e-14
+
+
+def test_p6_prox_optimality_and_minimisation():
+    rng = _rng(6)
+    ut = rng.uniform(-5, 10, 1000)
+    lam = rng.uniform(0.1, 3, 1000)
+    f = rng.integers(0, 15, 1000).astype(float)
+    u = oracle.prox(ut, lam, f)
+    pos = f > 0
+    assert np.all(u[pos] > 0)  # P l.323-324 positivity
+    assert np.all(u >= 0)
+    # first-order optimality of Eq.10/Eq.11 objective: (u - ut) + lam (1 - f/u) = 0
+    g = (u[pos] - ut[pos]) + lam[pos] * (1 - f[pos] / u[pos])
+    assert np.max(np.abs(g) / (1 + np.abs(ut[pos]))) < 1e-10
+    assert np.allclose(u[~pos], np.maximum(ut[~pos] - lam[~pos], 0.0), atol=0, rtol=0)
+    # direct scalar minimisation of (u - ut)^2/2 + lam (u - f log u) over u > 0
+    for i in range(0, 1000, 10):
+        if f[i] == 0:
+            continue
+        obj = lambda x: 0.5 * (x - ut[i]) ** 2 + lam[i] * (x - f[i] * math.log(x))
+        res = scipy.optimize.minimize_scalar(obj, bounds=(1e-12, 50), method="bounded",
+                                             options={"xatol": 1e-12})
+        assert abs(res.x - u[i]) < 1e-6
+
+
+def test_p6_prox_monotone():
+    ut = np.linspace(-6, 6, 2001)
+    for lam, f in [(0.5, 0.0), (1.0, 1.0), (2.0, 7.0)]:
+        u = oracle.prox(ut, lam, f)
+        assert np.all(np.diff(u) >= 0)
+
+
+# ---------------------------------------------------------------- P7/P8 zero diffusion
+@pytest.mark.parametrize("zero", ["filters", "weights"])
+def test_p7_p8_zero_diffusion_is_pure_reaction(zero):
+    p = make_problem(1)
+    f = p.f[0]
+    m = zero_model(4, 8, 3, 63, zero, lam=[1.0, 0.5, 2.0, 1.3])
+    # from u0 = f the output is exactly f (prox fixed point u = f, S l.182)
+    assert np.array_equal(oracle.denoise(f, m), f.astype(np.float64))
+    # from another u0 one stage is the scalar prox
+    u0 = _rng(8).uniform(0, 6, f.shape)
+    expect = oracle.prox(u0, 1.0, f)
+    assert np.array_equal(oracle.stage(u0, f, m, 0), expect)
+
+
+# ---------------------------------------------------------------- P9 flat input
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_p9_flat_image_is_fixed_under_r1(cfg):
+    p = make_problem(cfg)
+    c = 3.0
+    f = np.full((23, 31), c)
+    u = oracle.denoise(f, p.model)
+    # zero-mean fp32 filters: sum k ~ 1e-7, so flat stays flat to ~1e-8 (P l.309-311)
+    assert np.max(np.abs(u - c)) < 1e-5
+    if cfg == 1:
+        u2 = oracle.denoise(f, p.model, boundary=oracle.BOUNDARY_ADJOINT)
+        assert np.max(np.abs(u2 - c)) > 1e-3  # K^T 1 != 0 at the edges under R2
+
+
+# ---------------------------------------------------------------- P10 linear phi
+def test_p10_linear_phi_is_linear_diffusion_dense():
+    rng = _rng(10)
+    H, W, Nk, m = 11, 9, 4, 5
+    mdl = make_model(rng, 1, Nk, m, 63, 4.0)
+    c = rng.uniform(-0.5, 0.5, Nk)
+    mdl.rbf_w[0, :, 0] = c
+    c = mdl.rbf_w[0, :, 0].astype(np.float64)  # the oracle sees the fp32-rounded slopes
+    u = rng.uniform(0, 4, (H, W))
+    f = rng.integers(0, 6, (H, W)).astype(float)
+    _, ut = oracle.stage(u, f, mdl, 0, phi_mode=oracle.PHI_LINEAR, return_u_tilde=True)
+    A = np.eye(H * W)
+    for i in range(Nk):
+        k = mdl.filters[0, i].astype(np.float64)
+        A -= c[i] * _dense_conv_matrix(H, W, np.rot90(k, 2)) @ _dense_conv_matrix(H, W, k)
+    assert np.max(np.abs(ut.ravel() - A @ u.ravel())) < 1e-12
+    # interior equals one convolution with h = sum_i c_i kbar_i * k_i, a (2m-1)^2 kernel
+    h = sum(c[i] * scipy.signal.convolve2d(np.rot90(mdl.filters[0, i].astype(float), 2),
+                                           mdl.filters[0, i].astype(float)) for i in range(Nk))
+    interior = u - scipy.signal.convolve2d(u, h, mode="same")
+    R = 2 * (m // 2)
+    assert np.max(np.abs(ut[R:-R, R:-R] - interior[R:-R, R:-R])) < 1e-12
+    # and u_next is the prox of u_tilde
+    un = oracle.stage(u, f, mdl, 0, phi_mode=oracle.PHI_LINEAR)
+    assert np.max(np.abs(un - oracle.prox(ut, mdl.lam[0], f))) < 1e-14
+
+
+def test_stage_rbf_composition_with_shift_filters():
+    """Delta/shift filters make each response a (mirrored) shift of u, so u_tilde is
+    u - phi_0(u) - shift^{-1}(phi_1(shift u)) in the interior; distinct phi params per
+    filter catch index mix-ups between filters and their RBF grids."""
+    rng = _rng(11)
+    mdl = make_model(rng, 1, 2, 3, 63, 4.0)
+    mdl.filters[...] = 0
+    mdl.filters[0, 0, 1, 1] = 1.0   # delta
+    mdl.filters[0, 1, 1, 2] = 1.0   # v_1(p,q) = u(p, q-1)
+    mdl.rbf_mu0[0] = [-3.0, -5.0]
+    mdl.rbf_step[0] = [6.0 / 62, 10.0 / 62]
+    mdl.rbf_gamma[0] = [0.2, 0.3]
+    u = rng.uniform(0, 3, (10, 12))
+    f = np.ones_like(u)
+    _, ut = oracle.stage(u, f, mdl, 0, return_u_tilde=True)
+    g = lambda i, z: oracle.phi(mdl.rbf_w[0, i], mdl.rbf_mu0[0, i], mdl.rbf_step[0, i],
+                                mdl.rbf_gamma[0, i], z)
+    w0 = g(0, u)
+    v1 = np.empty_like(u)
+    v1[:, 1:] = u[:, :-1]
+    v1[:, 0] = u[:, 0]
+    w1 = g(1, v1)
+    expect = u - w0
+    expect[:, :-1] -= w1[:, 1:]   # kbar_1 * w_1 = w_1(p, q+1)
+    assert np.max(np.abs(ut[:, :-1] - expect[:, :-1])) < 1e-12
+
+
+# ---------------------------------------------------------------- P11 equivariance
+def test_p11_flip_and_transpose_equivariance():
+    p = make_problem(1)
+    f = p.f[0][:20, :24].astype(np.float64)
+    mdl = p.model
+    u = oracle.denoise(f, mdl)
+    rot = Model(np.ascontiguousarray(mdl.filters[:, :, ::-1, ::-1]), mdl.rbf_w, mdl.rbf_mu0,
+                mdl.rbf_step, mdl.rbf_gamma, mdl.lam)
+    u_rot = oracle.denoise(np.rot90(f, 2), rot)
+    assert np.max(np.abs(u_rot - np.rot90(u, 2))) < 1e-12
+    tr = Model(np.ascontiguousarray(np.swapaxes(mdl.filters, 2, 3)), mdl.rbf_w, mdl.rbf_mu0,
+               mdl.rbf_step, mdl.rbf_gamma, mdl.lam)
+    u_tr = oracle.denoise(np.ascontiguousarray(f.T), tr)
+    assert np.max(np.abs(u_tr - u.T)) < 1e-12
+
+
+# ---------------------------------------------------------------- P12 locality
+def test_p12_dependency_cone_window():
+    p = make_problem(2)
+    f = p.f[0][:128, :160]
+    full = oracle.denoise(f, p.model)
+    R = 2 * (p.model.k // 2) * p.model.T
+    for (y0, y1, x0, x1) in [(60, 70, 70, 90), (0, 8, 100, 160), (120, 128, 0, 5)]:
+        win = oracle.denoise_window(f, p.model, y0, y1, x0, x1)
+        assert np.max(np.abs(win - full[y0:y1, x0:x1])) < 1e-12
+    # a margin one pixel short of 2rT is not enough in general
+    cy0, cx0 = 60 - (R - 1), 70 - (R - 1)
+    short = oracle.denoise(f[cy0:70 + R - 1, cx0:90 + R - 1], p.model)
+    assert np.max(np.abs(short[R - 1:R - 1 + 10, R - 1:R - 1 + 20] - full[60:70, 70:90])) > 0
+
+
+# ---------------------------------------------------------------- P13/P14 fold, determinism, batch
+def test_p13_composition_and_determinism():
+    p = make_problem(1)
+    f = p.f[0]
+    u = f.astype(np.float64)
+    for t in range(p.model.T):
+        u = oracle.stage(u, f, p.model, t)
+    full = oracle.denoise(f, p.model)
+    assert np.array_equal(u, full)
+    assert np.array_equal(oracle.denoise(f, p.model), full)
+
+
+def test_p14_batch_independence():
+    p = make_problem(1)
+    f = p.f[0]
+    g = np.flipud(f).copy()
+    a = oracle.denoise(np.stack([f, g]), p.model)
+    b = oracle.denoise(np.stack([g, f]), p.model)
+    assert np.array_equal(a[0], b[1]) and np.array_equal(a[1], b[0])
+
+
+# ---------------------------------------------------------------- P16 fp32 noise floor
+# Gate: fp32 drift <= P16_GATE x tolerance, i.e. >= 5x headroom for the kernel's own
+# (different) fp32 rounding order.  Measured: 0.006-0.10 x tol.
+P16_GATE = 0.2
+
+
+@pytest.mark.parametrize("cfg,window", [(1, None), (2, (100, 50, 96)), (3, (100, 50, 80)),
+                                        (5, (1000, 1000, 64)), (5, (8128, 100, 64))])
+def test_p16_fp32_noise_floor_gate(cfg, window):
+    """A faithful fp32 evaluation stays well inside the parity tolerance of the double
+    oracle, so the configs are well-conditioned for an fp32 kernel."""
+    p = make_problem(cfg)
+    f, peak = p.f[0], float(p.peaks[0])
+    if window:
+        y, x, n = window
+        f = f[y:y + n, x:x + n]
+    u64 = oracle.denoise(f, p.model)
+    u32 = denoise_f32(f, p.model)
+    assert np.max(np.abs(u32 - u64)) <= P16_GATE * 1e-4 * peak
+
+
+def test_p16_fp32_noise_floor_c4_peaks():
+    """C4's shared model across its five peaks (first five images: one per peak)."""
+    p = make_problem(4)
+    for b in range(5):
+        f = p.f[b][200:260, 300:360]
+        u64 = oracle.denoise(f, p.model)
+        u32 = denoise_f32(f, p.model)
+        assert np.max(np.abs(u32 - u64)) <= P16_GATE * 1e-4 * float(p.peaks[b]), b
+
+
+# ---------------------------------------------------------------- PSNR helper
+def test_psnr_golden():
+    (peak, off, expect), = _golden("psnr_examples.txt")
+    ref = np.full((8, 8), 100.0)
+    assert abs(oracle.psnr(ref + off, ref, peak) - expect) < 1e-9
