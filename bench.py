@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark: TNRD/TRDPD Poisson-denoising inference on B200 (BASELINE.json metric
+"denoised MPix/s (48x7x7, T=8, fp32) at 1/2/4/8 B200; % of FP32 roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4|5|3] [--impl ours|reference]
+
+A step is one full inference pass (T = 8 fused stage launches) over the
+workload: by default BASELINE.json configs[3] (C4: 256 independent 512x512
+images, 48 7x7 filters, 63 RBFs, T = 8), its images sharded over the ranks
+(no data-path collective; total fixed -> "strong" scaling).  --config 5 runs
+C5 (one 8192^2 image) as row slabs with the per-stage NCCL halo exchange.
+
+For N > 1 launch with torchrun (one process per GPU); rank 0 prints one JSON
+line.  Timing: CUDA events on the launching stream, barrier + synchronize on
+both sides, max over ranks.  Inputs (~0.8 GB resident per step) exceed the
+126 MB L2, so no flush is needed.  See DESIGN.md §8.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+F_ALG = lambda Nk, k, M: 4 * Nk * k * k + 2 * Nk * M + 10  # flop / pixel / stage
+METRIC = "denoised MPix/s (48x7x7, T=8, fp32) at 1/2/4/8 B200; % of FP32 roofline"
+
+
+def fp32_peak_tflops(n_sm: int, mhz: float) -> float:
+    """FP32 FMA roofline: n_SM x 128 lanes x 2 flop x clock."""
+    return n_sm * 128 * 2 * mhz * 1e6 / 1e12
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the double-precision oracle (oracle/, as it stands) timed on
+    the host cores on bounded samples of the same workload."""
+    if rank != 0:
+        return 0
+    import oracle
+    from synth import make_problem
+    cfg = args.config
+    p = make_problem(cfg)
+    cores = oracle.num_threads()
+    # calibrate: one 32x32 crop, then size each step's sample to ~2 s
+    f0 = p.f[0]
+    t = time.perf_counter()
+    oracle.denoise(f0[:32, :32], p.model)
+    per_px = (time.perf_counter() - t) / (32 * 32)
+    side = int(np.clip(np.sqrt(2.0 / max(per_px, 1e-9)), 32, min(f0.shape)))
+    rng = np.random.default_rng(0)
+    times = []
+    for s in range(args.warmup + args.steps):
+        b = s % p.f.shape[0]
+        y = int(rng.integers(0, p.f.shape[1] - side + 1))
+        x = int(rng.integers(0, p.f.shape[2] - side + 1))
+        t = time.perf_counter()
+        oracle.denoise(p.f[b][y:y + side, x:x + side], p.model)
+        dt = time.perf_counter() - t
+        if s >= args.warmup:
+            times.append(dt)
+    mpix = side * side / 1e6
+    value = mpix * len(times) / sum(times)
+    sample = f"{side}x{side} window of a {p.cfg['name']} image per step (T={p.model.T}, Nk={p.model.Nk}, " \
+             f"k={p.model.k}, M={p.model.M}), double precision, OpenMP over rows"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(p, world, args),
+        "cpu_baseline": {"value": value, "unit": "MPix/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "MPix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(p, world, args):
+    c = p.cfg
+    return {"workload": f"{c['name']}: {c['B']}x{c['H']}x{c['W']} fp32, peaks {c['peaks']}, T={c['T']}, "
+                        f"Nk={c['Nk']}, k={c['k']}, M={c['M']} (BASELINE.json configs[{args.config - 1}])",
+            "batch": c["B"], "H": c["H"], "W": c["W"], "T": c["T"], "Nk": c["Nk"], "k": c["k"], "M": c["M"],
+            "parallelism": ("batch-shard" if args.config != 5 else "row-slab+nccl-halo") + f"x{world}",
+            "l2": "no flush: per-step working set (f, u, scratch) > 126 MB L2",
+            "flop_per_px_stage": F_ALG(c["Nk"], c["k"], c["M"])}
+
+
+def cpu_baseline(p, budget_s=12.0):
+    """The oracle on a bounded sample (rank 0, N = 1 only)."""
+    import oracle
+    f0 = p.f[0]
+    t = time.perf_counter()
+    oracle.denoise(f0[:32, :32], p.model)
+    per_px = (time.perf_counter() - t) / 1024
+    side = int(np.clip(np.sqrt(budget_s / max(per_px, 1e-9)), 32, min(f0.shape)))
+    y, x = (f0.shape[0] - side) // 2, (f0.shape[1] - side) // 2
+    t = time.perf_counter()
+    oracle.denoise(f0[y:y + side, x:x + side], p.model)
+    dt = time.perf_counter() - t
+    return {"value": side * side / 1e6 / dt, "unit": "MPix/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"one {side}x{side} window of image 0 (T={p.model.T}, full model), double precision, "
+                      f"{dt:.1f} s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4, choices=[3, 4, 5])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1510_02930_b200 as P
+    from synth import make_problem
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    p = make_problem(args.config)
+    model = p.model
+    B, H, W = p.f.shape
+    eng = P.TNRD(model, device=local)
+    stream = torch.cuda.current_stream()
+
+    if args.config == 5:
+        # row slabs, NCCL halo exchange per stage
+        r0, r1 = H * rank // world, H * (rank + 1) // world
+        f_dev = torch.from_numpy(p.f[0, r0:r1]).to(dev)
+        u_dev = torch.empty_like(f_dev)
+        if world > 1:
+            uid = P.tnrd_nccl_unique_id() if rank == 0 else bytes(128)
+            obj = [uid]
+            dist.broadcast_object_list(obj, src=0)
+            P.tnrd_comm_init(eng.h, obj[0], rank, world)
+
+        def step():
+            if world > 1:
+                P.tnrd_denoise_slab(eng.h, f_dev, u_dev, H, r0, 0.1)
+            else:
+                P.tnrd_denoise(eng.h, f_dev[None], u_dev[None])
+        px_rank = (r1 - r0) * W
+        shard = (r0, r1)
+    else:
+        b0, b1 = B * rank // world, B * (rank + 1) // world
+        f_dev = torch.from_numpy(p.f[b0:b1]).to(dev)
+        u_dev = torch.empty_like(f_dev)
+        peaks = p.peaks[b0:b1]
+
+        def step():
+            P.tnrd_denoise(eng.h, f_dev, u_dev, peaks)
+        px_rank = (b1 - b0) * H * W
+        shard = (b0, b1)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    n_launch0 = P.tnrd_launch_count(eng.h)
+    P.tnrd_set_profiling(eng.h, True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = P.tnrd_launch_count(eng.h) - n_launch0
+    launch_ms = P.tnrd_get_launch_times(eng.h)
+    P.tnrd_set_profiling(eng.h, False)
+    clocks = clk.summary()
+    t = torch.tensor([ms, float(launches), float(np.mean(launch_ms)) if len(launch_ms) else 0.0], device=dev)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        ms, launches = float(tmax[0]), int(tsum[1])
+        mean_launch_ms = float(tmax[2])
+    else:
+        mean_launch_ms = float(t[2])
+    ms_per_step = ms / args.steps
+    total_px = B * H * W
+    value = total_px / 1e6 / (ms_per_step / 1e3)
+
+    # ---- e2e: public host entry point, pinned host buffers, copies inside the timed region
+    e2e = None
+    if not args.no_e2e and args.config != 5:
+        f_host = torch.from_numpy(p.f[shard[0]:shard[1]]).pin_memory()
+        u_host = torch.empty_like(f_host).pin_memory()
+        nb = shard[1] - shard[0]
+        P.tnrd_denoise_host_ptr(eng.h, f_host.data_ptr(), u_host.data_ptr(), nb, H, W)  # warm
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k_e2e = max(1, min(args.steps, 5))
+        e0.record(stream)
+        for _ in range(k_e2e):
+            P.tnrd_denoise_host_ptr(eng.h, f_host.data_ptr(), u_host.data_ptr(), nb, H, W)
+        e1.record(stream)
+        barrier()
+        ems = torch.tensor([e0.elapsed_time(e1) / k_e2e], device=dev)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e2e = {"value": total_px / 1e6 / (float(ems[0]) / 1e3), "unit": "MPix/s",
+               "h2d_bytes_per_step": int(f_host.numel() * 4), "d2h_bytes_per_step": int(u_host.numel() * 4),
+               "steps": k_e2e, "entry_point": "tnrd_denoise_host"}
+
+    if rank == 0:
+        props = torch.cuda.get_device_properties(dev)
+        n_sm = props.multi_processor_count
+        max_mhz = (clocks or {}).get("sm_max_mhz") or 1965.0
+        peak = fp32_peak_tflops(n_sm, max_mhz)
+        flop_launch = F_ALG(model.Nk, model.k, model.M) * px_rank
+        achieved = flop_launch / (mean_launch_ms / 1e3) / 1e12 if mean_launch_ms > 0 else None
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tf):
+            try:
+                traffic = json.load(open(tf)).get(f"C{args.config}")
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(p, world, args),
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": "stage_kernel (one fused TNRD stage)",
+                         "flop_per_launch": flop_launch, "mean_launch_ms": mean_launch_ms,
+                         "peak_source": f"derived: {n_sm} SM x 128 FP32 lanes x 2 x {max_mhz:.0f} MHz "
+                                        "(MEASURED_PEAKS.json has no FP32 figure)"},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "e2e": e2e,
+            "device": props.name,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(p)
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,202 @@
+/*
+ * tnrd.h -- C ABI of libtnrd.so: B200-native (sm_100a) inference pass of the
+ * trained nonlinear reaction-diffusion Poisson denoiser TRDPD (Feng & Chen,
+ * arXiv 1510.02930).  "P l.N" cites PAPER.md, "S l.N" SPEC.md.
+ *
+ * The operation (P Eq.13, l.326-333; Eq.3 l.134-149):
+ *
+ *     u_0 = f                                         (P l.136, l.148)
+ *     for t = 0..T-1:
+ *        ut      = u_t - sum_{i<N_k} kbar_i^t * phi_i^t(k_i^t * u_t)   (tau = 1, l.333)
+ *        u_{t+1} = (ut - lam_t + sqrt((ut - lam_t)^2 + 4 lam_t f)) / 2 (Eq.12, l.318-322)
+ *
+ *   "*" is true 2-D convolution with the symmetric (half-sample mirror)
+ *   boundary (P l.302; S l.73), kbar_i the 180-degree rotation of k_i
+ *   (P l.143-144), and phi_i^t(z) = sum_{j<M} w_ij exp(-(z - mu_ij)^2 / (2 gamma_i^2)),
+ *   mu_ij = mu0_i + j*step_i: a Gaussian-RBF mixture on uniform centres
+ *   (P l.145-146 leaves phi free; S l.104-107; BASELINE.json north_star).
+ *
+ * Arithmetic is IEEE fp32 on the device (DESIGN.md §5 states the error budget
+ * against the double-precision oracle: max|du| <= 1e-4 * peak).
+ *
+ * Conventions for every entry point:
+ *   - images are row-major fp32, element (b, y, x) at ptr[b*H*ld + y*ld + x];
+ *     ld (in floats) >= W;
+ *   - pointers named *_dev are device pointers on the handle's device; *_host
+ *     are host pointers (pinned or pageable);
+ *   - calls are stream-ordered on `cuda_stream` (a cudaStream_t, NULL = legacy
+ *     default stream) and return after enqueueing, except where stated;
+ *   - errors are reported by return code only; nothing aborts or throws across
+ *     the ABI; tnrd_last_error(h) returns a message for the last failure on h.
+ *   - a handle is not thread-safe: one host thread at a time per handle.
+ */
+#ifndef TNRD_H_
+#define TNRD_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TNRD_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define TNRD_API __attribute__((visibility("default")))
+#else
+#define TNRD_API
+#endif
+
+typedef struct tnrd_handle tnrd_handle;
+
+typedef enum {
+    TNRD_OK = 0,
+    TNRD_EINVAL = 1,       /* invalid argument (value, size, alignment, aliasing)       */
+    TNRD_ESTATE = 2,       /* handle state: stage params unset, comm not initialised    */
+    TNRD_ENOMEM = 3,       /* device or host allocation failed                          */
+    TNRD_ECUDA = 4,        /* CUDA runtime error (message in tnrd_last_error)           */
+    TNRD_ENCCL = 5,        /* NCCL error or NCCL library not loadable                   */
+    TNRD_EUNSUPPORTED = 6  /* valid request this build does not implement               */
+} tnrd_status;
+
+typedef enum {
+    /* R1 (default): explicit rotated-kernel convolution of the symmetrically
+     * extended phi response, P l.302-311 ("revise the above formulation as
+     * explicit convolutions", nabla F = sum kbar_i * phi_i(k_i * u)). */
+    TNRD_BC_SYMMETRIC_EXPLICIT = 0,
+    /* R2: exact transpose K_i^T of the symmetric-boundary convolution
+     * (P l.295-301; S l.57-65).  Differs from R1 only in the outer r = k/2 pixels. */
+    TNRD_BC_SYMMETRIC_ADJOINT = 1
+} tnrd_boundary;
+
+typedef enum {
+    TNRD_PHI_EXACT = 0,    /* exact RBF sum (all terms above 2^-126 of their weight)   */
+    TNRD_PHI_TABLE = 1     /* tabulated phi -- not in this build: TNRD_EUNSUPPORTED    */
+} tnrd_phi_mode;
+
+/* Model shape.  T >= 1 stages, n_filters = N_k >= 1 (P l.423: N_k = m^2 - 1 if
+ * not specified, not enforced), ksize = m in {3, 5, 7}, n_rbf = M in [1, 256],
+ * device = CUDA ordinal. */
+typedef struct {
+    int T;
+    int n_filters;
+    int ksize;
+    int n_rbf;
+    int boundary;   /* tnrd_boundary */
+    int phi_mode;   /* tnrd_phi_mode */
+    int device;
+    int reserved;   /* must be 0 */
+} tnrd_desc;
+
+/* ABI version this library implements (TNRD_ABI_VERSION). */
+TNRD_API int tnrd_abi_version(void);
+
+/* Human-readable name of a status code (static string). */
+TNRD_API const char *tnrd_status_string(tnrd_status s);
+
+/* Create a handle for model shape *d on d->device.  *out receives the handle
+ * (owned by the caller, released with tnrd_destroy).  Allocates the device
+ * parameter store.  EINVAL: bad shape; EUNSUPPORTED: phi_mode TABLE or ksize
+ * outside {3,5,7}; ECUDA/ENOMEM: device errors.  Synchronous. */
+TNRD_API tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out);
+
+/* Set Theta^t = {lambda^t, phi_i^t, k_i^t} of stage t in [0, T) (P l.206-207).
+ * All pointers are HOST arrays, copied before return (the caller may free them):
+ *   filters   [N_k][m][m]  k_i^t row-major, the true-convolution kernel (kbar derived)
+ *   rbf_w     [N_k][M]     RBF weights w_ij
+ *   rbf_mu0   [N_k]        first centre mu_i0
+ *   rbf_step  [N_k]        centre spacing, > 0
+ *   rbf_gamma [N_k]        Gaussian width, > 0
+ *   lambda                 lambda^t > 0 (P Eq.13; not beta = log lambda, P l.415)
+ * EINVAL on non-finite values, step/gamma <= 0, lambda <= 0, t out of range.
+ * Derived fp32 evaluation constants are computed on the host in double.
+ * Synchronous (uploads with a blocking copy). */
+TNRD_API tnrd_status tnrd_set_stage_params(tnrd_handle *h, int t, const float *filters, const float *rbf_w,
+                                  const float *rbf_mu0, const float *rbf_step,
+                                  const float *rbf_gamma, float lambda);
+
+/* Denoise B images: u_dev <- u_T(f_dev) (P Eq.13 iterated, u_0 = f).
+ *   f_dev  device [B][H][ld]  Poisson counts (non-negative; not validated)
+ *   u_dev  device [B][H][ld]  output; must not alias f_dev (f is read every stage)
+ *   H, W >= ksize, B >= 1, ld >= W
+ *   peak   host [B] or NULL: per-image peak (P l.113-116), metadata only -- Eq.13
+ *          does not use it; it is validated (> 0, finite) when given.
+ * Scratch (one ping-pong image batch) is owned by the handle and grown on demand
+ * (synchronously, before enqueueing).  ESTATE if any stage is unset. */
+TNRD_API tnrd_status tnrd_denoise(tnrd_handle *h, const float *f_dev, float *u_dev, int B, int H, int W,
+                         long long ld, const float *peak, void *cuda_stream);
+
+/* End-to-end variant: f_host -> device -> denoise -> u_host, dense rows (ld = W).
+ * Host->device and device->host copies are enqueued on cuda_stream; the call
+ * synchronises the stream before returning (u_host is valid on return).
+ * Pinned host memory gives full PCIe/NVLink-C2C bandwidth. */
+TNRD_API tnrd_status tnrd_denoise_host(tnrd_handle *h, const float *f_host, float *u_host, int B, int H,
+                              int W, const float *peak, void *cuda_stream);
+
+/* Release the handle and everything it owns (device buffers, events, NCCL
+ * communicator).  NULL is a no-op.  Synchronises the device first. */
+TNRD_API tnrd_status tnrd_destroy(tnrd_handle *h);
+
+/* Message for the last failing call on h (or on the thread, if h is NULL).
+ * Valid until the next call on h. */
+TNRD_API const char *tnrd_last_error(const tnrd_handle *h);
+
+/* Number of kernels this handle has launched so far (evidence for the bench's
+ * gpu_launches count). */
+TNRD_API unsigned long long tnrd_launch_count(const tnrd_handle *h);
+
+/* ---------------- multi-GPU: row slabs of one large image ----------------
+ * Rank rho of N owns rows [row0, row0 + rows) of an H_global x W image.
+ * Before every stage each rank exchanges 2r = ksize-1 rows of u_t with each
+ * neighbour (ncclSend/ncclRecv on cuda_stream; DESIGN.md §6 reading C18: a
+ * fused stage depends on u within 2r rows).  f needs no exchange (the prox is
+ * pointwise).  Global top/bottom rows use the mirror; seams use neighbour data,
+ * so the result is bitwise equal to the single-GPU tnrd_denoise. */
+
+/* Fill id128 (128 bytes, host) with a fresh ncclUniqueId.  The caller
+ * broadcasts it to all ranks (e.g. with torch.distributed).  ENCCL if NCCL
+ * cannot be loaded (libnccl.so.2 is opened at run time; set TNRD_NCCL_LIB to
+ * its path to override the search). */
+TNRD_API tnrd_status tnrd_nccl_unique_id(void *id128);
+
+/* Create the handle's communicator (ncclCommInitRank) for rank of nranks.
+ * Collective across ranks; synchronous. */
+TNRD_API tnrd_status tnrd_comm_init(tnrd_handle *h, const void *id128, int rank, int nranks);
+
+/* Denoise this rank's slab.  f_slab_dev / u_slab_dev: device [rows][ld], the
+ * rank's own rows only.  rows >= ksize - 1 on every rank.  Enqueued on
+ * cuda_stream (NCCL calls included). */
+TNRD_API tnrd_status tnrd_denoise_slab(tnrd_handle *h, const float *f_slab_dev, float *u_slab_dev,
+                              int H_global, int W, int row0, int rows, long long ld, float peak,
+                              void *cuda_stream);
+
+/* Single-device emulation of the slab path: the image f_dev [H][ld] is split
+ * into nslabs row slabs processed with the same slab kernels and halo buffers,
+ * the halo exchange done with device-to-device copies instead of NCCL.  Used
+ * to test the partition on one GPU; result equals tnrd_denoise bitwise. */
+TNRD_API tnrd_status tnrd_denoise_slabs_loopback(tnrd_handle *h, const float *f_dev, float *u_dev, int H,
+                                        int W, long long ld, int nslabs, void *cuda_stream);
+
+/* ---------------- instrumentation and micro-parity ---------------- */
+
+/* Enable (1) / disable (0) per-launch CUDA-event timing of the stage kernels. */
+TNRD_API tnrd_status tnrd_set_profiling(tnrd_handle *h, int enable);
+
+/* After a profiled, completed tnrd_denoise: writes min(n, launches) per-launch
+ * durations in milliseconds to ms_out (host) and the count to *n_out.
+ * Synchronises on the recorded events. */
+TNRD_API tnrd_status tnrd_get_launch_times(tnrd_handle *h, float *ms_out, int n, int *n_out);
+
+/* Evaluate the device phi_i^t on n device values v_dev -> out_dev (same code
+ * as the stage kernel).  Stage t must be set. */
+TNRD_API tnrd_status tnrd_debug_phi(tnrd_handle *h, int t, int i, const float *v_dev, float *out_dev,
+                           long long n, void *cuda_stream);
+
+/* Evaluate the device Poisson prox (Eq.12, tau = 1) elementwise on n device
+ * values: out = prox_lambda(ut; f). */
+TNRD_API tnrd_status tnrd_debug_prox(const float *ut_dev, const float *f_dev, float lambda, float *out_dev,
+                            long long n, void *cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TNRD_H_ */

@@ -1,0 +1,669 @@
+// Host side of libtnrd.so: the C ABI declared in include/tnrd.h.
+//
+// Owns the per-stage parameter store, scratch buffers, the stage loop
+// (P Eq.13 iterated T times from u_0 = f), the
+// row-slab path with its per-stage halo exchange (NCCL P2P or a single-device
+// loopback), and per-launch CUDA-event instrumentation.  Every step of the
+// computation runs in the sm_100a kernels of tnrd_kernels.cu.
+#include "tnrd.h"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "nccl.h"
+#include "tnrd_internal.h"
+
+using tnrd::StageArgs;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct NcclApi {
+    bool loaded = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi &nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    const char *env = getenv("TNRD_NCCL_LIB");
+    void *lib = dlopen(env && *env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) {
+        api.why = std::string("cannot dlopen NCCL: ") + dlerror();
+        return api;
+    }
+#define TNRD_SYM(field, name)                                                   \
+    api.field = reinterpret_cast<decltype(api.field)>(dlsym(lib, name));        \
+    if (!api.field) { api.why = std::string("missing NCCL symbol ") + name; return api; }
+    TNRD_SYM(GetUniqueId, "ncclGetUniqueId");
+    TNRD_SYM(CommInitRank, "ncclCommInitRank");
+    TNRD_SYM(CommDestroy, "ncclCommDestroy");
+    TNRD_SYM(Send, "ncclSend");
+    TNRD_SYM(Recv, "ncclRecv");
+    TNRD_SYM(GroupStart, "ncclGroupStart");
+    TNRD_SYM(GroupEnd, "ncclGroupEnd");
+    TNRD_SYM(GetErrorString, "ncclGetErrorString");
+#undef TNRD_SYM
+    api.loaded = true;
+    return api;
+}
+
+}  // namespace
+
+struct tnrd_handle {
+    tnrd_desc d{};
+    int num_sms = 148;
+    int KK4 = 0;
+    int pstride_max = 0;
+    std::vector<int> pstride;     // per stage
+    std::vector<int> mode;        // per stage
+    std::vector<float> lambda;    // per stage
+    std::vector<char> is_set;     // per stage
+    float *d_params = nullptr;    // [T][Nk][pstride_max]
+    float *scratch = nullptr;
+    size_t scratch_bytes = 0;
+    float *e2e_f = nullptr, *e2e_u = nullptr;
+    size_t e2e_bytes = 0;
+    float *slab_buf[2] = {nullptr, nullptr};
+    size_t slab_bytes = 0;
+    std::vector<float *> lb_bufs;  // loopback slab buffers
+    size_t lb_bytes = 0;
+    ncclComm_t comm = nullptr;
+    int rank = 0, nranks = 1;
+    unsigned long long launches = 0;
+    bool profile = false;
+    std::vector<cudaEvent_t> ev;   // pairs (start, stop) per profiled launch
+    int ev_used = 0;
+    std::string err;
+};
+
+namespace {
+
+tnrd_status fail(tnrd_handle *h, tnrd_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (h) h->err = buf;
+    g_last_error = buf;
+    return s;
+}
+
+tnrd_status cuda_fail(tnrd_handle *h, cudaError_t e, const char *what) {
+    return fail(h, TNRD_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define TNRD_CUDA(h, call)                                          \
+    do {                                                            \
+        cudaError_t e_ = (call);                                    \
+        if (e_ != cudaSuccess) return cuda_fail((h), e_, #call);   \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+tnrd_status grow(tnrd_handle *h, float **p, size_t *have, size_t need, const char *what) {
+    if (*have >= need) return TNRD_OK;
+    if (*p) {
+        cudaDeviceSynchronize();
+        cudaFree(*p);
+        *p = nullptr;
+        *have = 0;
+    }
+    cudaError_t e = cudaMalloc(p, need);
+    if (e != cudaSuccess) return fail(h, TNRD_ENOMEM, "cudaMalloc(%zu) for %s: %s", need, what,
+                                      cudaGetErrorString(e));
+    *have = need;
+    return TNRD_OK;
+}
+
+tnrd_status check_ready(tnrd_handle *h) {
+    if (!h) return fail(nullptr, TNRD_EINVAL, "null handle");
+    for (int t = 0; t < h->d.T; ++t)
+        if (!h->is_set[t]) return fail(h, TNRD_ESTATE, "stage %d parameters are not set", t);
+    return TNRD_OK;
+}
+
+tnrd_status launch_one(tnrd_handle *h, int t, int tile, StageArgs &a, int B, cudaStream_t s) {
+    a.params = h->d_params + (size_t)t * h->d.n_filters * h->pstride_max;
+    a.Nk = h->d.n_filters;
+    a.pstride = h->pstride[t];
+    a.mode = h->mode[t];
+    a.boundary = h->d.boundary;
+    a.lambda = h->lambda[t];
+    if (h->profile) {
+        if ((size_t)h->ev_used + 2 > h->ev.size()) {
+            for (int k = 0; k < 64; ++k) {
+                cudaEvent_t e;
+                TNRD_CUDA(h, cudaEventCreate(&e));
+                h->ev.push_back(e);
+            }
+        }
+        TNRD_CUDA(h, cudaEventRecord(h->ev[h->ev_used], s));
+    }
+    cudaError_t e = tnrd::launch_stage(h->d.ksize, tile, a, B, s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "stage kernel launch");
+    if (h->profile) {
+        TNRD_CUDA(h, cudaEventRecord(h->ev[h->ev_used + 1], s));
+        h->ev_used += 2;
+    }
+    h->launches++;
+    return TNRD_OK;
+}
+
+// ---------------------------------------------------------------- slab machinery
+// A slab buffer holds rows [row0 - halo, row0 + rows + halo) of u (dense, ld = W).
+struct SlabExchange {
+    virtual ~SlabExchange() = default;
+    // Fill the top/bottom halo rows of slab `k`'s buffer `buf` for the coming stage.
+    virtual tnrd_status exchange(int k, float *buf) = 0;
+};
+
+tnrd_status run_slab(tnrd_handle *h, const float *f_slab, long long f_ld, float *u_slab, long long u_ld,
+                     int H, int W, int row0, int rows, float *buf0, float *buf1, SlabExchange &ex,
+                     int k, int stage, cudaStream_t s) {
+    // executes stage `stage` for slab k (stage 0 seeds the buffer with f first)
+    const int halo = h->d.ksize - 1;
+    float *in = (stage % 2 == 0) ? buf0 : buf1;
+    float *out_buf = (stage % 2 == 0) ? buf1 : buf0;
+    (void)in;
+    StageArgs a{};
+    a.u_in = {in, W, 0, row0 - halo};
+    a.f = {f_slab, f_ld, 0, row0};
+    const bool last = stage == h->d.T - 1;
+    if (last) {
+        a.u_out = u_slab; a.out_ld = u_ld; a.out_img_stride = 0; a.out_row_base = row0;
+    } else {
+        a.u_out = out_buf; a.out_ld = W; a.out_img_stride = 0; a.out_row_base = row0 - halo;
+    }
+    a.H = H; a.W = W;
+    a.y_begin = row0; a.y_end = row0 + rows;
+    a.avail_lo = row0 - halo < 0 ? 0 : row0 - halo;
+    a.avail_hi = row0 + rows + halo > H ? H : row0 + rows + halo;
+    const int tile = tnrd::choose_tile(h->d.ksize, 1, rows, W, h->num_sms);
+    (void)ex; (void)k;
+    return launch_one(h, stage, tile, a, 1, s);
+}
+
+struct NcclExchange : SlabExchange {
+    tnrd_handle *h; int rows, W; cudaStream_t s;
+    NcclExchange(tnrd_handle *h_, int rows_, int W_, cudaStream_t s_) : h(h_), rows(rows_), W(W_), s(s_) {}
+    tnrd_status exchange(int, float *buf) override {
+        NcclApi &api = nccl();
+        const int halo = h->d.ksize - 1;
+        const size_t n = (size_t)halo * W;
+        ncclResult_t r = api.GroupStart();
+        if (r == ncclSuccess && h->rank > 0) {
+            r = api.Send(buf + (size_t)halo * W, n, ncclFloat32, h->rank - 1, h->comm, s);
+            if (r == ncclSuccess) r = api.Recv(buf, n, ncclFloat32, h->rank - 1, h->comm, s);
+        }
+        if (r == ncclSuccess && h->rank < h->nranks - 1) {
+            r = api.Send(buf + (size_t)rows * W, n, ncclFloat32, h->rank + 1, h->comm, s);
+            if (r == ncclSuccess) r = api.Recv(buf + (size_t)(halo + rows) * W, n, ncclFloat32, h->rank + 1,
+                                               h->comm, s);
+        }
+        ncclResult_t r2 = api.GroupEnd();
+        if (r != ncclSuccess || r2 != ncclSuccess)
+            return fail(h, TNRD_ENCCL, "halo exchange: %s", api.GetErrorString(r != ncclSuccess ? r : r2));
+        return TNRD_OK;
+    }
+};
+
+void pack_stage(const tnrd_desc &d, int KK4, const float *filters, const float *w, const float *mu0,
+                const float *step, const float *gamma, int mode, int pstride, float *out) {
+    const int K = d.ksize, M = d.n_rbf;
+    const double sg_per_rho = std::sqrt(1.0 / (2.0 * std::log(2.0)));  // sqrt(log2(e)/2)
+    for (int i = 0; i < d.n_filters; ++i) {
+        float *p = out + (size_t)i * pstride;
+        std::memset(p, 0, sizeof(float) * pstride);
+        for (int j = 0; j < K * K; ++j) p[j] = filters[(size_t)i * K * K + j];
+        const double st = step[i], ga = gamma[i], m0 = mu0[i];
+        const double rho = st / ga, sg = rho * sg_per_rho;
+        const double a_s = sg / st, x_off = -m0 / st;
+        float *fc = p + KK4;
+        float *units = fc + 4;
+        const float *wi = w + (size_t)i * M;
+        if (mode == tnrd::MODE_HORNER) {
+            const int NB = (M + 7) / 8;
+            fc[0] = (float)a_s; fc[1] = (float)(2.0 * sg); fc[2] = (float)(1.0 / (8.0 * sg)); fc[3] = (float)NB;
+            for (int b = 0; b < NB; ++b) {
+                float *u = units + b * tnrd::kHornerUnit;
+                const int c = 8 * b + 4;
+                u[0] = (float)(sg * (x_off - c));
+                for (int dd = -4; dd <= 3; ++dd) {
+                    const int j = c + dd;
+                    const double coef = (j >= 0 && j < M) ? wi[j] * std::exp(-rho * rho * dd * dd / 2.0) : 0.0;
+                    u[1 + (dd + 4)] = (float)coef;   // u[1..8] = c_-4 .. c_3
+                }
+            }
+        } else {
+            fc[0] = (float)a_s; fc[1] = (float)(2.0 * sg); fc[2] = (float)(1.0 / sg); fc[3] = (float)M;
+            for (int j = 0; j < M; ++j) {
+                units[j * tnrd::kDirectUnit] = (float)(sg * (x_off - j));
+                units[j * tnrd::kDirectUnit + 1] = wi[j];
+            }
+        }
+    }
+}
+
+int pstride_for(const tnrd_desc &d, int KK4, int mode) {
+    const int M = d.n_rbf;
+    const int units = mode == tnrd::MODE_HORNER ? ((M + 7) / 8) * tnrd::kHornerUnit : M * tnrd::kDirectUnit;
+    return (KK4 + 4 + units + 3) / 4 * 4;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tnrd_abi_version(void) { return TNRD_ABI_VERSION; }
+
+const char *tnrd_status_string(tnrd_status s) {
+    switch (s) {
+        case TNRD_OK: return "TNRD_OK";
+        case TNRD_EINVAL: return "TNRD_EINVAL";
+        case TNRD_ESTATE: return "TNRD_ESTATE";
+        case TNRD_ENOMEM: return "TNRD_ENOMEM";
+        case TNRD_ECUDA: return "TNRD_ECUDA";
+        case TNRD_ENCCL: return "TNRD_ENCCL";
+        case TNRD_EUNSUPPORTED: return "TNRD_EUNSUPPORTED";
+    }
+    return "TNRD_UNKNOWN";
+}
+
+tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
+    if (!d || !out) return fail(nullptr, TNRD_EINVAL, "null argument");
+    *out = nullptr;
+    if (d->T < 1 || d->n_filters < 1 || d->n_rbf < 1 || d->n_rbf > 256)
+        return fail(nullptr, TNRD_EINVAL, "need T >= 1, n_filters >= 1, 1 <= n_rbf <= 256");
+    if (d->ksize < 3 || d->ksize % 2 == 0)
+        return fail(nullptr, TNRD_EINVAL, "ksize must be odd and >= 3 (got %d)", d->ksize);
+    if (d->ksize > 7) return fail(nullptr, TNRD_EUNSUPPORTED, "ksize %d not built (3, 5, 7)", d->ksize);
+    if (d->boundary != 0 && d->boundary != 1) return fail(nullptr, TNRD_EINVAL, "bad boundary %d", d->boundary);
+    if (d->phi_mode == TNRD_PHI_TABLE) return fail(nullptr, TNRD_EUNSUPPORTED, "tabulated phi not in this build");
+    if (d->phi_mode != TNRD_PHI_EXACT) return fail(nullptr, TNRD_EINVAL, "bad phi_mode %d", d->phi_mode);
+    if (d->reserved != 0) return fail(nullptr, TNRD_EINVAL, "reserved field must be 0");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess) return fail(nullptr, TNRD_ECUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+    if (d->device < 0 || d->device >= ndev) return fail(nullptr, TNRD_EINVAL, "device %d of %d", d->device, ndev);
+    DeviceGuard g(d->device);
+    tnrd_handle *h = new tnrd_handle();
+    h->d = *d;
+    cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, d->device);
+    h->KK4 = (d->ksize * d->ksize + 3) / 4 * 4;
+    h->pstride_max = std::max(pstride_for(*d, h->KK4, tnrd::MODE_HORNER), pstride_for(*d, h->KK4, tnrd::MODE_DIRECT));
+    h->pstride.assign(d->T, 0);
+    h->mode.assign(d->T, 0);
+    h->lambda.assign(d->T, 0.f);
+    h->is_set.assign(d->T, 0);
+    // shared-memory budget of the largest-stride stage on the small tile
+    int smem_optin = 0;
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, d->device);
+    const size_t need = tnrd::stage_smem_bytes(d->ksize, 1, d->n_filters, pstride_for(*d, h->KK4, tnrd::MODE_HORNER));
+    if ((long long)need > smem_optin) {
+        delete h;
+        return fail(nullptr, TNRD_EUNSUPPORTED, "model needs %zu B shared memory (> %d)", need, smem_optin);
+    }
+    const size_t bytes = sizeof(float) * (size_t)d->T * d->n_filters * h->pstride_max;
+    e = cudaMalloc(&h->d_params, bytes);
+    if (e != cudaSuccess) {
+        delete h;
+        return fail(nullptr, TNRD_ENOMEM, "cudaMalloc params: %s", cudaGetErrorString(e));
+    }
+    *out = h;
+    return TNRD_OK;
+}
+
+tnrd_status tnrd_set_stage_params(tnrd_handle *h, int t, const float *filters, const float *rbf_w,
+                                  const float *rbf_mu0, const float *rbf_step, const float *rbf_gamma,
+                                  float lambda) {
+    if (!h) return fail(nullptr, TNRD_EINVAL, "null handle");
+    if (t < 0 || t >= h->d.T) return fail(h, TNRD_EINVAL, "stage %d out of [0, %d)", t, h->d.T);
+    if (!filters || !rbf_w || !rbf_mu0 || !rbf_step || !rbf_gamma) return fail(h, TNRD_EINVAL, "null array");
+    if (!std::isfinite(lambda) || lambda <= 0.f) return fail(h, TNRD_EINVAL, "lambda must be finite and > 0");
+    const int Nk = h->d.n_filters, K = h->d.ksize, M = h->d.n_rbf;
+    double rho_max = 0.0;
+    for (int i = 0; i < Nk; ++i) {
+        if (!std::isfinite(rbf_mu0[i]) || !std::isfinite(rbf_step[i]) || !std::isfinite(rbf_gamma[i]))
+            return fail(h, TNRD_EINVAL, "non-finite RBF grid (filter %d)", i);
+        if (rbf_step[i] <= 0.f || rbf_gamma[i] <= 0.f)
+            return fail(h, TNRD_EINVAL, "RBF step and gamma must be > 0 (filter %d)", i);
+        rho_max = std::max(rho_max, (double)rbf_step[i] / rbf_gamma[i]);
+        for (int j = 0; j < K * K; ++j)
+            if (!std::isfinite(filters[(size_t)i * K * K + j])) return fail(h, TNRD_EINVAL, "non-finite filter tap");
+        for (int j = 0; j < M; ++j)
+            if (!std::isfinite(rbf_w[(size_t)i * M + j])) return fail(h, TNRD_EINVAL, "non-finite RBF weight");
+    }
+    const int mode = rho_max <= tnrd::kHornerMaxRho ? tnrd::MODE_HORNER : tnrd::MODE_DIRECT;
+    const int ps = pstride_for(h->d, h->KK4, mode);
+    std::vector<float> host((size_t)Nk * ps);
+    pack_stage(h->d, h->KK4, filters, rbf_w, rbf_mu0, rbf_step, rbf_gamma, mode, ps, host.data());
+    DeviceGuard g(h->d.device);
+    TNRD_CUDA(h, cudaMemcpy(h->d_params + (size_t)t * Nk * h->pstride_max, host.data(),
+                            sizeof(float) * host.size(), cudaMemcpyHostToDevice));
+    h->pstride[t] = ps;
+    h->mode[t] = mode;
+    h->lambda[t] = lambda;
+    h->is_set[t] = 1;
+    return TNRD_OK;
+}
+
+tnrd_status tnrd_denoise(tnrd_handle *h, const float *f, float *u, int B, int H, int W, long long ld,
+                         const float *peak, void *stream) {
+    tnrd_status st = check_ready(h);
+    if (st != TNRD_OK) return st;
+    if (!f || !u) return fail(h, TNRD_EINVAL, "null image pointer");
+    if (B < 1 || B > 65535) return fail(h, TNRD_EINVAL, "B must be in [1, 65535]");
+    if (H < h->d.ksize || W < h->d.ksize) return fail(h, TNRD_EINVAL, "H, W must be >= ksize");
+    if (ld < W) return fail(h, TNRD_EINVAL, "ld < W");
+    const long long span = (long long)B * H * ld;
+    if ((f < u && f + span > u) || (u < f && u + span > f) || f == u)
+        return fail(h, TNRD_EINVAL, "u must not alias f (the prox reads f every stage)");
+    if (peak)
+        for (int b = 0; b < B; ++b)
+            if (!std::isfinite(peak[b]) || peak[b] <= 0.f) return fail(h, TNRD_EINVAL, "peak[%d] must be > 0", b);
+    DeviceGuard g(h->d.device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int T = h->d.T;
+    if (T > 1) {
+        st = grow(h, &h->scratch, &h->scratch_bytes, sizeof(float) * (size_t)B * H * W, "scratch");
+        if (st != TNRD_OK) return st;
+    }
+    const int tile = tnrd::choose_tile(h->d.ksize, B, H, W, h->num_sms);
+    const tnrd::Image in_f{f, ld, (long long)H * ld, 0};
+    const tnrd::Image in_s{h->scratch, W, (long long)H * W, 0};
+    const tnrd::Image in_u{u, ld, (long long)H * ld, 0};
+    for (int t = 0; t < T; ++t) {
+        // ping-pong so that the last stage writes u: stage t writes u iff (T-1-t) is even
+        const bool to_u = ((T - 1 - t) % 2) == 0;
+        StageArgs a{};
+        a.u_in = t == 0 ? in_f : (to_u ? in_s : in_u);
+        a.f = in_f;
+        if (to_u) { a.u_out = u; a.out_ld = ld; a.out_img_stride = (long long)H * ld; }
+        else { a.u_out = h->scratch; a.out_ld = W; a.out_img_stride = (long long)H * W; }
+        a.out_row_base = 0;
+        a.H = H; a.W = W; a.y_begin = 0; a.y_end = H; a.avail_lo = 0; a.avail_hi = H;
+        st = launch_one(h, t, tile, a, B, s);
+        if (st != TNRD_OK) return st;
+    }
+    return TNRD_OK;
+}
+
+tnrd_status tnrd_denoise_host(tnrd_handle *h, const float *f_host, float *u_host, int B, int H, int W,
+                              const float *peak, void *stream) {
+    tnrd_status st = check_ready(h);
+    if (st != TNRD_OK) return st;
+    if (!f_host || !u_host) return fail(h, TNRD_EINVAL, "null host pointer");
+    if (B < 1 || H < 1 || W < 1) return fail(h, TNRD_EINVAL, "bad size");
+    DeviceGuard g(h->d.device);
+    const size_t bytes = sizeof(float) * (size_t)B * H * W;
+    size_t have_f = h->e2e_bytes, have_u = h->e2e_bytes;
+    st = grow(h, &h->e2e_f, &have_f, bytes, "e2e f");
+    if (st != TNRD_OK) return st;
+    st = grow(h, &h->e2e_u, &have_u, bytes, "e2e u");
+    if (st != TNRD_OK) return st;
+    h->e2e_bytes = std::min(have_f, have_u);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    TNRD_CUDA(h, cudaMemcpyAsync(h->e2e_f, f_host, bytes, cudaMemcpyHostToDevice, s));
+    st = tnrd_denoise(h, h->e2e_f, h->e2e_u, B, H, W, W, peak, stream);
+    if (st != TNRD_OK) return st;
+    TNRD_CUDA(h, cudaMemcpyAsync(u_host, h->e2e_u, bytes, cudaMemcpyDeviceToHost, s));
+    TNRD_CUDA(h, cudaStreamSynchronize(s));
+    return TNRD_OK;
+}
+
+tnrd_status tnrd_destroy(tnrd_handle *h) {
+    if (!h) return TNRD_OK;
+    {
+        DeviceGuard g(h->d.device);
+        cudaDeviceSynchronize();
+        cudaFree(h->d_params);
+        cudaFree(h->scratch);
+        cudaFree(h->e2e_f);
+        cudaFree(h->e2e_u);
+        cudaFree(h->slab_buf[0]);
+        cudaFree(h->slab_buf[1]);
+        for (float *p : h->lb_bufs) cudaFree(p);
+        for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+        if (h->comm && nccl().loaded) nccl().CommDestroy(h->comm);
+    }
+    delete h;
+    return TNRD_OK;
+}
+
+const char *tnrd_last_error(const tnrd_handle *h) {
+    return h ? h->err.c_str() : g_last_error.c_str();
+}
+
+unsigned long long tnrd_launch_count(const tnrd_handle *h) { return h ? h->launches : 0ULL; }
+
+tnrd_status tnrd_set_profiling(tnrd_handle *h, int enable) {
+    if (!h) return fail(nullptr, TNRD_EINVAL, "null handle");
+    h->profile = enable != 0;
+    h->ev_used = 0;
+    return TNRD_OK;
+}
+
+tnrd_status tnrd_get_launch_times(tnrd_handle *h, float *ms_out, int n, int *n_out) {
+    if (!h || !n_out) return fail(h, TNRD_EINVAL, "null argument");
+    const int have = h->ev_used / 2;
+    int k = 0;
+    for (; k < have && k < n; ++k) {
+        TNRD_CUDA(h, cudaEventSynchronize(h->ev[2 * k + 1]));
+        TNRD_CUDA(h, cudaEventElapsedTime(&ms_out[k], h->ev[2 * k], h->ev[2 * k + 1]));
+    }
+    *n_out = have;
+    return TNRD_OK;
+}
+
+tnrd_status tnrd_debug_phi(tnrd_handle *h, int t, int i, const float *v, float *out, long long n, void *stream) {
+    if (!h) return fail(nullptr, TNRD_EINVAL, "null handle");
+    if (t < 0 || t >= h->d.T || !h->is_set[t]) return fail(h, TNRD_ESTATE, "stage %d not set", t);
+    if (i < 0 || i >= h->d.n_filters) return fail(h, TNRD_EINVAL, "filter index");
+    DeviceGuard g(h->d.device);
+    cudaError_t e = tnrd::launch_debug_phi(h->d_params + (size_t)t * h->d.n_filters * h->pstride_max,
+                                           h->pstride[t], h->mode[t], h->d.ksize, i, v, out, n,
+                                           reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(h, e, "debug phi");
+    h->launches++;
+    return TNRD_OK;
+}
+
+tnrd_status tnrd_debug_prox(const float *ut, const float *f, float lambda, float *out, long long n, void *stream) {
+    if (!(lambda > 0.f)) return fail(nullptr, TNRD_EINVAL, "lambda must be > 0");
+    cudaError_t e = tnrd::launch_debug_prox(ut, f, lambda, out, n, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return fail(nullptr, TNRD_ECUDA, "debug prox: %s", cudaGetErrorString(e));
+    return TNRD_OK;
+}
+
+// ------------------------------------------------------------------ slabs
+tnrd_status tnrd_nccl_unique_id(void *id128) {
+    if (!id128) return fail(nullptr, TNRD_EINVAL, "null id");
+    NcclApi &api = nccl();
+    if (!api.loaded) return fail(nullptr, TNRD_ENCCL, "%s", api.why.c_str());
+    ncclUniqueId id;
+    ncclResult_t r = api.GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(nullptr, TNRD_ENCCL, "ncclGetUniqueId: %s", api.GetErrorString(r));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id128, &id, 128);
+    return TNRD_OK;
+}
+
+tnrd_status tnrd_comm_init(tnrd_handle *h, const void *id128, int rank, int nranks) {
+    if (!h || !id128) return fail(h, TNRD_EINVAL, "null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(h, TNRD_EINVAL, "rank %d of %d", rank, nranks);
+    NcclApi &api = nccl();
+    if (!api.loaded) return fail(h, TNRD_ENCCL, "%s", api.why.c_str());
+    DeviceGuard g(h->d.device);
+    ncclUniqueId id;
+    std::memcpy(&id, id128, 128);
+    if (h->comm) { api.CommDestroy(h->comm); h->comm = nullptr; }
+    ncclResult_t r = api.CommInitRank(&h->comm, nranks, id, rank);
+    if (r != ncclSuccess) return fail(h, TNRD_ENCCL, "ncclCommInitRank: %s", api.GetErrorString(r));
+    h->rank = rank;
+    h->nranks = nranks;
+    return TNRD_OK;
+}
+
+namespace {
+tnrd_status slab_args_ok(tnrd_handle *h, int H, int W, int row0, int rows, long long ld) {
+    const int halo = h->d.ksize - 1;
+    if (W < h->d.ksize || H < h->d.ksize) return fail(h, TNRD_EINVAL, "H, W must be >= ksize");
+    if (rows < halo || rows < 1) return fail(h, TNRD_EINVAL, "slab rows (%d) must be >= ksize-1", rows);
+    if (row0 < 0 || row0 + rows > H) return fail(h, TNRD_EINVAL, "slab [%d, %d) outside [0, %d)", row0, row0 + rows, H);
+    if (ld < W) return fail(h, TNRD_EINVAL, "ld < W");
+    return TNRD_OK;
+}
+
+// Run all T stages of one slab set.  `slabs` lists (row0, rows, buf0, buf1) per slab k;
+// `ex` fills halos.  Stage order: for t: for k (exchange, then compute) -- the
+// exchange of stage t only reads rows written by stage t-1.
+struct SlabDesc { int row0, rows; float *buf[2]; const float *f; long long f_ld; float *u; long long u_ld; };
+
+tnrd_status run_slabs(tnrd_handle *h, std::vector<SlabDesc> &sl, int H, int W, SlabExchange &ex, cudaStream_t s) {
+    const int halo = h->d.ksize - 1;
+    for (size_t k = 0; k < sl.size(); ++k) {  // seed buffer 0 with f (u_0 = f)
+        cudaError_t e = tnrd::launch_copy_rows(sl[k].f, sl[k].f_ld, sl[k].buf[0] + (size_t)halo * W, W,
+                                               sl[k].rows, W, s);
+        if (e != cudaSuccess) return cuda_fail(h, e, "seed slab");
+    }
+    for (int t = 0; t < h->d.T; ++t) {
+        for (size_t k = 0; k < sl.size(); ++k) {
+            tnrd_status st = ex.exchange((int)k, sl[k].buf[t % 2]);
+            if (st != TNRD_OK) return st;
+        }
+        for (size_t k = 0; k < sl.size(); ++k) {
+            tnrd_status st = run_slab(h, sl[k].f, sl[k].f_ld, sl[k].u, sl[k].u_ld, H, W, sl[k].row0, sl[k].rows,
+                                      sl[k].buf[0], sl[k].buf[1], ex, (int)k, t, s);
+            if (st != TNRD_OK) return st;
+        }
+    }
+    return TNRD_OK;
+}
+
+struct LoopbackExchange : SlabExchange {
+    tnrd_handle *h; std::vector<SlabDesc> *sl; int W; cudaStream_t s; int t = 0;
+    LoopbackExchange(tnrd_handle *h_, std::vector<SlabDesc> *sl_, int W_, cudaStream_t s_) : h(h_), sl(sl_), W(W_), s(s_) {}
+    tnrd_status exchange(int k, float *buf) override {
+        // halos of slab k come from the same-parity buffers of slabs k-1 and k+1
+        const int halo = h->d.ksize - 1;
+        std::vector<SlabDesc> &v = *sl;
+        const int par = (buf == v[k].buf[0]) ? 0 : 1;
+        const size_t n = sizeof(float) * (size_t)halo * W;
+        if (k > 0) {
+            const SlabDesc &up = v[k - 1];
+            cudaError_t e = cudaMemcpyAsync(buf, up.buf[par] + (size_t)up.rows * W, n, cudaMemcpyDeviceToDevice, s);
+            if (e != cudaSuccess) return cuda_fail(h, e, "loopback halo up");
+        }
+        if (k + 1 < (int)v.size()) {
+            const SlabDesc &dn = v[k + 1];
+            cudaError_t e = cudaMemcpyAsync(buf + (size_t)(halo + v[k].rows) * W, dn.buf[par] + (size_t)halo * W, n,
+                                            cudaMemcpyDeviceToDevice, s);
+            if (e != cudaSuccess) return cuda_fail(h, e, "loopback halo down");
+        }
+        return TNRD_OK;
+    }
+};
+}  // namespace
+
+tnrd_status tnrd_denoise_slab(tnrd_handle *h, const float *f_slab, float *u_slab, int H, int W, int row0, int rows,
+                              long long ld, float peak, void *stream) {
+    tnrd_status st = check_ready(h);
+    if (st != TNRD_OK) return st;
+    if (!h->comm && h->nranks > 1) return fail(h, TNRD_ESTATE, "communicator not initialised");
+    if (!f_slab || !u_slab || f_slab == u_slab) return fail(h, TNRD_EINVAL, "bad slab pointers");
+    if (!std::isfinite(peak) || peak <= 0.f) return fail(h, TNRD_EINVAL, "peak must be > 0");
+    st = slab_args_ok(h, H, W, row0, rows, ld);
+    if (st != TNRD_OK) return st;
+    DeviceGuard g(h->d.device);
+    const int halo = h->d.ksize - 1;
+    const size_t bytes = sizeof(float) * (size_t)(rows + 2 * halo) * W;
+    size_t have0 = h->slab_bytes, have1 = h->slab_bytes;
+    st = grow(h, &h->slab_buf[0], &have0, bytes, "slab buffer");
+    if (st != TNRD_OK) return st;
+    st = grow(h, &h->slab_buf[1], &have1, bytes, "slab buffer");
+    if (st != TNRD_OK) return st;
+    h->slab_bytes = std::min(have0, have1);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    std::vector<SlabDesc> sl{{row0, rows, {h->slab_buf[0], h->slab_buf[1]}, f_slab, ld, u_slab, ld}};
+    NcclExchange ex(h, rows, W, s);
+    if (h->nranks == 1) {
+        struct NoExchange : SlabExchange { tnrd_status exchange(int, float *) override { return TNRD_OK; } } none;
+        return run_slabs(h, sl, H, W, none, s);
+    }
+    return run_slabs(h, sl, H, W, ex, s);
+}
+
+tnrd_status tnrd_denoise_slabs_loopback(tnrd_handle *h, const float *f, float *u, int H, int W, long long ld,
+                                        int nslabs, void *stream) {
+    tnrd_status st = check_ready(h);
+    if (st != TNRD_OK) return st;
+    if (!f || !u || f == u) return fail(h, TNRD_EINVAL, "bad pointers");
+    if (nslabs < 1 || nslabs > H) return fail(h, TNRD_EINVAL, "nslabs");
+    DeviceGuard g(h->d.device);
+    const int halo = h->d.ksize - 1;
+    std::vector<SlabDesc> sl(nslabs);
+    int maxrows = 0;
+    for (int k = 0; k < nslabs; ++k) {
+        const int r0 = (int)((long long)H * k / nslabs), r1 = (int)((long long)H * (k + 1) / nslabs);
+        st = slab_args_ok(h, H, W, r0, r1 - r0, ld);
+        if (st != TNRD_OK) return st;
+        sl[k].row0 = r0; sl[k].rows = r1 - r0;
+        maxrows = std::max(maxrows, r1 - r0);
+    }
+    const size_t bytes = sizeof(float) * (size_t)(maxrows + 2 * halo) * W;
+    if ((int)h->lb_bufs.size() < 2 * nslabs || h->lb_bytes < bytes) {
+        cudaDeviceSynchronize();
+        for (float *p : h->lb_bufs) cudaFree(p);
+        h->lb_bufs.assign(2 * nslabs, nullptr);
+        for (auto &p : h->lb_bufs) {
+            cudaError_t e = cudaMalloc(&p, bytes);
+            if (e != cudaSuccess) return fail(h, TNRD_ENOMEM, "loopback buffers: %s", cudaGetErrorString(e));
+        }
+        h->lb_bytes = bytes;
+    }
+    for (int k = 0; k < nslabs; ++k) {
+        sl[k].buf[0] = h->lb_bufs[2 * k];
+        sl[k].buf[1] = h->lb_bufs[2 * k + 1];
+        sl[k].f = f + (size_t)sl[k].row0 * ld; sl[k].f_ld = ld;
+        sl[k].u = u + (size_t)sl[k].row0 * ld; sl[k].u_ld = ld;
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    LoopbackExchange ex(h, &sl, W, s);
+    return run_slabs(h, sl, H, W, ex, s);
+}
+
+}  // extern "C"

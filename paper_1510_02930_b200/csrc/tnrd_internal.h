@@ -1,0 +1,78 @@
+// Internal declarations shared by the host ABI (tnrd_api.cpp) and the sm_100a
+// kernels (tnrd_kernels.cu).  Not part of the public ABI (include/tnrd.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tnrd {
+
+// ---------------------------------------------------------------------------
+// Per-stage parameter block (device global memory, copied to shared memory by
+// every CTA).  Per filter i, `pstride` floats (multiple of 4):
+//
+//   taps  [KK4]     k_i row-major (K*K values, zero padded to a multiple of 4)
+//   fc    [4]       { a_s, two_sg, inv_ustep, n_units }
+//   units [n_units][UNIT]
+//
+// phi evaluation.  With x = (v - mu0)/step the response in
+// centre units, rho = step/gamma and sg = rho*sqrt(log2(e)/2):
+//
+//  MODE_HORNER (rho <= kHornerMaxRho): unit b covers centres j = 8b..8b+7,
+//    centred at c_b = 8b + 4.  ys = sg*(x - c_b) = a_s*v + cs_b,
+//      G = 2^(-ys^2) = exp(-rho^2 (x-c_b)^2 / 2)
+//      R = 2^(two_sg * clamp(ys, +-kClamp)) = exp(rho^2 (x - c_b))
+//      sum_{d=-4..3} w_{c_b+d} exp(-rho^2 (x-c_b-d)^2/2)
+//        = G * ( sum_{d=0..3} c_d R^d + sum_{d=1..4} c_{-d} R^{-d} ),
+//      c_d = w_{c_b+d} exp(-rho^2 d^2 / 2)          (exact identity)
+//    unit layout (12 floats): { cs_b, c_-4, c_-3, c_-2, c_-1, c_0, c_1, c_2, c_3, 0, 0, 0 }
+//  MODE_DIRECT (any rho): unit j is centre j: ys = a_s*v + cs_j, term w_j 2^(-ys^2)
+//    unit layout (4 floats): { cs_j, w_j, 0, 0 }
+//
+//  G (or the direct term) is exactly 0 in fp32 (ex2.approx.ftz flushes results
+//  below 2^-126) once |ys| > 11.2249; the kernel evaluates, per warp, the units
+//  whose |ys| <= kWindow for some lane, so every unit it skips contributes
+//  exactly 0 as well: the result does not depend on which pixels share a warp.
+// ---------------------------------------------------------------------------
+enum { MODE_HORNER = 0, MODE_DIRECT = 1 };
+constexpr int kHornerUnit = 12;
+constexpr int kDirectUnit = 4;
+constexpr float kWindow = 11.25f;     // > sqrt(126): all nonzero G lie inside
+constexpr float kClamp = 12.0f;       // clamp of ys before forming R (no overflow)
+constexpr double kHornerMaxRho = 1.5; // R^4 stays finite under the clamp
+
+struct Image {
+    const float *ptr;      // element (b, y, x) at ptr + b*img_stride + (y - row_base)*ld + x
+    long long ld;
+    long long img_stride;
+    int row_base;
+};
+
+struct StageArgs {
+    const float *params;   // this stage's parameter block (Nk * pstride floats)
+    Image u_in;            // u_t  (rows [avail_lo, avail_hi) addressable)
+    Image f;               // f    (rows [y_begin, y_end) addressable)
+    float *u_out;          // u_{t+1}, addressed like out_* below
+    long long out_ld;
+    long long out_img_stride;
+    int out_row_base;
+    int H, W;              // global image size (mirror at rows 0/H, cols 0/W)
+    int y_begin, y_end;    // output rows of this launch
+    int avail_lo, avail_hi;// rows of u_in that may be read
+    int Nk, pstride, mode;
+    int boundary;          // 0 = R1, 1 = R2
+    float lambda;
+};
+
+// Kernel launchers (tnrd_kernels.cu).  Return cudaSuccess or the launch error.
+size_t stage_smem_bytes(int ksize, int tile, int Nk, int pstride);
+int choose_tile(int ksize, int B, int H, int W, int num_sms);
+cudaError_t launch_stage(int ksize, int tile, const StageArgs &a, int B, cudaStream_t s);
+cudaError_t launch_debug_phi(const float *params, int pstride, int mode, int ksize, int i,
+                             const float *v, float *out, long long n, cudaStream_t s);
+cudaError_t launch_debug_prox(const float *ut, const float *f, float lambda, float *out,
+                              long long n, cudaStream_t s);
+cudaError_t launch_copy_rows(const float *src, long long src_ld, float *dst, long long dst_ld,
+                             int rows, int W, cudaStream_t s);
+
+}  // namespace tnrd
