@@ -74,7 +74,7 @@ NcclApi &nccl() {
 struct tnrd_handle {
     tnrd_desc d{};
     int num_sms = 148;
-    int KK4 = 0;
+    bool allow_large_tile = true;  // the 2x64x64 tile pair fits in shared memory
     int pstride_max = 0;
     std::vector<int> pstride;     // per stage
     std::vector<int> mode;        // per stage
@@ -212,7 +212,7 @@ tnrd_status run_slab(tnrd_handle *h, const float *f_slab, long long f_ld, float 
     a.y_begin = row0; a.y_end = row0 + rows;
     a.avail_lo = row0 - halo < 0 ? 0 : row0 - halo;
     a.avail_hi = row0 + rows + halo > H ? H : row0 + rows + halo;
-    const int tile = tnrd::choose_tile(h->d.ksize, 1, rows, W, h->num_sms);
+    const int tile = h->allow_large_tile ? tnrd::choose_tile(h->d.ksize, 1, rows, W, h->num_sms) : 1;
     (void)ex; (void)k;
     return launch_one(h, stage, tile, a, 1, s);
 }
@@ -241,33 +241,48 @@ struct NcclExchange : SlabExchange {
     }
 };
 
-void pack_stage(const tnrd_desc &d, int KK4, const float *filters, const float *w, const float *mu0,
+// Largest |ys| at which the Horner factors stay finite: sum|c| * R^3 and
+// sum|c| * R^-4 (R = 2^(2 sg ys)) below 2^120, i.e. 8 sg |ys| + log2(sum|c|) <= 120.
+double horner_yclamp(double sg, double sum_abs_c) {
+    const double l2 = std::log2(std::max(sum_abs_c, 1e-30));
+    return std::min(64.0, (120.0 - std::max(l2, -30.0)) / (8.0 * sg));
+}
+
+// Host-side evaluation constants of one stage (layout in tnrd_internal.h),
+// computed in double and rounded once to fp32.
+void pack_stage(const tnrd_desc &d, const float *filters, const float *w, const float *mu0,
                 const float *step, const float *gamma, int mode, int pstride, float *out) {
-    const int K = d.ksize, M = d.n_rbf;
+    const int K = d.ksize, M = d.n_rbf, K8 = tnrd::tap_pitch(K);
     const double sg_per_rho = std::sqrt(1.0 / (2.0 * std::log(2.0)));  // sqrt(log2(e)/2)
     for (int i = 0; i < d.n_filters; ++i) {
         float *p = out + (size_t)i * pstride;
         std::memset(p, 0, sizeof(float) * pstride);
-        for (int j = 0; j < K * K; ++j) p[j] = filters[(size_t)i * K * K + j];
+        for (int a = 0; a < K; ++a)
+            for (int b = 0; b < K; ++b) p[a * K8 + b] = filters[(size_t)i * K * K + a * K + b];
         const double st = step[i], ga = gamma[i], m0 = mu0[i];
         const double rho = st / ga, sg = rho * sg_per_rho;
         const double a_s = sg / st, x_off = -m0 / st;
-        float *fc = p + KK4;
-        float *units = fc + 4;
+        float *fc = p + tnrd::tap_floats(K);
+        float *units = fc + tnrd::kFc;
         const float *wi = w + (size_t)i * M;
         if (mode == tnrd::MODE_HORNER) {
             const int NB = (M + 7) / 8;
-            fc[0] = (float)a_s; fc[1] = (float)(2.0 * sg); fc[2] = (float)(1.0 / (8.0 * sg)); fc[3] = (float)NB;
+            double smax = 0.0;
             for (int b = 0; b < NB; ++b) {
                 float *u = units + b * tnrd::kHornerUnit;
                 const int c = 8 * b + 4;
                 u[0] = (float)(sg * (x_off - c));
+                double s = 0.0;
                 for (int dd = -4; dd <= 3; ++dd) {
                     const int j = c + dd;
                     const double coef = (j >= 0 && j < M) ? wi[j] * std::exp(-rho * rho * dd * dd / 2.0) : 0.0;
                     u[1 + (dd + 4)] = (float)coef;   // u[1..8] = c_-4 .. c_3
+                    s += std::fabs(coef);
                 }
+                smax = std::max(smax, s);
             }
+            fc[0] = (float)a_s; fc[1] = (float)(2.0 * sg); fc[2] = (float)(1.0 / (8.0 * sg)); fc[3] = (float)NB;
+            fc[4] = (float)horner_yclamp(sg, smax);
         } else {
             fc[0] = (float)a_s; fc[1] = (float)(2.0 * sg); fc[2] = (float)(1.0 / sg); fc[3] = (float)M;
             for (int j = 0; j < M; ++j) {
@@ -278,10 +293,10 @@ void pack_stage(const tnrd_desc &d, int KK4, const float *filters, const float *
     }
 }
 
-int pstride_for(const tnrd_desc &d, int KK4, int mode) {
+int pstride_for(const tnrd_desc &d, int mode) {
     const int M = d.n_rbf;
     const int units = mode == tnrd::MODE_HORNER ? ((M + 7) / 8) * tnrd::kHornerUnit : M * tnrd::kDirectUnit;
-    return (KK4 + 4 + units + 3) / 4 * 4;
+    return (tnrd::tap_floats(d.ksize) + tnrd::kFc + units + 3) / 4 * 4;
 }
 
 }  // namespace
@@ -323,8 +338,7 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
     tnrd_handle *h = new tnrd_handle();
     h->d = *d;
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, d->device);
-    h->KK4 = (d->ksize * d->ksize + 3) / 4 * 4;
-    h->pstride_max = std::max(pstride_for(*d, h->KK4, tnrd::MODE_HORNER), pstride_for(*d, h->KK4, tnrd::MODE_DIRECT));
+    h->pstride_max = std::max(pstride_for(*d, tnrd::MODE_HORNER), pstride_for(*d, tnrd::MODE_DIRECT));
     h->pstride.assign(d->T, 0);
     h->mode.assign(d->T, 0);
     h->lambda.assign(d->T, 0.f);
@@ -332,11 +346,12 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
     // shared-memory budget of the largest-stride stage on the small tile
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, d->device);
-    const size_t need = tnrd::stage_smem_bytes(d->ksize, 1, d->n_filters, pstride_for(*d, h->KK4, tnrd::MODE_HORNER));
-    if ((long long)need > smem_optin) {
+    const size_t need_s = tnrd::stage_smem_bytes(d->ksize, 1, d->n_filters, h->pstride_max);
+    if ((long long)need_s > smem_optin) {
         delete h;
-        return fail(nullptr, TNRD_EUNSUPPORTED, "model needs %zu B shared memory (> %d)", need, smem_optin);
+        return fail(nullptr, TNRD_EUNSUPPORTED, "model needs %zu B shared memory (> %d)", need_s, smem_optin);
     }
+    h->allow_large_tile = (long long)tnrd::stage_smem_bytes(d->ksize, 0, d->n_filters, h->pstride_max) <= smem_optin;
     const size_t bytes = sizeof(float) * (size_t)d->T * d->n_filters * h->pstride_max;
     e = cudaMalloc(&h->d_params, bytes);
     if (e != cudaSuccess) {
@@ -367,10 +382,22 @@ tnrd_status tnrd_set_stage_params(tnrd_handle *h, int t, const float *filters, c
         for (int j = 0; j < M; ++j)
             if (!std::isfinite(rbf_w[(size_t)i * M + j])) return fail(h, TNRD_EINVAL, "non-finite RBF weight");
     }
-    const int mode = rho_max <= tnrd::kHornerMaxRho ? tnrd::MODE_HORNER : tnrd::MODE_DIRECT;
-    const int ps = pstride_for(h->d, h->KK4, mode);
-    std::vector<float> host((size_t)Nk * ps);
-    pack_stage(h->d, h->KK4, filters, rbf_w, rbf_mu0, rbf_step, rbf_gamma, mode, ps, host.data());
+    // Horner units when every Gaussian is wide enough and the factors stay finite
+    // over the whole kWindow; otherwise one unit per centre.
+    int mode = rho_max <= tnrd::kHornerMaxRho ? tnrd::MODE_HORNER : tnrd::MODE_DIRECT;
+    std::vector<float> host;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        const int ps = pstride_for(h->d, mode);
+        host.assign((size_t)Nk * ps, 0.f);
+        pack_stage(h->d, filters, rbf_w, rbf_mu0, rbf_step, rbf_gamma, mode, ps, host.data());
+        if (mode == tnrd::MODE_DIRECT) break;
+        bool ok = true;
+        for (int i = 0; i < Nk; ++i)
+            ok = ok && host[(size_t)i * ps + tnrd::tap_floats(K) + 4] >= tnrd::kWindow + 0.5f;
+        if (ok) break;
+        mode = tnrd::MODE_DIRECT;
+    }
+    const int ps = pstride_for(h->d, mode);
     DeviceGuard g(h->d.device);
     TNRD_CUDA(h, cudaMemcpy(h->d_params + (size_t)t * Nk * h->pstride_max, host.data(),
                             sizeof(float) * host.size(), cudaMemcpyHostToDevice));
@@ -402,7 +429,7 @@ tnrd_status tnrd_denoise(tnrd_handle *h, const float *f, float *u, int B, int H,
         st = grow(h, &h->scratch, &h->scratch_bytes, sizeof(float) * (size_t)B * H * W, "scratch");
         if (st != TNRD_OK) return st;
     }
-    const int tile = tnrd::choose_tile(h->d.ksize, B, H, W, h->num_sms);
+    const int tile = h->allow_large_tile ? tnrd::choose_tile(h->d.ksize, B, H, W, h->num_sms) : 1;
     const tnrd::Image in_f{f, ld, (long long)H * ld, 0};
     const tnrd::Image in_s{h->scratch, W, (long long)H * W, 0};
     const tnrd::Image in_u{u, ld, (long long)H * ld, 0};

@@ -11,21 +11,23 @@ namespace tnrd {
 // Per-stage parameter block (device global memory, copied to shared memory by
 // every CTA).  Per filter i, `pstride` floats (multiple of 4):
 //
-//   taps  [KK4]     k_i row-major (K*K values, zero padded to a multiple of 4)
-//   fc    [4]       { a_s, two_sg, inv_ustep, n_units }
+//   taps  [K][K8]   k_i row-major, each row zero padded to K8 = roundup(K, 4)
+//                   floats so that a tap row is whole float4s
+//   fc    [8]       { a_s, two_sg, inv_ustep, n_units, yclamp, 0, 0, 0 }
 //   units [n_units][UNIT]
 //
 // phi evaluation.  With x = (v - mu0)/step the response in
 // centre units, rho = step/gamma and sg = rho*sqrt(log2(e)/2):
 //
-//  MODE_HORNER (rho <= kHornerMaxRho): unit b covers centres j = 8b..8b+7,
-//    centred at c_b = 8b + 4.  ys = sg*(x - c_b) = a_s*v + cs_b,
-//      G = 2^(-ys^2) = exp(-rho^2 (x-c_b)^2 / 2)
-//      R = 2^(two_sg * clamp(ys, +-kClamp)) = exp(rho^2 (x - c_b))
+//  MODE_HORNER: unit b covers centres j = 8b..8b+7, centred at c_b = 8b + 4.
+//    ys = sg*(x - c_b) = a_s*v + cs_b,
+//      G = 2^(-ys^2) = exp(-rho^2 (x-c_b)^2 / 2),   R = 2^(two_sg*ys) = exp(rho^2 (x - c_b)),
 //      sum_{d=-4..3} w_{c_b+d} exp(-rho^2 (x-c_b-d)^2/2)
-//        = G * ( sum_{d=0..3} c_d R^d + sum_{d=1..4} c_{-d} R^{-d} ),
+//        = G * ( sum_{d=0..3} c_d R^d + R^-1 sum_{d=1..4} c_{-d} R^{-(d-1)} ),
 //      c_d = w_{c_b+d} exp(-rho^2 d^2 / 2)          (exact identity)
 //    unit layout (12 floats): { cs_b, c_-4, c_-3, c_-2, c_-1, c_0, c_1, c_2, c_3, 0, 0, 0 }
+//    yclamp: |ys| bound under which sum|c| * R^3 and sum|c| * R^-4 stay below
+//    2^120 (host-computed, >= kWindow + 0.5 or the stage uses MODE_DIRECT).
 //  MODE_DIRECT (any rho): unit j is centre j: ys = a_s*v + cs_j, term w_j 2^(-ys^2)
 //    unit layout (4 floats): { cs_j, w_j, 0, 0 }
 //
@@ -37,9 +39,12 @@ namespace tnrd {
 enum { MODE_HORNER = 0, MODE_DIRECT = 1 };
 constexpr int kHornerUnit = 12;
 constexpr int kDirectUnit = 4;
+constexpr int kFc = 8;                // floats of per-filter constants
 constexpr float kWindow = 11.25f;     // > sqrt(126): all nonzero G lie inside
-constexpr float kClamp = 12.0f;       // clamp of ys before forming R (no overflow)
-constexpr double kHornerMaxRho = 1.5; // R^4 stays finite under the clamp
+constexpr double kHornerMaxRho = 1.5; // wider Gaussians only (else MODE_DIRECT)
+
+__host__ __device__ constexpr int tap_pitch(int K) { return (K + 3) / 4 * 4; }
+__host__ __device__ constexpr int tap_floats(int K) { return K * tap_pitch(K); }
 
 struct Image {
     const float *ptr;      // element (b, y, x) at ptr + b*img_stride + (y - row_base)*ld + x
@@ -62,12 +67,14 @@ struct StageArgs {
     int Nk, pstride, mode;
     int boundary;          // 0 = R1, 1 = R2
     float lambda;
+    // tiling (filled by launch_stage): tiles in x-fastest, then y, then image order
+    int tiles_x, tiles_y, n_tiles;
 };
 
 // Kernel launchers (tnrd_kernels.cu).  Return cudaSuccess or the launch error.
 size_t stage_smem_bytes(int ksize, int tile, int Nk, int pstride);
 int choose_tile(int ksize, int B, int H, int W, int num_sms);
-cudaError_t launch_stage(int ksize, int tile, const StageArgs &a, int B, cudaStream_t s);
+cudaError_t launch_stage(int ksize, int tile, StageArgs &a, int B, cudaStream_t s);
 cudaError_t launch_debug_phi(const float *params, int pstride, int mode, int ksize, int i,
                              const float *v, float *out, long long n, cudaStream_t s);
 cudaError_t launch_debug_prox(const float *ut, const float *f, float lambda, float *out,

@@ -9,13 +9,22 @@
 //   ut  = u - d            explicit diffusion, tau = 1  (P l.331-333)
 //   u+  = prox_lambda(ut)  Poisson proximal map         (P Eq.12, l.318-322)
 //
-// One CTA owns a TWxTH output tile.  u (tile + 2r halo) and the stage
-// parameters live in shared memory; for each filter the CTA computes w_i on
-// the tile + r halo into a double-buffered shared array (phase A), then every
-// thread accumulates its output block's kbar_i * w_i in registers (phase B).
-// The N_k response maps never leave the SM; HBM sees u, f and u+ once per
-// stage (12 B/pixel).  All arithmetic is fp32 with explicit fmaf in a fixed
-// per-pixel order, so results do not depend on tiling, batching or slabbing.
+// Tile pairs and packed fp32x2.  One CTA owns TWO TWxTH output
+// tiles, A and B (consecutive in x-fastest / y / image order).  Shared memory
+// holds u (tile + 2r halo) and, per filter, w_i (tile + r halo) of both tiles
+// interleaved as float2 {A, B}, so every multiply-add of both convolutions and
+// of the phi evaluation is one sm_100a FFMA2 on a register pair, with the
+// filter tap or phi coefficient as a broadcast scalar operand.  FFMA2 does the
+// two lanes' FMAs with the same per-element IEEE rounding as FFMA; it halves
+// the issue slots per FMA, which is what bounded the one-pixel-per-lane kernel
+// (ncu: 73% issue active at 12.3k instructions/pixel/stage).
+//
+// Per filter i the CTA computes w_i on the tile + r halo (phase A: runs of
+// RUNW pixel pairs per thread), then every thread accumulates its BR x 2 block
+// of kbar_i * w_i in registers (phase B).  The N_k response maps never leave
+// the SM; HBM sees u, f and u+ once per stage (12 B/pixel).  Every pixel's
+// arithmetic is a fixed sequence of IEEE fp32 operations, independent of its
+// tile, its partner tile, batching or slabbing.
 //
 // Boundary R1 (P l.302-311): w is extended by the half-sample mirror.  Out-of-
 // image w positions are written by the thread that computes their mirror
@@ -27,6 +36,36 @@
 
 namespace tnrd {
 namespace {
+
+typedef unsigned long long f2;  // packed fp32x2: low word = tile A, high word = tile B
+
+__device__ __forceinline__ f2 pk(float a, float b) {
+    f2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ f2 bc(float s) { return pk(s, s); }
+__device__ __forceinline__ float lo(f2 a) {
+    float x, y;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(a));
+    return x;
+}
+__device__ __forceinline__ float hi(f2 a) {
+    float x, y;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(a));
+    return y;
+}
+// d = a * b + c, elementwise, round-to-nearest (FFMA2)
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+    f2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+    f2 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
 
 __device__ __forceinline__ float ex2_ftz(float x) {
     float r;
@@ -63,109 +102,184 @@ __device__ __forceinline__ float prox_poisson(float ut, float lam, float f) {
     return __fdiv_rn(2.0f * lam * f, sigma - delta);
 }
 
-// phi_i on NP values of one lane.  Warp-collective: all lanes must call it
-// with the same `fp` and `mode` (see tnrd_internal.h for the scheme).
+// Horner units [u0, u1] on NP pairs (see tnrd_internal.h).  CLAMP bounds ys to
+// +-yclamp before forming R = 2^(two_sg ys) so R^3 and R^-4 stay finite for lanes
+// far from the unit; the caller uses CLAMP = false only when no evaluated lane can
+// reach the bound, where both variants compute bitwise the same values.
+template <int NP, bool CLAMP>
+__device__ __forceinline__ void horner_units(const float *__restrict__ units, float a_s, float two_sg,
+                                             float yclamp, int u0, int u1, const f2 (&v)[NP],
+                                             f2 (&w)[NP]) {
+    for (int u = u0; u <= u1; ++u) {
+        const float4 *up = reinterpret_cast<const float4 *>(units + u * kHornerUnit);
+        const float4 q0 = up[0], q1 = up[1], q2 = up[2];
+        // q0 = {cs, c-4, c-3, c-2}, q1 = {c-1, c0, c1, c2}, q2 = {c3, ...}
+#pragma unroll
+        for (int e = 0; e < NP; ++e) {
+            const f2 ys = fma2(v[e], bc(a_s), bc(q0.x));
+            const f2 sq = mul2(ys, ys);
+            const f2 G = pk(ex2_ftz(-lo(sq)), ex2_ftz(-hi(sq)));
+            f2 yc = ys;
+            if (CLAMP)
+                yc = pk(fminf(fmaxf(lo(ys), -yclamp), yclamp), fminf(fmaxf(hi(ys), -yclamp), yclamp));
+            const f2 yr = mul2(yc, bc(two_sg));
+            const f2 R = pk(ex2_ftz(lo(yr)), ex2_ftz(hi(yr)));
+            const f2 Ri = pk(ex2_ftz(-lo(yr)), ex2_ftz(-hi(yr)));
+            const f2 pp = fma2(fma2(fma2(R, bc(q2.x), bc(q1.w)), R, bc(q1.z)), R, bc(q1.y));
+            const f2 pm = fma2(fma2(fma2(Ri, bc(q0.y), bc(q0.z)), Ri, bc(q0.w)), Ri, bc(q1.x));
+            w[e] = fma2(G, fma2(pm, Ri, pp), w[e]);
+        }
+    }
+}
+
+// phi_i on NP value pairs of one lane.  Warp-collective: all lanes must call it
+// with the same `fp` and `mode`.
 template <int NP>
-__device__ __forceinline__ void phi_eval(const float *__restrict__ fp, int mode,
-                                         const float (&v)[NP], float (&w)[NP]) {
+__device__ __forceinline__ void phi_x2(const float *__restrict__ fp, int mode, const f2 (&v)[NP],
+                                       f2 (&w)[NP]) {
     const float4 fc = *reinterpret_cast<const float4 *>(fp);
     const float a_s = fc.x, two_sg = fc.y, inv_ustep = fc.z;
     const int nunits = __float2int_rn(fc.w);
-    const float *units = fp + 4;
-    const float cs0 = units[0];
-    float lo = INFINITY, hi = -INFINITY;
+    const float yclamp = fp[4];
+    const float *units = fp + kFc;
+    float vmin = INFINITY, vmax = -INFINITY;
 #pragma unroll
     for (int e = 0; e < NP; ++e) {
-        const float ys0 = fmaf(a_s, v[e], cs0);
-        lo = fminf(lo, ys0);
-        hi = fmaxf(hi, ys0);
-        w[e] = 0.0f;
+        vmin = fminf(vmin, fminf(lo(v[e]), hi(v[e])));
+        vmax = fmaxf(vmax, fmaxf(lo(v[e]), hi(v[e])));
+        w[e] = 0ull;
     }
-    lo = warp_min(lo);
-    hi = warp_max(hi);
+    // a_s > 0 and fmaf rounding is monotone, so these are the min / max of ys_0
+    const float cs0 = units[0];
+    const float ylo = warp_min(fmaf(a_s, vmin, cs0));
+    const float yhi = warp_max(fmaf(a_s, vmax, cs0));
     // unit u has ys_u = ys_0 - u*ustep; it can be nonzero only if |ys_u| <= kWindow
-    const int u0 = max(0, __float2int_ru((lo - kWindow) * inv_ustep));
-    const int u1 = min(nunits - 1, __float2int_rd((hi + kWindow) * inv_ustep));
+    const int u0 = max(0, __float2int_ru((ylo - kWindow) * inv_ustep));
+    const int u1 = min(nunits - 1, __float2int_rd((yhi + kWindow) * inv_ustep));
     if (mode == MODE_HORNER) {
-        for (int u = u0; u <= u1; ++u) {
-            const float4 *up = reinterpret_cast<const float4 *>(units + u * kHornerUnit);
-            const float4 q0 = up[0], q1 = up[1], q2 = up[2];
-            // q0 = {cs, c-4, c-3, c-2}, q1 = {c-1, c0, c1, c2}, q2 = {c3, ...}
-#pragma unroll
-            for (int e = 0; e < NP; ++e) {
-                const float ys = fmaf(a_s, v[e], q0.x);
-                const float G = ex2_ftz(ys * -ys);
-                const float yr = fminf(fmaxf(ys, -kClamp), kClamp) * two_sg;
-                const float R = ex2_ftz(yr);
-                const float Ri = ex2_ftz(-yr);
-                const float pp = fmaf(fmaf(fmaf(q2.x, R, q1.w), R, q1.z), R, q1.y);
-                const float pm = fmaf(fmaf(fmaf(q0.y, Ri, q0.z), Ri, q0.w), Ri, q1.x) * Ri;
-                w[e] = fmaf(G, pp + pm, w[e]);
-            }
-        }
+        // every evaluated unit has |ys_u| <= (yhi - ylo) + kWindow for every lane
+        if ((yhi - ylo) + (kWindow + 0.05f) <= yclamp)
+            horner_units<NP, false>(units, a_s, two_sg, yclamp, u0, u1, v, w);
+        else
+            horner_units<NP, true>(units, a_s, two_sg, yclamp, u0, u1, v, w);
     } else {
         for (int u = u0; u <= u1; ++u) {
             const float2 q = *reinterpret_cast<const float2 *>(units + u * kDirectUnit);
 #pragma unroll
             for (int e = 0; e < NP; ++e) {
-                const float ys = fmaf(a_s, v[e], q.x);
-                w[e] = fmaf(q.y, ex2_ftz(ys * -ys), w[e]);
+                const f2 ys = fma2(v[e], bc(a_s), bc(q.x));
+                const f2 sq = mul2(ys, ys);
+                const f2 E = pk(ex2_ftz(-lo(sq)), ex2_ftz(-hi(sq)));
+                w[e] = fma2(E, bc(q.y), w[e]);
             }
         }
     }
 }
 
-template <int K, int TW, int TH, int NT, int BR>
-struct Tile {
+// pitch p >= need (in float2) with p == r (mod 16)
+constexpr int pitch_mod16(int need, int r) { return need + (((r - need) % 16) + 16) % 16; }
+
+template <int K, int TW, int TH, int NT, int RUNW, int BR>
+struct Geo {
     static constexpr int R = K / 2;
-    static constexpr int KK = K * K;
-    static constexpr int KK4 = (KK + 3) / 4 * 4;
-    static constexpr int WW = (TW + 2 * R + 3) / 4 * 4;  // phi-region buffer width
-    static constexpr int WH = TH + 2 * R;                 // phi-region rows
-    static constexpr int RUNS_ROW = WW / 4;
-    static constexpr int NRUN = RUNS_ROW * WH;
-    static constexpr int SEG = 4 + 2 * R;                 // row window of a 4-wide run
-    static constexpr int UW = (WW + 2 * R + 3) / 4 * 4;   // u tile width
+    static constexpr int K8 = tap_pitch(K);
+    static constexpr int KT = tap_floats(K);
+    static constexpr int BC = 2;                                  // phase-B block width (pairs)
+    static constexpr int WWc = (TW + 2 * R + RUNW - 1) / RUNW * RUNW;  // w region width
+    static constexpr int RPR = WWc / RUNW;                         // runs per w row
+    static constexpr int WH = TH + 2 * R;                          // w region rows
+    static constexpr int NRUN = WH * RPR;
+    static constexpr int SEG = RUNW + 2 * R;                       // u window of a run
+    static constexpr int SEGB = BC + 2 * R;                        // w window of a phase-B row
     static constexpr int UH = TH + 4 * R;
-    static constexpr int NBX = TW / 4;
+    static constexpr int UWc = WWc + 2 * R;
+    // Bank-conflict-free LDS.128: lanes of a run row sit 2*RUNW
+    // words apart; with RUNW = 10 and a pitch == 10*RPR (mod 16) float2, any 8
+    // consecutive runs hit 8 distinct 4-bank groups (group = 5*run mod 8).
+    static constexpr int PU = pitch_mod16(UWc, (10 * RPR) % 16);
+    static constexpr int PW = pitch_mod16(WWc, (10 * RPR) % 16);
+    static constexpr int NBX = TW / BC;
     static constexpr int NBY = TH / BR;
+    static_assert(RUNW == 10, "pitch rule assumes RUNW = 10");
+    static_assert(SEG % 2 == 0 && SEGB % 2 == 0, "whole 16-byte segments");
     static_assert(NBX * NBY == NT, "exactly one phase-B block per thread");
+    static_assert(NBX % 8 == 0, "a quarter warp stays in one phase-B row");
     static_assert(NT % 32 == 0, "whole warps");
-    static constexpr int smem_floats_fixed = UH * UW + 2 * WH * WW;
+    static constexpr int smem_f2 = UH * PU + 2 * WH * PW;
 };
 
-// Load SEG consecutive floats starting at a 16-byte aligned shared address.
-template <int SEG>
-__device__ __forceinline__ void load_seg(const float *p, float (&s)[SEG]) {
+template <int N>
+__device__ __forceinline__ void load_f2(const f2 *p, f2 (&s)[N]) {
 #pragma unroll
-    for (int j = 0; j + 4 <= SEG; j += 4) {
-        const float4 q = *reinterpret_cast<const float4 *>(p + j);
-        s[j] = q.x; s[j + 1] = q.y; s[j + 2] = q.z; s[j + 3] = q.w;
-    }
-    if constexpr (SEG % 4 == 2) {
-        const float2 q = *reinterpret_cast<const float2 *>(p + SEG - 2);
-        s[SEG - 2] = q.x; s[SEG - 1] = q.y;
+    for (int j = 0; j < N; j += 2) {
+        const ulonglong2 q = *reinterpret_cast<const ulonglong2 *>(p + j);
+        s[j] = q.x;
+        s[j + 1] = q.y;
     }
 }
 
-template <int K, int TW, int TH, int NT, int BR, int MINB>
+template <int K>
+__device__ __forceinline__ void load_taps_row(const float *p, float (&t)[tap_pitch(K)]) {
+#pragma unroll
+    for (int j = 0; j < tap_pitch(K); j += 4) {
+        const float4 q = *reinterpret_cast<const float4 *>(p + j);
+        t[j] = q.x; t[j + 1] = q.y; t[j + 2] = q.z; t[j + 3] = q.w;
+    }
+}
+
+struct TileGeo {
+    int b, x0, y0;
+    bool border;
+};
+
+__device__ __forceinline__ TileGeo tile_geo(const StageArgs &a, int t, int TW, int TH, int R) {
+    const int per_img = a.tiles_x * a.tiles_y;
+    TileGeo g;
+    g.b = t / per_img;
+    const int rem = t - g.b * per_img;
+    const int ty = rem / a.tiles_x;
+    g.x0 = (rem - ty * a.tiles_x) * TW;
+    g.y0 = a.y_begin + ty * TH;
+    g.border = (g.x0 - R < 0) || (g.x0 + TW + R > a.W) || (g.y0 - R < 0) || (g.y0 + TH + R > a.H);
+    return g;
+}
+
+// Mirror partners of an in-image w position (py, px) within r of an edge (R1).
+// `h` selects the half (0 = tile A, 1 = tile B) of the float2 w slot.
+template <int R, int WH, int WWc, int PW>
+__device__ __forceinline__ void mirror_store(float *Wf, int h, int H, int W, int y0, int x0, int wr, int wcol,
+                                             int py, int px, float val) {
+    const int my = py < R ? -1 - py : (py >= H - R ? 2 * H - 1 - py : INT_MIN);
+    const int mx = px < R ? -1 - px : (px >= W - R ? 2 * W - 1 - px : INT_MIN);
+    const int ty = my - (y0 - R), tx = mx - (x0 - R);
+    const bool ym = my != INT_MIN && ty >= 0 && ty < WH;
+    const bool xm = mx != INT_MIN && tx >= 0 && tx < WWc;
+    if (xm) Wf[2 * (wr * PW + tx) + h] = val;
+    if (ym) Wf[2 * (ty * PW + wcol) + h] = val;
+    if (xm && ym) Wf[2 * (ty * PW + tx) + h] = val;
+}
+
+template <int K, int TW, int TH, int NT, int RUNW, int BR, int MINB>
 __global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__ StageArgs a) {
-    using Tl = Tile<K, TW, TH, NT, BR>;
-    constexpr int R = Tl::R, KK4 = Tl::KK4, WW = Tl::WW, WH = Tl::WH, UW = Tl::UW, UH = Tl::UH;
-    constexpr int SEG = Tl::SEG;
+    using G = Geo<K, TW, TH, NT, RUNW, BR>;
+    constexpr int R = G::R, K8 = G::K8, KT = G::KT, BC = G::BC;
+    constexpr int WWc = G::WWc, RPR = G::RPR, WH = G::WH, NRUN = G::NRUN, UH = G::UH, UWc = G::UWc;
+    constexpr int PU = G::PU, PW = G::PW, SEG = G::SEG, SEGB = G::SEGB;
 
     extern __shared__ float4 smem4[];
     float *s_par = reinterpret_cast<float *>(smem4);
-    float *s_u = s_par + a.Nk * a.pstride;
-    float *s_w = s_u + UH * UW;
+    f2 *s_u = reinterpret_cast<f2 *>(s_par + a.Nk * a.pstride);
+    f2 *s_w = s_u + UH * PU;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    const int b = blockIdx.z;
-    const int x0 = blockIdx.x * TW;
-    const int y0 = a.y_begin + blockIdx.y * TH;
     const int H = a.H, W = a.W;
+
+    const int tA = 2 * blockIdx.x;
+    const bool hasB = tA + 1 < a.n_tiles;
+    const TileGeo gA = tile_geo(a, tA, TW, TH, R);
+    const TileGeo gB = hasB ? tile_geo(a, tA + 1, TW, TH, R) : gA;
 
     // ---- stage parameters -> smem (float4 copy)
     {
@@ -173,189 +287,221 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__
         const int n4 = a.Nk * a.pstride / 4;
         for (int j = tid; j < n4; j += NT) smem4[j] = __ldg(src + j);
     }
-    // ---- u tile (tile + 2r halo), half-sample mirror at the image edges
+    // ---- u of both tiles (tile + 2r halo), half-sample mirror at the image edges
     {
-        const float *ub = a.u_in.ptr + (long long)b * a.u_in.img_stride;
-        for (int j = tid; j < UH * UW; j += NT) {
-            const int r = j / UW, c = j - r * UW;
-            int gy = reflect(y0 - 2 * R + r, H);
-            gy = min(max(gy, a.avail_lo), a.avail_hi - 1);
-            const int gx = reflect(x0 - 2 * R + c, W);
-            s_u[j] = __ldg(ub + (long long)(gy - a.u_in.row_base) * a.u_in.ld + gx);
+        const float *ubA = a.u_in.ptr + (long long)gA.b * a.u_in.img_stride;
+        const float *ubB = a.u_in.ptr + (long long)gB.b * a.u_in.img_stride;
+        for (int j = tid; j < UH * UWc; j += NT) {
+            const int r = j / UWc, c = j - r * UWc;
+            int gyA = reflect(gA.y0 - 2 * R + r, H), gyB = reflect(gB.y0 - 2 * R + r, H);
+            gyA = min(max(gyA, a.avail_lo), a.avail_hi - 1);
+            gyB = min(max(gyB, a.avail_lo), a.avail_hi - 1);
+            const int gxA = reflect(gA.x0 - 2 * R + c, W), gxB = reflect(gB.x0 - 2 * R + c, W);
+            const float uA = __ldg(ubA + (long long)(gyA - a.u_in.row_base) * a.u_in.ld + gxA);
+            const float uB = __ldg(ubB + (long long)(gyB - a.u_in.row_base) * a.u_in.ld + gxB);
+            s_u[r * PU + c] = pk(uA, uB);
         }
     }
     __syncthreads();
 
-    const bool border = (x0 - R < 0) || (x0 + TW + R > W) || (y0 - R < 0) || (y0 + TH + R > H);
-    // phase-B block of this thread: BR rows x 4 cols at (oyl, oxl) in the tile
-    const int oyl = (tid / Tl::NBX) * BR, oxl = (tid % Tl::NBX) * 4;
-    const bool r2_edge = (a.boundary == 1) &&
-                         ((x0 + oxl - R < 0) || (x0 + oxl + 4 + R > W) ||
-                          (y0 + oyl - R < 0) || (y0 + oyl + BR + R > H));
+    // phase-B block of this thread: BR rows x BC pair-columns at (oyl, oxl) in the tile
+    const int oyl = (tid / G::NBX) * BR, oxl = (tid % G::NBX) * BC;
+    const auto r2_edge = [&](const TileGeo &g) {
+        return (a.boundary == 1) && ((g.x0 + oxl - R < 0) || (g.x0 + oxl + BC + R > W) ||
+                                     (g.y0 + oyl - R < 0) || (g.y0 + oyl + BR + R > H));
+    };
+    const bool r2A = r2_edge(gA), r2B = r2_edge(gB);
 
-    float acc[BR][4];
+    f2 acc[BR][BC];
 #pragma unroll
     for (int ry = 0; ry < BR; ++ry)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[ry][e] = 0.0f;
+        for (int e = 0; e < BC; ++e) acc[ry][e] = 0ull;
 
     for (int i = 0; i < a.Nk; ++i) {
         const float *fpar = s_par + i * a.pstride;
-        float *Wb = s_w + (i & 1) * (WH * WW);
-        float tk[KK4];
-#pragma unroll
-        for (int j = 0; j < KK4; j += 4) {
-            const float4 q = *reinterpret_cast<const float4 *>(fpar + j);
-            tk[j] = q.x; tk[j + 1] = q.y; tk[j + 2] = q.z; tk[j + 3] = q.w;
-        }
+        f2 *Wb = s_w + (i & 1) * (WH * PW);
 
         // ---------------- phase A: w_i = phi_i(k_i * u) on the tile + r halo
-        for (int base = warp * 32; base < Tl::NRUN; base += NT) {
-            const bool valid = base + lane < Tl::NRUN;
-            const int run = valid ? base + lane : Tl::NRUN - 1;
-            const int wr = run / Tl::RUNS_ROW;
-            const int wc = (run - wr * Tl::RUNS_ROW) * 4;
-            float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        for (int base = warp * 32; base < NRUN; base += NT) {
+            const bool valid = base + lane < NRUN;
+            const int run = valid ? base + lane : NRUN - 1;
+            const int wr = run / RPR;
+            const int wc = (run - wr * RPR) * RUNW;
+            f2 v[RUNW];
+#pragma unroll
+            for (int e = 0; e < RUNW; ++e) v[e] = 0ull;
 #pragma unroll
             for (int ta = 0; ta < K; ++ta) {  // tap row a = ta - R reads u row (py - a)
-                float seg[SEG];
-                load_seg<SEG>(s_u + (wr + 2 * R - ta) * UW + wc, seg);
+                f2 seg[SEG];
+                load_f2<SEG>(s_u + (wr + 2 * R - ta) * PU + wc, seg);
+                float tk[K8];
+                load_taps_row<K>(fpar + ta * K8, tk);
 #pragma unroll
                 for (int tb = 0; tb < K; ++tb) {  // tap col b = tb - R reads u col (px - b)
-                    const float kv = tk[ta * K + tb];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) v[e] = fmaf(kv, seg[e + 2 * R - tb], v[e]);
+                    for (int e = 0; e < RUNW; ++e) v[e] = fma2(seg[e + 2 * R - tb], bc(tk[tb]), v[e]);
                 }
             }
-            float w[4];
-            phi_eval<4>(fpar + KK4, a.mode, v, w);
+            f2 w[RUNW];
+            phi_x2<RUNW>(fpar + KT, a.mode, v, w);
             if (valid) {
-                const int py = y0 - R + wr, px0 = x0 - R + wc;
-                float *wrow = Wb + wr * WW + wc;
-                const bool row_in = (unsigned)py < (unsigned)H;
-                if (row_in && px0 >= 0 && px0 + 3 < W) {
-                    *reinterpret_cast<float4 *>(wrow) = make_float4(w[0], w[1], w[2], w[3]);
-                } else if (row_in) {
+                const int pyA = gA.y0 - R + wr, pyB = gB.y0 - R + wr;
+                const int pxA = gA.x0 - R + wc, pxB = gB.x0 - R + wc;
+                const bool rowA = (unsigned)pyA < (unsigned)H, rowB = (unsigned)pyB < (unsigned)H;
+                f2 *wrow = Wb + wr * PW + wc;
+                if (rowA && rowB && pxA >= 0 && pxA + RUNW <= W && pxB >= 0 && pxB + RUNW <= W) {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        if ((unsigned)(px0 + e) < (unsigned)W) wrow[e] = w[e];
-                }
-                if (border && row_in) {
-                    // mirror partners of in-image positions within r of an edge
-                    const int my = py < R ? -1 - py : (py >= H - R ? 2 * H - 1 - py : INT_MIN);
-                    const int ty = my - (y0 - R);
-                    const bool ym = my != INT_MIN && ty >= 0 && ty < WH;
+                    for (int e = 0; e < RUNW; e += 2)
+                        *reinterpret_cast<ulonglong2 *>(wrow + e) = make_ulonglong2(w[e], w[e + 1]);
+                } else {
+                    float *wf = reinterpret_cast<float *>(wrow);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int px = px0 + e;
-                        if ((unsigned)px >= (unsigned)W) continue;
-                        const int mx = px < R ? -1 - px : (px >= W - R ? 2 * W - 1 - px : INT_MIN);
-                        const int tx = mx - (x0 - R);
-                        const bool xm = mx != INT_MIN && tx >= 0 && tx < WW;
-                        if (xm) Wb[wr * WW + tx] = w[e];
-                        if (ym) Wb[ty * WW + wc + e] = w[e];
-                        if (xm && ym) Wb[ty * WW + tx] = w[e];
+                    for (int e = 0; e < RUNW; ++e) {
+                        if (rowA && (unsigned)(pxA + e) < (unsigned)W) wf[2 * e] = lo(w[e]);
+                        if (rowB && (unsigned)(pxB + e) < (unsigned)W) wf[2 * e + 1] = hi(w[e]);
                     }
+                }
+                float *Wf = reinterpret_cast<float *>(Wb);
+                if (gA.border && rowA) {
+#pragma unroll
+                    for (int e = 0; e < RUNW; ++e)
+                        if ((unsigned)(pxA + e) < (unsigned)W)
+                            mirror_store<R, WH, WWc, PW>(Wf, 0, H, W, gA.y0, gA.x0, wr, wc + e, pyA, pxA + e,
+                                                         lo(w[e]));
+                }
+                if (gB.border && rowB) {
+#pragma unroll
+                    for (int e = 0; e < RUNW; ++e)
+                        if ((unsigned)(pxB + e) < (unsigned)W)
+                            mirror_store<R, WH, WWc, PW>(Wf, 1, H, W, gB.y0, gB.x0, wr, wc + e, pyB, pxB + e,
+                                                         hi(w[e]));
                 }
             }
         }
         __syncthreads();
 
         // ---------------- phase B: acc += kbar_i * w_i (correlation with k_i)
-        if (!r2_edge) {
+        if (!(r2A || r2B)) {
 #pragma unroll
             for (int wrow = 0; wrow < BR + 2 * R; ++wrow) {
-                float seg[SEG];
-                load_seg<SEG>(Wb + (oyl + wrow) * WW + oxl, seg);
+                f2 seg[SEGB];
+                load_f2<SEGB>(Wb + (oyl + wrow) * PW + oxl, seg);
 #pragma unroll
                 for (int ry = 0; ry < BR; ++ry) {
                     const int ta = wrow - ry;  // tap row index a + R
                     if (ta < 0 || ta >= K) continue;
+                    float tk[K8];
+                    load_taps_row<K>(fpar + ta * K8, tk);
 #pragma unroll
-                    for (int tb = 0; tb < K; ++tb) {
-                        const float kv = tk[ta * K + tb];
+                    for (int tb = 0; tb < K; ++tb)
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) acc[ry][e] = fmaf(kv, seg[e + tb], acc[ry][e]);
-                    }
+                        for (int e = 0; e < BC; ++e) acc[ry][e] = fma2(seg[e + tb], bc(tk[tb]), acc[ry][e]);
                 }
             }
         } else {
             // R2 (exact K^T) near an image edge: a tap whose source lies outside the
-            // image uses the tap mirrored in that direction.
-            for (int wrow = 0; wrow < BR + 2 * R; ++wrow) {
-                float seg[SEG];
-                load_seg<SEG>(Wb + (oyl + wrow) * WW + oxl, seg);
-                const int sy = y0 + oyl + wrow - R;  // source row
-                const bool yout = (unsigned)sy >= (unsigned)H;
+            // image uses the tap mirrored in that direction.  Scalar,
+            // per tile half, same operation order as the fast path.
+            const float *Wf = reinterpret_cast<const float *>(Wb);
 #pragma unroll
-                for (int ry = 0; ry < BR; ++ry) {
-                    const int ta = wrow - ry;
-                    if (ta < 0 || ta >= K) continue;
-                    const int tay = yout ? (K - 1 - ta) : ta;
+            for (int h = 0; h < 2; ++h) {
+                const TileGeo &g = h ? gB : gA;
+                const bool r2 = h ? r2B : r2A;
+                float accs[BR][BC];
 #pragma unroll
-                    for (int tb = 0; tb < K; ++tb) {
+                for (int ry = 0; ry < BR; ++ry)
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int sx = x0 + oxl + e + tb - R;
-                            const int tbx = ((unsigned)sx >= (unsigned)W) ? (K - 1 - tb) : tb;
-                            acc[ry][e] = fmaf(fpar[tay * K + tbx], seg[e + tb], acc[ry][e]);
+                    for (int e = 0; e < BC; ++e) accs[ry][e] = h ? hi(acc[ry][e]) : lo(acc[ry][e]);
+                for (int wrow = 0; wrow < BR + 2 * R; ++wrow) {
+                    const int sy = g.y0 + oyl + wrow - R;  // source row
+                    const bool yout = r2 && (unsigned)sy >= (unsigned)H;
+#pragma unroll
+                    for (int ry = 0; ry < BR; ++ry) {
+                        const int ta = wrow - ry;
+                        if (ta < 0 || ta >= K) continue;
+                        const int tay = yout ? (K - 1 - ta) : ta;
+#pragma unroll
+                        for (int tb = 0; tb < K; ++tb) {
+#pragma unroll
+                            for (int e = 0; e < BC; ++e) {
+                                const int sx = g.x0 + oxl + e + tb - R;
+                                const int tbx = (r2 && (unsigned)sx >= (unsigned)W) ? (K - 1 - tb) : tb;
+                                const float wv = Wf[2 * ((oyl + wrow) * PW + oxl + e + tb) + h];
+                                accs[ry][e] = fmaf(fpar[tay * K8 + tbx], wv, accs[ry][e]);
+                            }
                         }
                     }
                 }
+#pragma unroll
+                for (int ry = 0; ry < BR; ++ry)
+#pragma unroll
+                    for (int e = 0; e < BC; ++e)
+                        acc[ry][e] = h ? pk(lo(acc[ry][e]), accs[ry][e]) : pk(accs[ry][e], hi(acc[ry][e]));
             }
         }
     }
 
-    // ---------------- epilogue: ut = u - d, u+ = prox(ut), store
-    const float *fb = a.f.ptr + (long long)b * a.f.img_stride;
-    float *ob = a.u_out + (long long)b * a.out_img_stride;
+    // ---------------- epilogue: ut = u - d, u+ = prox(ut), store (per tile half)
 #pragma unroll
-    for (int ry = 0; ry < BR; ++ry) {
-        const int oy = y0 + oyl + ry;
-        if (oy >= a.y_end) continue;
+    for (int h = 0; h < 2; ++h) {
+        if (h == 1 && !hasB) break;
+        const TileGeo &g = h ? gB : gA;
+        const float *fb = a.f.ptr + (long long)g.b * a.f.img_stride;
+        float *ob = a.u_out + (long long)g.b * a.out_img_stride;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int ox = x0 + oxl + e;
-            if (ox >= W) continue;
-            const float u = s_u[(oyl + ry + 2 * R) * UW + oxl + e + 2 * R];
-            const float fv = __ldg(fb + (long long)(oy - a.f.row_base) * a.f.ld + ox);
-            ob[(long long)(oy - a.out_row_base) * a.out_ld + ox] =
-                prox_poisson(u - acc[ry][e], a.lambda, fv);
+        for (int ry = 0; ry < BR; ++ry) {
+            const int oy = g.y0 + oyl + ry;
+            if (oy >= a.y_end) continue;
+#pragma unroll
+            for (int e = 0; e < BC; ++e) {
+                const int ox = g.x0 + oxl + e;
+                if (ox >= W) continue;
+                const f2 u2 = s_u[(oyl + ry + 2 * R) * PU + oxl + e + 2 * R];
+                const float u = h ? hi(u2) : lo(u2);
+                const float d = h ? hi(acc[ry][e]) : lo(acc[ry][e]);
+                const float fv = __ldg(fb + (long long)(oy - a.f.row_base) * a.f.ld + ox);
+                ob[(long long)(oy - a.out_row_base) * a.out_ld + ox] = prox_poisson(u - d, a.lambda, fv);
+            }
         }
     }
 }
 
-// Tile configurations: 0 = "L" 64x64 output tile, 256 threads, 2 CTAs/SM;
-//                      1 = "S" 32x32 output tile, 128 threads (small images).
-template <int K>
-struct Cfg0 { static constexpr int TW = 64, TH = 64, NT = 256, BR = 4, MINB = 2; };
-template <int K>
-struct Cfg1 { static constexpr int TW = 32, TH = 32, NT = 128, BR = 2, MINB = 4; };
+// Tile configurations: 0 = "L" two 64x64 output tiles, 512 threads, 1 CTA/SM;
+//                      1 = "S" two 32x32 output tiles, 128 threads (small images).
+struct Cfg0 { static constexpr int TW = 64, TH = 64, NT = 512, RUNW = 10, BR = 4, MINB = 1; };
+struct Cfg1 { static constexpr int TW = 32, TH = 32, NT = 128, RUNW = 10, BR = 4, MINB = 3; };
 
 template <int K, class C>
 size_t smem_bytes(int Nk, int pstride) {
-    using Tl = Tile<K, C::TW, C::TH, C::NT, C::BR>;
-    return sizeof(float) * ((size_t)Nk * pstride + Tl::smem_floats_fixed);
+    using Gm = Geo<K, C::TW, C::TH, C::NT, C::RUNW, C::BR>;
+    return sizeof(float) * (size_t)Nk * pstride + sizeof(f2) * (size_t)Gm::smem_f2;
 }
 
 template <int K, class C>
-cudaError_t launch(const StageArgs &a, int B, cudaStream_t s) {
-    auto kern = stage_kernel<K, C::TW, C::TH, C::NT, C::BR, C::MINB>;
+cudaError_t launch(StageArgs &a, int B, cudaStream_t s) {
+    auto kern = stage_kernel<K, C::TW, C::TH, C::NT, C::RUNW, C::BR, C::MINB>;
     const size_t smem = smem_bytes<K, C>(a.Nk, a.pstride);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((a.W + C::TW - 1) / C::TW, (a.y_end - a.y_begin + C::TH - 1) / C::TH, B);
-    kern<<<grid, C::NT, smem, s>>>(a);
+    a.tiles_x = (a.W + C::TW - 1) / C::TW;
+    a.tiles_y = (a.y_end - a.y_begin + C::TH - 1) / C::TH;
+    const long long n = (long long)B * a.tiles_x * a.tiles_y;
+    if (n > INT_MAX - 1) return cudaErrorInvalidValue;
+    a.n_tiles = (int)n;
+    kern<<<(unsigned)((n + 1) / 2), C::NT, smem, s>>>(a);
     return cudaGetLastError();
 }
 
 __global__ void debug_phi_kernel(const float *__restrict__ fp, int mode, const float *__restrict__ v,
                                  float *__restrict__ out, long long n) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    float vv[1] = {i < n ? v[i] : 0.0f};
-    float ww[1];
-    phi_eval<1>(fp, mode, vv, ww);  // every lane participates (warp-collective)
-    if (i < n) out[i] = ww[0];
+    // each thread evaluates a pair (elements 2t, 2t+1) through the stage kernel's phi_x2
+    const long long i = 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+    f2 vv[1] = {pk(i < n ? v[i] : 0.0f, i + 1 < n ? v[i + 1] : 0.0f)};
+    f2 ww[1];
+    phi_x2<1>(fp, mode, vv, ww);  // every lane participates (warp-collective)
+    if (i < n) out[i] = lo(ww[0]);
+    if (i + 1 < n) out[i + 1] = hi(ww[0]);
 }
 
 __global__ void debug_prox_kernel(const float *ut, const float *f, float lam, float *out, long long n) {
@@ -367,40 +513,40 @@ __global__ void debug_prox_kernel(const float *ut, const float *f, float lam, fl
 
 size_t stage_smem_bytes(int ksize, int tile, int Nk, int pstride) {
     switch (ksize * 2 + tile) {
-        case 6: return smem_bytes<3, Cfg0<3>>(Nk, pstride);
-        case 7: return smem_bytes<3, Cfg1<3>>(Nk, pstride);
-        case 10: return smem_bytes<5, Cfg0<5>>(Nk, pstride);
-        case 11: return smem_bytes<5, Cfg1<5>>(Nk, pstride);
-        case 14: return smem_bytes<7, Cfg0<7>>(Nk, pstride);
-        case 15: return smem_bytes<7, Cfg1<7>>(Nk, pstride);
+        case 6: return smem_bytes<3, Cfg0>(Nk, pstride);
+        case 7: return smem_bytes<3, Cfg1>(Nk, pstride);
+        case 10: return smem_bytes<5, Cfg0>(Nk, pstride);
+        case 11: return smem_bytes<5, Cfg1>(Nk, pstride);
+        case 14: return smem_bytes<7, Cfg0>(Nk, pstride);
+        case 15: return smem_bytes<7, Cfg1>(Nk, pstride);
     }
     return 0;
 }
 
 int choose_tile(int ksize, int B, int H, int W, int num_sms) {
     (void)ksize;
-    const long long big = (long long)B * ((H + 63) / 64) * ((W + 63) / 64);
-    return big >= 2LL * num_sms ? 0 : 1;
+    // "L" when its tile pairs fill every SM at least twice, else the small tiles
+    const long long pairs = ((long long)B * ((H + 63) / 64) * ((W + 63) / 64) + 1) / 2;
+    return pairs >= 2LL * num_sms ? 0 : 1;
 }
 
-cudaError_t launch_stage(int ksize, int tile, const StageArgs &a, int B, cudaStream_t s) {
+cudaError_t launch_stage(int ksize, int tile, StageArgs &a, int B, cudaStream_t s) {
     switch (ksize * 2 + tile) {
-        case 6: return launch<3, Cfg0<3>>(a, B, s);
-        case 7: return launch<3, Cfg1<3>>(a, B, s);
-        case 10: return launch<5, Cfg0<5>>(a, B, s);
-        case 11: return launch<5, Cfg1<5>>(a, B, s);
-        case 14: return launch<7, Cfg0<7>>(a, B, s);
-        case 15: return launch<7, Cfg1<7>>(a, B, s);
+        case 6: return launch<3, Cfg0>(a, B, s);
+        case 7: return launch<3, Cfg1>(a, B, s);
+        case 10: return launch<5, Cfg0>(a, B, s);
+        case 11: return launch<5, Cfg1>(a, B, s);
+        case 14: return launch<7, Cfg0>(a, B, s);
+        case 15: return launch<7, Cfg1>(a, B, s);
     }
     return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_debug_phi(const float *params, int pstride, int mode, int ksize, int i,
                              const float *v, float *out, long long n, cudaStream_t s) {
-    const int KK4 = (ksize * ksize + 3) / 4 * 4;
-    const float *fp = params + (long long)i * pstride + KK4;
+    const float *fp = params + (long long)i * pstride + tap_floats(ksize);
     const int threads = 256;
-    const long long blocks = (n + threads - 1) / threads;
+    const long long blocks = ((n + 1) / 2 + threads - 1) / threads;
     if (blocks > 0) debug_phi_kernel<<<(unsigned)blocks, threads, 0, s>>>(fp, mode, v, out, n);
     return cudaGetLastError();
 }
