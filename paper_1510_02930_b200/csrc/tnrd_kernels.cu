@@ -85,6 +85,15 @@ __device__ __forceinline__ float warp_max(float x) {
     return r;
 }
 
+// Named CTA barriers for the producer/consumer hand-off of the w slots.
+// bar.arrive does not wait; both order the participants' shared-memory accesses.
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 // Half-sample symmetric index (S l.73), single reflection, clamped for safety.
 __device__ __forceinline__ int reflect(int x, int n) {
     x = x < 0 ? -1 - x : x;
@@ -179,8 +188,11 @@ __device__ __forceinline__ void phi_x2(const float *__restrict__ fp, int mode, c
 // pitch p >= need (in float2) with p == r (mod 16)
 constexpr int pitch_mod16(int need, int r) { return need + (((r - need) % 16) + 16) % 16; }
 
-template <int K, int TW, int TH, int NT, int RUNW, int BR>
+template <int K_, int TW, int TH, int NT, int RUNW_, int BR_>
 struct Geo {
+    static constexpr int K = K_, RUNW = RUNW_, BR = BR_;
+    static constexpr int NX = NT / 2;                             // X threads: convolutions
+    static constexpr int NY = NT / 2;                             // Y threads: phi
     static constexpr int R = K / 2;
     static constexpr int K8 = tap_pitch(K);
     static constexpr int KT = tap_floats(K);
@@ -202,10 +214,10 @@ struct Geo {
     static constexpr int NBY = TH / BR;
     static_assert(RUNW == 10, "pitch rule assumes RUNW = 10");
     static_assert(SEG % 2 == 0 && SEGB % 2 == 0, "whole 16-byte segments");
-    static_assert(NBX * NBY == NT, "exactly one phase-B block per thread");
+    static_assert(NBX * NBY == NX, "exactly one phase-B block per X thread");
     static_assert(NBX % 8 == 0, "a quarter warp stays in one phase-B row");
     static_assert(NT % 32 == 0, "whole warps");
-    static constexpr int smem_f2 = UH * PU + 2 * WH * PW;
+    static constexpr int smem_f2 = UH * PU + 3 * WH * PW;  // u + 3 v/w slots
 };
 
 template <int N>
@@ -259,22 +271,183 @@ __device__ __forceinline__ void mirror_store(float *Wf, int h, int H, int W, int
     if (xm && ym) Wf[2 * (ty * PW + tx) + h] = val;
 }
 
-template <int K, int TW, int TH, int NT, int RUNW, int BR, int MINB>
+// Forward filter bank of filter i (X threads xt in [0, NX)): v_i = k_i * u on
+// the tile + r halo of both tiles, every region position, into the slot Vb.
+template <class G>
+__device__ __forceinline__ void phase_conv(const float *__restrict__ fpar, const f2 *s_u, f2 *Vb, int xt) {
+    constexpr int K = G::K, R = G::R, K8 = G::K8, RUNW = G::RUNW;
+    constexpr int RPR = G::RPR, NRUN = G::NRUN, PU = G::PU, PW = G::PW, SEG = G::SEG;
+    for (int run = xt; run < NRUN; run += G::NX) {
+        const int wr = run / RPR;
+        const int wc = (run - wr * RPR) * RUNW;
+        f2 v[RUNW];
+#pragma unroll
+        for (int e = 0; e < RUNW; ++e) v[e] = 0ull;
+#pragma unroll
+        for (int ta = 0; ta < K; ++ta) {  // tap row a = ta - R reads u row (py - a)
+            f2 seg[SEG];
+            load_f2<SEG>(s_u + (wr + 2 * R - ta) * PU + wc, seg);
+            float tk[K8];
+            load_taps_row<K>(fpar + ta * K8, tk);
+#pragma unroll
+            for (int tb = 0; tb < K; ++tb) {  // tap col b = tb - R reads u col (px - b)
+#pragma unroll
+                for (int e = 0; e < RUNW; ++e) v[e] = fma2(seg[e + 2 * R - tb], bc(tk[tb]), v[e]);
+            }
+        }
+        f2 *vrow = Vb + wr * PW + wc;
+#pragma unroll
+        for (int e = 0; e < RUNW; e += 2)
+            *reinterpret_cast<ulonglong2 *>(vrow + e) = make_ulonglong2(v[e], v[e + 1]);
+    }
+}
+
+// Influence of filter i (Y threads yt in [0, NY)), in place on the slot:
+// w_i = phi_i(v_i) at in-image positions, plus the R1 mirror partners of
+// in-image positions within r of an edge (out-of-image slots, which no run
+// reads as an in-image v).  Warp-collective per run.
+template <class G>
+__device__ __forceinline__ void phase_phi(const StageArgs &a, const TileGeo &gA, const TileGeo &gB,
+                                          const float *__restrict__ fpar, f2 *Wb, int yt) {
+    constexpr int R = G::R, KT = G::KT, RUNW = G::RUNW;
+    constexpr int WWc = G::WWc, RPR = G::RPR, WH = G::WH, NRUN = G::NRUN, PW = G::PW;
+    const int lane = yt & 31, ywarp = yt >> 5;
+    const int H = a.H, W = a.W;
+    for (int base = ywarp * 32; base < NRUN; base += G::NY) {
+        const bool valid = base + lane < NRUN;
+        const int run = valid ? base + lane : NRUN - 1;
+        const int wr = run / RPR;
+        const int wc = (run - wr * RPR) * RUNW;
+        f2 *wrow = Wb + wr * PW + wc;
+        f2 v[RUNW];
+        load_f2<RUNW>(wrow, v);
+        f2 w[RUNW];
+        phi_x2<RUNW>(fpar + KT, a.mode, v, w);
+        if (valid) {
+            const int pyA = gA.y0 - R + wr, pyB = gB.y0 - R + wr;
+            const int pxA = gA.x0 - R + wc, pxB = gB.x0 - R + wc;
+            const bool rowA = (unsigned)pyA < (unsigned)H, rowB = (unsigned)pyB < (unsigned)H;
+            if (rowA && rowB && pxA >= 0 && pxA + RUNW <= W && pxB >= 0 && pxB + RUNW <= W) {
+#pragma unroll
+                for (int e = 0; e < RUNW; e += 2)
+                    *reinterpret_cast<ulonglong2 *>(wrow + e) = make_ulonglong2(w[e], w[e + 1]);
+            } else {
+                float *wf = reinterpret_cast<float *>(wrow);
+#pragma unroll
+                for (int e = 0; e < RUNW; ++e) {
+                    if (rowA && (unsigned)(pxA + e) < (unsigned)W) wf[2 * e] = lo(w[e]);
+                    if (rowB && (unsigned)(pxB + e) < (unsigned)W) wf[2 * e + 1] = hi(w[e]);
+                }
+            }
+            float *Wf = reinterpret_cast<float *>(Wb);
+            if (gA.border && rowA) {
+#pragma unroll
+                for (int e = 0; e < RUNW; ++e)
+                    if ((unsigned)(pxA + e) < (unsigned)W)
+                        mirror_store<R, WH, WWc, PW>(Wf, 0, H, W, gA.y0, gA.x0, wr, wc + e, pyA, pxA + e, lo(w[e]));
+            }
+            if (gB.border && rowB) {
+#pragma unroll
+                for (int e = 0; e < RUNW; ++e)
+                    if ((unsigned)(pxB + e) < (unsigned)W)
+                        mirror_store<R, WH, WWc, PW>(Wf, 1, H, W, gB.y0, gB.x0, wr, wc + e, pyB, pxB + e, hi(w[e]));
+            }
+        }
+    }
+}
+
+// Phase B for filter i (consumer threads): acc += kbar_i * w_i on the thread's
+// BR x BC pair block at (oyl, oxl) -- a correlation of the w slot with k_i.
+template <class G>
+__device__ __forceinline__ void phase_b(const StageArgs &a, const TileGeo &gA, const TileGeo &gB, bool r2A,
+                                        bool r2B, const float *__restrict__ fpar, const f2 *Wb, int oyl, int oxl,
+                                        f2 (&acc)[G::BR][G::BC]) {
+    constexpr int K = G::K, R = G::R, K8 = G::K8, BR = G::BR, BC = G::BC, PW = G::PW, SEGB = G::SEGB;
+    if (!(r2A || r2B)) {
+#pragma unroll
+        for (int wrow = 0; wrow < BR + 2 * R; ++wrow) {
+            f2 seg[SEGB];
+            load_f2<SEGB>(Wb + (oyl + wrow) * PW + oxl, seg);
+#pragma unroll
+            for (int ry = 0; ry < BR; ++ry) {
+                const int ta = wrow - ry;  // tap row index a + R
+                if (ta < 0 || ta >= K) continue;
+                float tk[K8];
+                load_taps_row<K>(fpar + ta * K8, tk);
+#pragma unroll
+                for (int tb = 0; tb < K; ++tb)
+#pragma unroll
+                    for (int e = 0; e < BC; ++e) acc[ry][e] = fma2(seg[e + tb], bc(tk[tb]), acc[ry][e]);
+            }
+        }
+        return;
+    }
+    // R2 (exact K^T) near an image edge: a tap whose source lies outside the
+    // image uses the tap mirrored in that direction.  Scalar,
+    // per tile half, same operation order as the fast path.
+    const int H = a.H, W = a.W;
+    const float *Wf = reinterpret_cast<const float *>(Wb);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const TileGeo &g = h ? gB : gA;
+        const bool r2 = h ? r2B : r2A;
+        float accs[BR][BC];
+#pragma unroll
+        for (int ry = 0; ry < BR; ++ry)
+#pragma unroll
+            for (int e = 0; e < BC; ++e) accs[ry][e] = h ? hi(acc[ry][e]) : lo(acc[ry][e]);
+        for (int wrow = 0; wrow < BR + 2 * R; ++wrow) {
+            const int sy = g.y0 + oyl + wrow - R;  // source row
+            const bool yout = r2 && (unsigned)sy >= (unsigned)H;
+#pragma unroll
+            for (int ry = 0; ry < BR; ++ry) {
+                const int ta = wrow - ry;
+                if (ta < 0 || ta >= K) continue;
+                const int tay = yout ? (K - 1 - ta) : ta;
+#pragma unroll
+                for (int tb = 0; tb < K; ++tb) {
+#pragma unroll
+                    for (int e = 0; e < BC; ++e) {
+                        const int sx = g.x0 + oxl + e + tb - R;
+                        const int tbx = (r2 && (unsigned)sx >= (unsigned)W) ? (K - 1 - tb) : tb;
+                        const float wv = Wf[2 * ((oyl + wrow) * PW + oxl + e + tb) + h];
+                        accs[ry][e] = fmaf(fpar[tay * K8 + tbx], wv, accs[ry][e]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int ry = 0; ry < BR; ++ry)
+#pragma unroll
+            for (int e = 0; e < BC; ++e)
+                acc[ry][e] = h ? pk(lo(acc[ry][e]), accs[ry][e]) : pk(accs[ry][e], hi(acc[ry][e]));
+    }
+}
+
+// Warp-specialised stage kernel.  Warps [0, NT/2) are "X":
+// the FMA-only work -- forward filter bank of filter i+1 into slot (i+1)%3,
+// then the adjoint of filter i from slot i%3, then the epilogue.  Warps
+// [NT/2, NT) are "Y": the MUFU-heavy phi of filter i, in place on slot i%3.
+// Named barriers: VFULL_s (X arrive, Y wait) and WFULL_s (Y arrive, X wait).
+// Three slots need no "empty" barrier: X rewrites slot (i+1)%3 only after its
+// own WFULL wait of iteration i-1, i.e. after every X thread finished the
+// adjoint of filter i-2 that read it, and Y touches a slot only between its
+// VFULL and WFULL.  So phi(i) runs concurrently with conv(i+1) + adjoint(i-1).
+template <int K_, int TW, int TH, int NT, int RUNW_, int BR_, int MINB>
 __global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__ StageArgs a) {
-    using G = Geo<K, TW, TH, NT, RUNW, BR>;
-    constexpr int R = G::R, K8 = G::K8, KT = G::KT, BC = G::BC;
-    constexpr int WWc = G::WWc, RPR = G::RPR, WH = G::WH, NRUN = G::NRUN, UH = G::UH, UWc = G::UWc;
-    constexpr int PU = G::PU, PW = G::PW, SEG = G::SEG, SEGB = G::SEGB;
+    using G = Geo<K_, TW, TH, NT, RUNW_, BR_>;
+    constexpr int R = G::R, BR = G::BR, BC = G::BC;
+    constexpr int UH = G::UH, UWc = G::UWc, PU = G::PU, SLOT = G::WH * G::PW;
+    constexpr int BAR_VFULL = 1, BAR_WFULL = 4;  // ids 1-3 and 4-6 (0 = __syncthreads)
 
     extern __shared__ float4 smem4[];
     float *s_par = reinterpret_cast<float *>(smem4);
     f2 *s_u = reinterpret_cast<f2 *>(s_par + a.Nk * a.pstride);
-    f2 *s_w = s_u + UH * PU;
+    f2 *s_w = s_u + UH * PU;  // 3 slots
 
     const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const int warp = tid >> 5;
     const int H = a.H, W = a.W;
+    const int Nk = a.Nk;
 
     const int tA = 2 * blockIdx.x;
     const bool hasB = tA + 1 < a.n_tiles;
@@ -284,7 +457,7 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__
     // ---- stage parameters -> smem (float4 copy)
     {
         const float4 *src = reinterpret_cast<const float4 *>(a.params);
-        const int n4 = a.Nk * a.pstride / 4;
+        const int n4 = Nk * a.pstride / 4;
         for (int j = tid; j < n4; j += NT) smem4[j] = __ldg(src + j);
     }
     // ---- u of both tiles (tile + 2r halo), half-sample mirror at the image edges
@@ -304,8 +477,21 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__
     }
     __syncthreads();
 
-    // phase-B block of this thread: BR rows x BC pair-columns at (oyl, oxl) in the tile
-    const int oyl = (tid / G::NBX) * BR, oxl = (tid % G::NBX) * BC;
+    if (tid >= G::NX) {
+        // ======================= Y: phi in place, filter by filter
+        const int yt = tid - G::NX;
+        for (int i = 0; i < Nk; ++i) {
+            const int slot = i % 3;
+            named_sync(BAR_VFULL + slot, NT);
+            phase_phi<G>(a, gA, gB, s_par + i * a.pstride, s_w + slot * SLOT, yt);
+            named_arrive(BAR_WFULL + slot, NT);
+        }
+        return;
+    }
+
+    // ======================= X: forward conv (i+1), adjoint (i), epilogue
+    const int xt = tid;
+    const int oyl = (xt / G::NBX) * BR, oxl = (xt % G::NBX) * BC;
     const auto r2_edge = [&](const TileGeo &g) {
         return (a.boundary == 1) && ((g.x0 + oxl - R < 0) || (g.x0 + oxl + BC + R > W) ||
                                      (g.y0 + oyl - R < 0) || (g.y0 + oyl + BR + R > H));
@@ -318,128 +504,17 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__
 #pragma unroll
         for (int e = 0; e < BC; ++e) acc[ry][e] = 0ull;
 
-    for (int i = 0; i < a.Nk; ++i) {
-        const float *fpar = s_par + i * a.pstride;
-        f2 *Wb = s_w + (i & 1) * (WH * PW);
-
-        // ---------------- phase A: w_i = phi_i(k_i * u) on the tile + r halo
-        for (int base = warp * 32; base < NRUN; base += NT) {
-            const bool valid = base + lane < NRUN;
-            const int run = valid ? base + lane : NRUN - 1;
-            const int wr = run / RPR;
-            const int wc = (run - wr * RPR) * RUNW;
-            f2 v[RUNW];
-#pragma unroll
-            for (int e = 0; e < RUNW; ++e) v[e] = 0ull;
-#pragma unroll
-            for (int ta = 0; ta < K; ++ta) {  // tap row a = ta - R reads u row (py - a)
-                f2 seg[SEG];
-                load_f2<SEG>(s_u + (wr + 2 * R - ta) * PU + wc, seg);
-                float tk[K8];
-                load_taps_row<K>(fpar + ta * K8, tk);
-#pragma unroll
-                for (int tb = 0; tb < K; ++tb) {  // tap col b = tb - R reads u col (px - b)
-#pragma unroll
-                    for (int e = 0; e < RUNW; ++e) v[e] = fma2(seg[e + 2 * R - tb], bc(tk[tb]), v[e]);
-                }
-            }
-            f2 w[RUNW];
-            phi_x2<RUNW>(fpar + KT, a.mode, v, w);
-            if (valid) {
-                const int pyA = gA.y0 - R + wr, pyB = gB.y0 - R + wr;
-                const int pxA = gA.x0 - R + wc, pxB = gB.x0 - R + wc;
-                const bool rowA = (unsigned)pyA < (unsigned)H, rowB = (unsigned)pyB < (unsigned)H;
-                f2 *wrow = Wb + wr * PW + wc;
-                if (rowA && rowB && pxA >= 0 && pxA + RUNW <= W && pxB >= 0 && pxB + RUNW <= W) {
-#pragma unroll
-                    for (int e = 0; e < RUNW; e += 2)
-                        *reinterpret_cast<ulonglong2 *>(wrow + e) = make_ulonglong2(w[e], w[e + 1]);
-                } else {
-                    float *wf = reinterpret_cast<float *>(wrow);
-#pragma unroll
-                    for (int e = 0; e < RUNW; ++e) {
-                        if (rowA && (unsigned)(pxA + e) < (unsigned)W) wf[2 * e] = lo(w[e]);
-                        if (rowB && (unsigned)(pxB + e) < (unsigned)W) wf[2 * e + 1] = hi(w[e]);
-                    }
-                }
-                float *Wf = reinterpret_cast<float *>(Wb);
-                if (gA.border && rowA) {
-#pragma unroll
-                    for (int e = 0; e < RUNW; ++e)
-                        if ((unsigned)(pxA + e) < (unsigned)W)
-                            mirror_store<R, WH, WWc, PW>(Wf, 0, H, W, gA.y0, gA.x0, wr, wc + e, pyA, pxA + e,
-                                                         lo(w[e]));
-                }
-                if (gB.border && rowB) {
-#pragma unroll
-                    for (int e = 0; e < RUNW; ++e)
-                        if ((unsigned)(pxB + e) < (unsigned)W)
-                            mirror_store<R, WH, WWc, PW>(Wf, 1, H, W, gB.y0, gB.x0, wr, wc + e, pyB, pxB + e,
-                                                         hi(w[e]));
-                }
-            }
+    phase_conv<G>(s_par, s_u, s_w, xt);
+    named_arrive(BAR_VFULL + 0, NT);
+    for (int i = 0; i < Nk; ++i) {
+        if (i + 1 < Nk) {
+            const int nslot = (i + 1) % 3;
+            phase_conv<G>(s_par + (i + 1) * a.pstride, s_u, s_w + nslot * SLOT, xt);
+            named_arrive(BAR_VFULL + nslot, NT);
         }
-        __syncthreads();
-
-        // ---------------- phase B: acc += kbar_i * w_i (correlation with k_i)
-        if (!(r2A || r2B)) {
-#pragma unroll
-            for (int wrow = 0; wrow < BR + 2 * R; ++wrow) {
-                f2 seg[SEGB];
-                load_f2<SEGB>(Wb + (oyl + wrow) * PW + oxl, seg);
-#pragma unroll
-                for (int ry = 0; ry < BR; ++ry) {
-                    const int ta = wrow - ry;  // tap row index a + R
-                    if (ta < 0 || ta >= K) continue;
-                    float tk[K8];
-                    load_taps_row<K>(fpar + ta * K8, tk);
-#pragma unroll
-                    for (int tb = 0; tb < K; ++tb)
-#pragma unroll
-                        for (int e = 0; e < BC; ++e) acc[ry][e] = fma2(seg[e + tb], bc(tk[tb]), acc[ry][e]);
-                }
-            }
-        } else {
-            // R2 (exact K^T) near an image edge: a tap whose source lies outside the
-            // image uses the tap mirrored in that direction.  Scalar,
-            // per tile half, same operation order as the fast path.
-            const float *Wf = reinterpret_cast<const float *>(Wb);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const TileGeo &g = h ? gB : gA;
-                const bool r2 = h ? r2B : r2A;
-                float accs[BR][BC];
-#pragma unroll
-                for (int ry = 0; ry < BR; ++ry)
-#pragma unroll
-                    for (int e = 0; e < BC; ++e) accs[ry][e] = h ? hi(acc[ry][e]) : lo(acc[ry][e]);
-                for (int wrow = 0; wrow < BR + 2 * R; ++wrow) {
-                    const int sy = g.y0 + oyl + wrow - R;  // source row
-                    const bool yout = r2 && (unsigned)sy >= (unsigned)H;
-#pragma unroll
-                    for (int ry = 0; ry < BR; ++ry) {
-                        const int ta = wrow - ry;
-                        if (ta < 0 || ta >= K) continue;
-                        const int tay = yout ? (K - 1 - ta) : ta;
-#pragma unroll
-                        for (int tb = 0; tb < K; ++tb) {
-#pragma unroll
-                            for (int e = 0; e < BC; ++e) {
-                                const int sx = g.x0 + oxl + e + tb - R;
-                                const int tbx = (r2 && (unsigned)sx >= (unsigned)W) ? (K - 1 - tb) : tb;
-                                const float wv = Wf[2 * ((oyl + wrow) * PW + oxl + e + tb) + h];
-                                accs[ry][e] = fmaf(fpar[tay * K8 + tbx], wv, accs[ry][e]);
-                            }
-                        }
-                    }
-                }
-#pragma unroll
-                for (int ry = 0; ry < BR; ++ry)
-#pragma unroll
-                    for (int e = 0; e < BC; ++e)
-                        acc[ry][e] = h ? pk(lo(acc[ry][e]), accs[ry][e]) : pk(accs[ry][e], hi(acc[ry][e]));
-            }
-        }
+        const int slot = i % 3;
+        named_sync(BAR_WFULL + slot, NT);  // phi of filter i done
+        phase_b<G>(a, gA, gB, r2A, r2B, s_par + i * a.pstride, s_w + slot * SLOT, oyl, oxl, acc);
     }
 
     // ---------------- epilogue: ut = u - d, u+ = prox(ut), store (per tile half)
@@ -469,8 +544,8 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__
 
 // Tile configurations: 0 = "L" two 64x64 output tiles, 512 threads, 1 CTA/SM;
 //                      1 = "S" two 32x32 output tiles, 128 threads (small images).
-struct Cfg0 { static constexpr int TW = 64, TH = 64, NT = 512, RUNW = 10, BR = 4, MINB = 1; };
-struct Cfg1 { static constexpr int TW = 32, TH = 32, NT = 128, RUNW = 10, BR = 4, MINB = 3; };
+struct Cfg0 { static constexpr int TW = 64, TH = 64, NT = 512, RUNW = 10, BR = 8, MINB = 1; };
+struct Cfg1 { static constexpr int TW = 32, TH = 32, NT = 128, RUNW = 10, BR = 8, MINB = 3; };
 
 template <int K, class C>
 size_t smem_bytes(int Nk, int pstride) {
