@@ -339,15 +339,17 @@ __device__ __forceinline__ void phase_phi(const StageArgs &a, const TileGeo &gA,
                     if (rowB && (unsigned)(pxB + e) < (unsigned)W) wf[2 * e + 1] = hi(w[e]);
                 }
             }
+            // mirror partners exist only for runs that reach within r of an edge
+            const auto near_edge = [&](int py, int px) {
+                return py < R || py >= H - R || px < R || px + RUNW > W - R;
+            };
             float *Wf = reinterpret_cast<float *>(Wb);
-            if (gA.border && rowA) {
-#pragma unroll
+            if (gA.border && rowA && near_edge(pyA, pxA)) {
                 for (int e = 0; e < RUNW; ++e)
                     if ((unsigned)(pxA + e) < (unsigned)W)
                         mirror_store<R, WH, WWc, PW>(Wf, 0, H, W, gA.y0, gA.x0, wr, wc + e, pyA, pxA + e, lo(w[e]));
             }
-            if (gB.border && rowB) {
-#pragma unroll
+            if (gB.border && rowB && near_edge(pyB, pxB)) {
                 for (int e = 0; e < RUNW; ++e)
                     if ((unsigned)(pxB + e) < (unsigned)W)
                         mirror_store<R, WH, WWc, PW>(Wf, 1, H, W, gB.y0, gB.x0, wr, wc + e, pyB, pxB + e, hi(w[e]));
@@ -364,6 +366,9 @@ __device__ __forceinline__ void phase_b(const StageArgs &a, const TileGeo &gA, c
                                         f2 (&acc)[G::BR][G::BC]) {
     constexpr int K = G::K, R = G::R, K8 = G::K8, BR = G::BR, BC = G::BC, PW = G::PW, SEGB = G::SEGB;
     if (!(r2A || r2B)) {
+        float tk[K][K8];  // all taps of filter i, loaded once
+#pragma unroll
+        for (int ta = 0; ta < K; ++ta) load_taps_row<K>(fpar + ta * K8, tk[ta]);
 #pragma unroll
         for (int wrow = 0; wrow < BR + 2 * R; ++wrow) {
             f2 seg[SEGB];
@@ -372,12 +377,10 @@ __device__ __forceinline__ void phase_b(const StageArgs &a, const TileGeo &gA, c
             for (int ry = 0; ry < BR; ++ry) {
                 const int ta = wrow - ry;  // tap row index a + R
                 if (ta < 0 || ta >= K) continue;
-                float tk[K8];
-                load_taps_row<K>(fpar + ta * K8, tk);
 #pragma unroll
                 for (int tb = 0; tb < K; ++tb)
 #pragma unroll
-                    for (int e = 0; e < BC; ++e) acc[ry][e] = fma2(seg[e + tb], bc(tk[tb]), acc[ry][e]);
+                    for (int e = 0; e < BC; ++e) acc[ry][e] = fma2(seg[e + tb], bc(tk[ta][tb]), acc[ry][e]);
             }
         }
         return;
