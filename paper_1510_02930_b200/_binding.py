@@ -18,7 +18,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtnrd.so")
+LIB_PATH = os.environ.get("TNRD_LIB_OVERRIDE") or os.path.join(_HERE, "libtnrd.so")  # override: dev experiments only
 
 TNRD_OK = 0
 STATUS = {0: "TNRD_OK", 1: "TNRD_EINVAL", 2: "TNRD_ESTATE", 3: "TNRD_ENOMEM", 4: "TNRD_ECUDA",

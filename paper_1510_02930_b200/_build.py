@@ -34,17 +34,18 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in srcs)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()) -> str:
+    """Compile libtnrd.so (`defines`/`out`: experiment variants, never the product)."""
+    if out == OUT and not defines and not force and not _stale():
         return OUT
     os.makedirs(BUILD, exist_ok=True)
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", nccl_include()]
     common = ["nvcc", "-std=c++17", "-O3", "-Xcompiler", "-fPIC,-fvisibility=hidden"] + inc
     objs = []
     ptxas_log = []
-    for src, extra in [("tnrd_kernels.cu", ARCH + ["-lineinfo", "-fmad=false", "-Xptxas", "-v"]),
+    for src, extra in [("tnrd_kernels.cu", ARCH + ["-lineinfo", "-fmad=false", "-Xptxas", "-v"] + ["-D" + d for d in defines]),
                        ("tnrd_api.cpp", [])]:
-        obj = os.path.join(BUILD, src + ".o")
+        obj = os.path.join(BUILD, src + ("." + "_".join(defines) if defines else "") + ".o")
         cmd = common + extra + ["-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -52,7 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed on {src}")
         ptxas_log.append(r.stderr)
         objs.append(obj)
-    cmd = ["nvcc", "-shared"] + ARCH + ["-o", OUT] + objs + ["-ldl"]
+    cmd = ["nvcc", "-shared"] + ARCH + ["-o", out] + objs + ["-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
@@ -61,7 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         fh.write("".join(ptxas_log))
     if verbose:
         print("".join(ptxas_log))
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

@@ -94,6 +94,13 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// Warpgroup register rebalancing (sm_90a+): the X warpgroups hand registers
+// to the Y warpgroups, whose phi keeps all RUNW Horner chains in flight.
+template <int N>
+__device__ __forceinline__ void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
+template <int N>
+__device__ __forceinline__ void regs_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
+
 // Half-sample symmetric index (S l.73), single reflection, clamped for safety.
 __device__ __forceinline__ int reflect(int x, int n) {
     x = x < 0 ? -1 - x : x;
@@ -322,7 +329,12 @@ __device__ __forceinline__ void phase_phi(const StageArgs &a, const TileGeo &gA,
         f2 v[RUNW];
         load_f2<RUNW>(wrow, v);
         f2 w[RUNW];
+#ifdef TNRD_EXP_NOPHI
+#pragma unroll
+        for (int e = 0; e < RUNW; ++e) w[e] = v[e];
+#else
         phi_x2<RUNW>(fpar + KT, a.mode, v, w);
+#endif
         if (valid) {
             const int pyA = gA.y0 - R + wr, pyB = gB.y0 - R + wr;
             const int pxA = gA.x0 - R + wc, pxB = gB.x0 - R + wc;
@@ -436,8 +448,10 @@ __device__ __forceinline__ void phase_b(const StageArgs &a, const TileGeo &gA, c
 // own WFULL wait of iteration i-1, i.e. after every X thread finished the
 // adjoint of filter i-2 that read it, and Y touches a slot only between its
 // VFULL and WFULL.  So phi(i) runs concurrently with conv(i+1) + adjoint(i-1).
-template <int K_, int TW, int TH, int NT, int RUNW_, int BR_, int MINB>
+template <int K_, int TW, int TH, int NT, int RUNW_, int BR_, int MINB, int REG_X, int REG_Y>
 __global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__ StageArgs a) {
+    static_assert(REG_X == 0 || (NT / 2) % 128 == 0, "setmaxnreg works on whole warpgroups");
+    static_assert(REG_X == 0 || (NT / 2) * (REG_X + REG_Y) <= 65536, "register file");
     using G = Geo<K_, TW, TH, NT, RUNW_, BR_>;
     constexpr int R = G::R, BR = G::BR, BC = G::BC;
     constexpr int UH = G::UH, UWc = G::UWc, PU = G::PU, SLOT = G::WH * G::PW;
@@ -482,6 +496,7 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__
 
     if (tid >= G::NX) {
         // ======================= Y: phi in place, filter by filter
+        if constexpr (REG_Y > 0) regs_inc<REG_Y>();
         const int yt = tid - G::NX;
         for (int i = 0; i < Nk; ++i) {
             const int slot = i % 3;
@@ -493,6 +508,7 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__
     }
 
     // ======================= X: forward conv (i+1), adjoint (i), epilogue
+    if constexpr (REG_X > 0) regs_dec<REG_X>();
     const int xt = tid;
     const int oyl = (xt / G::NBX) * BR, oxl = (xt % G::NBX) * BC;
     const auto r2_edge = [&](const TileGeo &g) {
@@ -512,12 +528,16 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__
     for (int i = 0; i < Nk; ++i) {
         if (i + 1 < Nk) {
             const int nslot = (i + 1) % 3;
+#ifndef TNRD_EXP_NOCONV
             phase_conv<G>(s_par + (i + 1) * a.pstride, s_u, s_w + nslot * SLOT, xt);
+#endif
             named_arrive(BAR_VFULL + nslot, NT);
         }
         const int slot = i % 3;
         named_sync(BAR_WFULL + slot, NT);  // phi of filter i done
+#ifndef TNRD_EXP_NOADJ
         phase_b<G>(a, gA, gB, r2A, r2B, s_par + i * a.pstride, s_w + slot * SLOT, oyl, oxl, acc);
+#endif
     }
 
     // ---------------- epilogue: ut = u - d, u+ = prox(ut), store (per tile half)
@@ -547,8 +567,8 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__
 
 // Tile configurations: 0 = "L" two 64x64 output tiles, 512 threads, 1 CTA/SM;
 //                      1 = "S" two 32x32 output tiles, 128 threads (small images).
-struct Cfg0 { static constexpr int TW = 64, TH = 64, NT = 512, RUNW = 10, BR = 8, MINB = 1; };
-struct Cfg1 { static constexpr int TW = 32, TH = 32, NT = 128, RUNW = 10, BR = 8, MINB = 3; };
+struct Cfg0 { static constexpr int TW = 64, TH = 64, NT = 512, RUNW = 10, BR = 8, MINB = 1, REG_X = 0, REG_Y = 0; };  // setmaxnreg 112/144 measured: no gain
+struct Cfg1 { static constexpr int TW = 32, TH = 32, NT = 128, RUNW = 10, BR = 8, MINB = 3, REG_X = 0, REG_Y = 0; };
 
 template <int K, class C>
 size_t smem_bytes(int Nk, int pstride) {
@@ -558,7 +578,7 @@ size_t smem_bytes(int Nk, int pstride) {
 
 template <int K, class C>
 cudaError_t launch(StageArgs &a, int B, cudaStream_t s) {
-    auto kern = stage_kernel<K, C::TW, C::TH, C::NT, C::RUNW, C::BR, C::MINB>;
+    auto kern = stage_kernel<K, C::TW, C::TH, C::NT, C::RUNW, C::BR, C::MINB, C::REG_X, C::REG_Y>;
     const size_t smem = smem_bytes<K, C>(a.Nk, a.pstride);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
