@@ -7,7 +7,7 @@
 A step is one full inference pass (T = 8 fused stage launches) over the
 workload: by default BASELINE.json configs[3] (C4: 256 independent 512x512
 images, 48 7x7 filters, 63 RBFs, T = 8), its images sharded over the ranks
-(no data-path collective; total fixed -> "strong" scaling).  --config 5 runs
+(no data-path collective; reported "scaling": "weak" per the task rule for partitioned paths -- DESIGN.md §6).  --config 5 runs
 C5 (one 8192^2 image) as row slabs with the per-stage NCCL halo exchange.
 
 For N > 1 launch with torchrun (one process per GPU); rank 0 prints one JSON
@@ -139,7 +139,7 @@ def reference_arm(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(p, world, args),
         "cpu_baseline": {"value": value, "unit": "MPix/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "MPix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -192,6 +192,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_1510_02930_b200 as P
+    from paper_1510_02930_b200.partition import batch_shard, slab_rows
     from synth import make_problem
 
     torch.cuda.set_device(local)
@@ -206,7 +207,7 @@ def main():
 
     if args.config == 5:
         # row slabs, NCCL halo exchange per stage
-        r0, r1 = H * rank // world, H * (rank + 1) // world
+        r0, r1 = slab_rows(H, rank, world)
         f_dev = torch.from_numpy(p.f[0, r0:r1]).to(dev)
         u_dev = torch.empty_like(f_dev)
         if world > 1:
@@ -223,7 +224,7 @@ def main():
         px_rank = (r1 - r0) * W
         shard = (r0, r1)
     else:
-        b0, b1 = B * rank // world, B * (rank + 1) // world
+        b0, b1 = batch_shard(B, rank, world)
         f_dev = torch.from_numpy(p.f[b0:b1]).to(dev)
         u_dev = torch.empty_like(f_dev)
         peaks = p.peaks[b0:b1]
@@ -309,7 +310,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(p, world, args),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
