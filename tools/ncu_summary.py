@@ -68,7 +68,7 @@ def summarize(rep):
         s = {
             "kernel": name[:120],
             "duration_ms": dur,
-            "sm_mhz": num(m, "sm__cycles_elapsed.avg.per_second"),
+            "sm_mhz": (num(m, "sm__cycles_elapsed.avg.per_second") or 0) * {"Ghz": 1e3, "GHz": 1e3, "Mhz": 1.0, "MHz": 1.0, "hz": 1e-6}.get(m.get("sm__cycles_elapsed.avg.per_second", ("", ""))[0], 1.0),
             "regs": num(m, "launch__registers_per_thread"),
             "smem_per_block_kb": (num(m, "launch__shared_mem_per_block_dynamic") or 0) *
                                  {"byte": 1 / 1024, "Kbyte": 1000 / 1024, "Mbyte": 1e6 / 1024}.get(
@@ -101,7 +101,7 @@ def summarize(rep):
                 s[key] *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
         dur_unit = m.get("gpu__time_duration.sum", ("", ""))[0]
         if dur is not None:
-            s["duration_ms"] = dur * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(dur_unit, 1e-6)
+            s["duration_ms"] = dur * {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3, "s": 1e3}.get(dur_unit, 1e-6)
         out.append(s)
     mix = sass_mix(rep)
     return {"launches": out, "sass": mix}
