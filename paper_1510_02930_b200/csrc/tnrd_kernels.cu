@@ -195,36 +195,44 @@ __device__ __forceinline__ void phi_x2(const float *__restrict__ fp, int mode, c
 // pitch p >= need (in float2) with p == r (mod 16)
 constexpr int pitch_mod16(int need, int r) { return need + (((r - need) % 16) + 16) % 16; }
 
-template <int K_, int TW, int TH, int NT, int RUNW_, int BR_>
+// Kernel geometry for filter size K and tile configuration C (see Cfg0 / Cfg1).
+template <int K_, class C>
 struct Geo {
-    static constexpr int K = K_, RUNW = RUNW_, BR = BR_;
-    static constexpr int NX = NT / 2;                             // X threads: convolutions
-    static constexpr int NY = NT / 2;                             // Y threads: phi
+    static constexpr int K = K_;
+    static constexpr int TW = C::TW, TH = C::TH, BR = C::BR;
+    static constexpr int NX = 32 * C::XW;                          // X threads: convolutions
+    static constexpr int NY = 32 * C::YW;                          // Y threads: phi
+    static constexpr int NT = NX + NY;
+    static constexpr int NSLOT = C::NSLOT;                         // v/w slots in flight
+    static constexpr bool ACC_SMEM = C::ACC_SMEM;                  // park d between filters in smem
+    static constexpr int RUNWX = 10, RUNWY = C::RUNWY;             // pairs per conv run / phi run
     static constexpr int R = K / 2;
     static constexpr int K8 = tap_pitch(K);
     static constexpr int KT = tap_floats(K);
-    static constexpr int BC = 2;                                  // phase-B block width (pairs)
-    static constexpr int WWc = (TW + 2 * R + RUNW - 1) / RUNW * RUNW;  // w region width
-    static constexpr int RPR = WWc / RUNW;                         // runs per w row
+    static constexpr int BC = 2;                                   // adjoint block width (pairs)
+    static constexpr int WWc = (TW + 2 * R + RUNWX - 1) / RUNWX * RUNWX;  // w region width
+    static constexpr int RPRX = WWc / RUNWX, RPRY = WWc / RUNWY;   // runs per w row
     static constexpr int WH = TH + 2 * R;                          // w region rows
-    static constexpr int NRUN = WH * RPR;
-    static constexpr int SEG = RUNW + 2 * R;                       // u window of a run
-    static constexpr int SEGB = BC + 2 * R;                        // w window of a phase-B row
+    static constexpr int NRUNX = WH * RPRX, NRUNY = WH * RPRY;
+    static constexpr int SEG = RUNWX + 2 * R;                      // u window of a conv run
+    static constexpr int SEGB = BC + 2 * R;                        // w window of an adjoint row
     static constexpr int UH = TH + 4 * R;
     static constexpr int UWc = WWc + 2 * R;
-    // Bank-conflict-free LDS.128: lanes of a run row sit 2*RUNW
-    // words apart; with RUNW = 10 and a pitch == 10*RPR (mod 16) float2, any 8
-    // consecutive runs hit 8 distinct 4-bank groups (group = 5*run mod 8).
-    static constexpr int PU = pitch_mod16(UWc, (10 * RPR) % 16);
-    static constexpr int PW = pitch_mod16(WWc, (10 * RPR) % 16);
+    // Bank-conflict-free shared loads: conv lanes sit 2*RUNWX = 20
+    // words apart; with a pitch == 10*RPRX (mod 16) float2, any 8 consecutive runs
+    // hit 8 distinct 4-bank groups (LDS.128), and for RUNWY = 5 any 16 consecutive
+    // phi runs hit 16 distinct 2-bank groups (LDS.64).
+    static constexpr int PU = pitch_mod16(UWc, (10 * RPRX) % 16);
+    static constexpr int PW = pitch_mod16(WWc, (10 * RPRX) % 16);
     static constexpr int NBX = TW / BC;
     static constexpr int NBY = TH / BR;
-    static_assert(RUNW == 10, "pitch rule assumes RUNW = 10");
+    static constexpr int ACC_F2 = ACC_SMEM ? NX * BR * BC : 0;
+    static_assert(WWc % RUNWY == 0 && (RUNWY == 10 || RUNWY == 5), "phi runs tile the w row");
     static_assert(SEG % 2 == 0 && SEGB % 2 == 0, "whole 16-byte segments");
-    static_assert(NBX * NBY == NX, "exactly one phase-B block per X thread");
-    static_assert(NBX % 8 == 0, "a quarter warp stays in one phase-B row");
-    static_assert(NT % 32 == 0, "whole warps");
-    static constexpr int smem_f2 = UH * PU + 3 * WH * PW;  // u + 3 v/w slots
+    static_assert(NBX * NBY == NX, "exactly one adjoint block per X thread");
+    static_assert(NBX % 8 == 0, "a quarter warp stays in one adjoint row");
+    static_assert(NSLOT == 2 || NSLOT == 3, "slot ring");
+    static constexpr int smem_f2 = UH * PU + NSLOT * WH * PW + ACC_F2;
 };
 
 template <int N>
@@ -234,6 +242,28 @@ __device__ __forceinline__ void load_f2(const f2 *p, f2 (&s)[N]) {
         const ulonglong2 q = *reinterpret_cast<const ulonglong2 *>(p + j);
         s[j] = q.x;
         s[j + 1] = q.y;
+    }
+}
+
+// N consecutive pairs from shared memory: 16-byte loads when N is even and the
+// start is 16-byte aligned (ALIGNED), else 8-byte loads.
+template <int N, bool ALIGNED>
+__device__ __forceinline__ void load_pairs(const f2 *p, f2 (&s)[N]) {
+    if constexpr (ALIGNED && N % 2 == 0) {
+        load_f2<N>(p, s);
+    } else {
+#pragma unroll
+        for (int j = 0; j < N; ++j) s[j] = p[j];
+    }
+}
+template <int N, bool ALIGNED>
+__device__ __forceinline__ void store_pairs(f2 *p, const f2 (&s)[N]) {
+    if constexpr (ALIGNED && N % 2 == 0) {
+#pragma unroll
+        for (int j = 0; j < N; j += 2) *reinterpret_cast<ulonglong2 *>(p + j) = make_ulonglong2(s[j], s[j + 1]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < N; ++j) p[j] = s[j];
     }
 }
 
@@ -282,8 +312,8 @@ __device__ __forceinline__ void mirror_store(float *Wf, int h, int H, int W, int
 // the tile + r halo of both tiles, every region position, into the slot Vb.
 template <class G>
 __device__ __forceinline__ void phase_conv(const float *__restrict__ fpar, const f2 *s_u, f2 *Vb, int xt) {
-    constexpr int K = G::K, R = G::R, K8 = G::K8, RUNW = G::RUNW;
-    constexpr int RPR = G::RPR, NRUN = G::NRUN, PU = G::PU, PW = G::PW, SEG = G::SEG;
+    constexpr int K = G::K, R = G::R, K8 = G::K8, RUNW = G::RUNWX;
+    constexpr int RPR = G::RPRX, NRUN = G::NRUNX, PU = G::PU, PW = G::PW, SEG = G::SEG;
     for (int run = xt; run < NRUN; run += G::NX) {
         const int wr = run / RPR;
         const int wc = (run - wr * RPR) * RUNW;
@@ -292,14 +322,24 @@ __device__ __forceinline__ void phase_conv(const float *__restrict__ fpar, const
         for (int e = 0; e < RUNW; ++e) v[e] = 0ull;
 #pragma unroll
         for (int ta = 0; ta < K; ++ta) {  // tap row a = ta - R reads u row (py - a)
-            f2 seg[SEG];
-            load_f2<SEG>(s_u + (wr + 2 * R - ta) * PU + wc, seg);
             float tk[K8];
             load_taps_row<K>(fpar + ta * K8, tk);
+            const f2 *urow = s_u + (wr + 2 * R - ta) * PU + wc;
+            // stream the SEG-pair u window two pairs at a time: pair j feeds
+            // v[e] with tap col tb = e + 2R - j (tap col b = tb - R reads u col px - b)
 #pragma unroll
-            for (int tb = 0; tb < K; ++tb) {  // tap col b = tb - R reads u col (px - b)
+            for (int j0 = 0; j0 < SEG; j0 += 2) {
+                const ulonglong2 q = *reinterpret_cast<const ulonglong2 *>(urow + j0);
+                const f2 uj[2] = {q.x, q.y};
 #pragma unroll
-                for (int e = 0; e < RUNW; ++e) v[e] = fma2(seg[e + 2 * R - tb], bc(tk[tb]), v[e]);
+                for (int jj = 0; jj < 2; ++jj) {
+                    const int j = j0 + jj;
+#pragma unroll
+                    for (int e = 0; e < RUNW; ++e) {
+                        const int tb = e + 2 * R - j;
+                        if (tb >= 0 && tb < K) v[e] = fma2(uj[jj], bc(tk[tb]), v[e]);
+                    }
+                }
             }
         }
         f2 *vrow = Vb + wr * PW + wc;
@@ -316,8 +356,9 @@ __device__ __forceinline__ void phase_conv(const float *__restrict__ fpar, const
 template <class G>
 __device__ __forceinline__ void phase_phi(const StageArgs &a, const TileGeo &gA, const TileGeo &gB,
                                           const float *__restrict__ fpar, f2 *Wb, int yt) {
-    constexpr int R = G::R, KT = G::KT, RUNW = G::RUNW;
-    constexpr int WWc = G::WWc, RPR = G::RPR, WH = G::WH, NRUN = G::NRUN, PW = G::PW;
+    constexpr int R = G::R, KT = G::KT, RUNW = G::RUNWY;
+    constexpr int WWc = G::WWc, RPR = G::RPRY, WH = G::WH, NRUN = G::NRUNY, PW = G::PW;
+    constexpr bool AL = RUNW % 2 == 0;  // runs start 16-byte aligned
     const int lane = yt & 31, ywarp = yt >> 5;
     const int H = a.H, W = a.W;
     for (int base = ywarp * 32; base < NRUN; base += G::NY) {
@@ -327,7 +368,7 @@ __device__ __forceinline__ void phase_phi(const StageArgs &a, const TileGeo &gA,
         const int wc = (run - wr * RPR) * RUNW;
         f2 *wrow = Wb + wr * PW + wc;
         f2 v[RUNW];
-        load_f2<RUNW>(wrow, v);
+        load_pairs<RUNW, AL>(wrow, v);
         f2 w[RUNW];
 #ifdef TNRD_EXP_NOPHI
 #pragma unroll
@@ -340,9 +381,7 @@ __device__ __forceinline__ void phase_phi(const StageArgs &a, const TileGeo &gA,
             const int pxA = gA.x0 - R + wc, pxB = gB.x0 - R + wc;
             const bool rowA = (unsigned)pyA < (unsigned)H, rowB = (unsigned)pyB < (unsigned)H;
             if (rowA && rowB && pxA >= 0 && pxA + RUNW <= W && pxB >= 0 && pxB + RUNW <= W) {
-#pragma unroll
-                for (int e = 0; e < RUNW; e += 2)
-                    *reinterpret_cast<ulonglong2 *>(wrow + e) = make_ulonglong2(w[e], w[e + 1]);
+                store_pairs<RUNW, AL>(wrow, w);
             } else {
                 float *wf = reinterpret_cast<float *>(wrow);
 #pragma unroll
@@ -378,21 +417,41 @@ __device__ __forceinline__ void phase_b(const StageArgs &a, const TileGeo &gA, c
                                         f2 (&acc)[G::BR][G::BC]) {
     constexpr int K = G::K, R = G::R, K8 = G::K8, BR = G::BR, BC = G::BC, PW = G::PW, SEGB = G::SEGB;
     if (!(r2A || r2B)) {
-        float tk[K][K8];  // all taps of filter i, loaded once
+        if constexpr (!G::ACC_SMEM) {
+            float tk[K][K8];  // all taps of filter i, loaded once
 #pragma unroll
-        for (int ta = 0; ta < K; ++ta) load_taps_row<K>(fpar + ta * K8, tk[ta]);
+            for (int ta = 0; ta < K; ++ta) load_taps_row<K>(fpar + ta * K8, tk[ta]);
 #pragma unroll
-        for (int wrow = 0; wrow < BR + 2 * R; ++wrow) {
-            f2 seg[SEGB];
-            load_f2<SEGB>(Wb + (oyl + wrow) * PW + oxl, seg);
+            for (int wrow = 0; wrow < BR + 2 * R; ++wrow) {
+                f2 seg[SEGB];
+                load_f2<SEGB>(Wb + (oyl + wrow) * PW + oxl, seg);
 #pragma unroll
-            for (int ry = 0; ry < BR; ++ry) {
-                const int ta = wrow - ry;  // tap row index a + R
-                if (ta < 0 || ta >= K) continue;
+                for (int ry = 0; ry < BR; ++ry) {
+                    const int ta = wrow - ry;  // tap row index a + R
+                    if (ta < 0 || ta >= K) continue;
 #pragma unroll
-                for (int tb = 0; tb < K; ++tb)
+                    for (int tb = 0; tb < K; ++tb)
 #pragma unroll
-                    for (int e = 0; e < BC; ++e) acc[ry][e] = fma2(seg[e + tb], bc(tk[ta][tb]), acc[ry][e]);
+                        for (int e = 0; e < BC; ++e) acc[ry][e] = fma2(seg[e + tb], bc(tk[ta][tb]), acc[ry][e]);
+                }
+            }
+        } else {
+            // register-lean variant: one tap row at a time (same operation order)
+#pragma unroll
+            for (int wrow = 0; wrow < BR + 2 * R; ++wrow) {
+                f2 seg[SEGB];
+                load_f2<SEGB>(Wb + (oyl + wrow) * PW + oxl, seg);
+#pragma unroll
+                for (int ry = 0; ry < BR; ++ry) {
+                    const int ta = wrow - ry;
+                    if (ta < 0 || ta >= K) continue;
+                    float tk[K8];
+                    load_taps_row<K>(fpar + ta * K8, tk);
+#pragma unroll
+                    for (int tb = 0; tb < K; ++tb)
+#pragma unroll
+                        for (int e = 0; e < BC; ++e) acc[ry][e] = fma2(seg[e + tb], bc(tk[tb]), acc[ry][e]);
+                }
             }
         }
         return;
@@ -439,28 +498,29 @@ __device__ __forceinline__ void phase_b(const StageArgs &a, const TileGeo &gA, c
     }
 }
 
-// Warp-specialised stage kernel.  Warps [0, NT/2) are "X":
-// the FMA-only work -- forward filter bank of filter i+1 into slot (i+1)%3,
-// then the adjoint of filter i from slot i%3, then the epilogue.  Warps
-// [NT/2, NT) are "Y": the MUFU-heavy phi of filter i, in place on slot i%3.
+// Warp-specialised stage kernel.  Warps [0, XW) are "X": the
+// FMA-only work -- forward filter bank of filter i+1 into slot (i+1)%NSLOT, then
+// the adjoint of filter i from slot i%NSLOT, then the epilogue.  The remaining
+// YW warps are "Y": the MUFU-heavy phi of filter i, in place on slot i%NSLOT.
 // Named barriers: VFULL_s (X arrive, Y wait) and WFULL_s (Y arrive, X wait).
-// Three slots need no "empty" barrier: X rewrites slot (i+1)%3 only after its
-// own WFULL wait of iteration i-1, i.e. after every X thread finished the
-// adjoint of filter i-2 that read it, and Y touches a slot only between its
-// VFULL and WFULL.  So phi(i) runs concurrently with conv(i+1) + adjoint(i-1).
-template <int K_, int TW, int TH, int NT, int RUNW_, int BR_, int MINB, int REG_X, int REG_Y>
-__global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__ StageArgs a) {
-    static_assert(REG_X == 0 || (NT / 2) % 128 == 0, "setmaxnreg works on whole warpgroups");
-    static_assert(REG_X == 0 || (NT / 2) * (REG_X + REG_Y) <= 65536, "register file");
-    using G = Geo<K_, TW, TH, NT, RUNW_, BR_>;
-    constexpr int R = G::R, BR = G::BR, BC = G::BC;
+// With three slots no "empty" barrier is needed: X rewrites slot (i+1)%3 only
+// after its own WFULL wait of iteration i-1, i.e. after every X thread finished
+// the adjoint of filter i-2 that read it.  With two slots an X-only barrier
+// before conv(i+1) ensures every X thread finished the adjoint of filter i-1.
+// Either way phi(i) runs concurrently with conv(i+1) and the adjoint of i-1.
+template <int K_, class C>
+__global__ void __launch_bounds__(32 * (C::XW + C::YW), C::MINB) stage_kernel(const __grid_constant__ StageArgs a) {
+    using G = Geo<K_, C>;
+    constexpr int NT = G::NT, NSLOT = G::NSLOT;
+    constexpr int R = G::R, BR = G::BR, BC = G::BC, TW = G::TW, TH = G::TH;
     constexpr int UH = G::UH, UWc = G::UWc, PU = G::PU, SLOT = G::WH * G::PW;
-    constexpr int BAR_VFULL = 1, BAR_WFULL = 4;  // ids 1-3 and 4-6 (0 = __syncthreads)
+    constexpr int BAR_VFULL = 1, BAR_WFULL = 4, BAR_X = 7;  // ids 1-3, 4-6, 7 (0 = __syncthreads)
 
     extern __shared__ float4 smem4[];
     float *s_par = reinterpret_cast<float *>(smem4);
     f2 *s_u = reinterpret_cast<f2 *>(s_par + a.Nk * a.pstride);
-    f2 *s_w = s_u + UH * PU;  // 3 slots
+    f2 *s_w = s_u + UH * PU;              // NSLOT slots
+    f2 *s_acc = s_w + NSLOT * SLOT;       // G::ACC_F2 pairs (ACC_SMEM)
 
     const int tid = threadIdx.x;
     const int H = a.H, W = a.W;
@@ -496,10 +556,9 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__
 
     if (tid >= G::NX) {
         // ======================= Y: phi in place, filter by filter
-        if constexpr (REG_Y > 0) regs_inc<REG_Y>();
         const int yt = tid - G::NX;
         for (int i = 0; i < Nk; ++i) {
-            const int slot = i % 3;
+            const int slot = i % NSLOT;
             named_sync(BAR_VFULL + slot, NT);
             phase_phi<G>(a, gA, gB, s_par + i * a.pstride, s_w + slot * SLOT, yt);
             named_arrive(BAR_WFULL + slot, NT);
@@ -508,7 +567,6 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__
     }
 
     // ======================= X: forward conv (i+1), adjoint (i), epilogue
-    if constexpr (REG_X > 0) regs_dec<REG_X>();
     const int xt = tid;
     const int oyl = (xt / G::NBX) * BR, oxl = (xt % G::NBX) * BC;
     const auto r2_edge = [&](const TileGeo &g) {
@@ -516,29 +574,62 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__
                                      (g.y0 + oyl - R < 0) || (g.y0 + oyl + BR + R > H));
     };
     const bool r2A = r2_edge(gA), r2B = r2_edge(gB);
+    // accumulator block of this thread in smem: 16-byte chunk j of thread xt at
+    // [j][xt] (lane-consecutive, conflict-free)
+    ulonglong2 *accp = reinterpret_cast<ulonglong2 *>(s_acc) + xt;
+    constexpr int ACC_CHUNKS = BR * BC / 2;
 
-    f2 acc[BR][BC];
+    // d of this thread's block: in registers across filters (S), or parked in smem
+    // between filters so it is not live during the forward conv (L, 80 registers)
+    f2 acc_reg[BR][BC];
 #pragma unroll
     for (int ry = 0; ry < BR; ++ry)
 #pragma unroll
-        for (int e = 0; e < BC; ++e) acc[ry][e] = 0ull;
+        for (int e = 0; e < BC; ++e) acc_reg[ry][e] = 0ull;
 
     phase_conv<G>(s_par, s_u, s_w, xt);
     named_arrive(BAR_VFULL + 0, NT);
     for (int i = 0; i < Nk; ++i) {
         if (i + 1 < Nk) {
-            const int nslot = (i + 1) % 3;
+            const int nslot = (i + 1) % NSLOT;
+            if (NSLOT == 2 && i >= 1) named_sync(BAR_X, G::NX);  // adjoint(i-1) done with this slot
 #ifndef TNRD_EXP_NOCONV
             phase_conv<G>(s_par + (i + 1) * a.pstride, s_u, s_w + nslot * SLOT, xt);
 #endif
             named_arrive(BAR_VFULL + nslot, NT);
         }
-        const int slot = i % 3;
+        const int slot = i % NSLOT;
         named_sync(BAR_WFULL + slot, NT);  // phi of filter i done
+        if constexpr (G::ACC_SMEM) {
+            f2 acc[BR][BC];
+#pragma unroll
+            for (int j = 0; j < ACC_CHUNKS; ++j) {
+                const ulonglong2 q = i > 0 ? accp[j * G::NX] : make_ulonglong2(0ull, 0ull);
+                acc[(2 * j) / BC][(2 * j) % BC] = q.x;
+                acc[(2 * j + 1) / BC][(2 * j + 1) % BC] = q.y;
+            }
 #ifndef TNRD_EXP_NOADJ
-        phase_b<G>(a, gA, gB, r2A, r2B, s_par + i * a.pstride, s_w + slot * SLOT, oyl, oxl, acc);
+            phase_b<G>(a, gA, gB, r2A, r2B, s_par + i * a.pstride, s_w + slot * SLOT, oyl, oxl, acc);
 #endif
+#pragma unroll
+            for (int j = 0; j < ACC_CHUNKS; ++j)
+                accp[j * G::NX] = make_ulonglong2(acc[(2 * j) / BC][(2 * j) % BC],
+                                                  acc[(2 * j + 1) / BC][(2 * j + 1) % BC]);
+        } else {
+#ifndef TNRD_EXP_NOADJ
+            phase_b<G>(a, gA, gB, r2A, r2B, s_par + i * a.pstride, s_w + slot * SLOT, oyl, oxl, acc_reg);
+#endif
+        }
     }
+    if constexpr (G::ACC_SMEM) {
+#pragma unroll
+        for (int j = 0; j < ACC_CHUNKS; ++j) {
+            const ulonglong2 q = accp[j * G::NX];
+            acc_reg[(2 * j) / BC][(2 * j) % BC] = q.x;
+            acc_reg[(2 * j + 1) / BC][(2 * j + 1) % BC] = q.y;
+        }
+    }
+    f2 (&acc)[BR][BC] = acc_reg;
 
     // ---------------- epilogue: ut = u - d, u+ = prox(ut), store (per tile half)
 #pragma unroll
@@ -565,20 +656,25 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const __grid_constant__
     }
 }
 
-// Tile configurations: 0 = "L" two 64x64 output tiles, 512 threads, 1 CTA/SM;
-//                      1 = "S" two 32x32 output tiles, 128 threads (small images).
-struct Cfg0 { static constexpr int TW = 64, TH = 64, NT = 512, RUNW = 10, BR = 8, MINB = 1, REG_X = 0, REG_Y = 0; };  // setmaxnreg 112/144 measured: no gain
-struct Cfg1 { static constexpr int TW = 32, TH = 32, NT = 128, RUNW = 10, BR = 8, MINB = 3, REG_X = 0, REG_Y = 0; };
+// Tile configurations.
+//  0 = "L": two 64x64 output tiles, 8 X warps + 8 Y warps (512 threads, 128
+//      registers), 3 slots, d in registers; 1 CTA per SM (~200 KB shared memory).
+//      (8 + 16 warps at 80 registers, d parked in smem, 2 slots: 27.1 vs 23.8 ms.)
+//  1 = "S": two 32x32 output tiles, 2 + 2 warps, 3 slots, d in registers, for
+//      images too small to fill the GPU with "L" tiles.
+struct Cfg0 { static constexpr int TW = 64, TH = 64, XW = 8, YW = 8, RUNWY = 10, BR = 8, NSLOT = 3, MINB = 1;
+              static constexpr bool ACC_SMEM = false; };
+struct Cfg1 { static constexpr int TW = 32, TH = 32, XW = 2, YW = 2, RUNWY = 10, BR = 8, NSLOT = 3, MINB = 3;
+              static constexpr bool ACC_SMEM = false; };
 
 template <int K, class C>
 size_t smem_bytes(int Nk, int pstride) {
-    using Gm = Geo<K, C::TW, C::TH, C::NT, C::RUNW, C::BR>;
-    return sizeof(float) * (size_t)Nk * pstride + sizeof(f2) * (size_t)Gm::smem_f2;
+    return sizeof(float) * (size_t)Nk * pstride + sizeof(f2) * (size_t)Geo<K, C>::smem_f2;
 }
 
 template <int K, class C>
 cudaError_t launch(StageArgs &a, int B, cudaStream_t s) {
-    auto kern = stage_kernel<K, C::TW, C::TH, C::NT, C::RUNW, C::BR, C::MINB, C::REG_X, C::REG_Y>;
+    auto kern = stage_kernel<K, C>;
     const size_t smem = smem_bytes<K, C>(a.Nk, a.pstride);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -587,7 +683,7 @@ cudaError_t launch(StageArgs &a, int B, cudaStream_t s) {
     const long long n = (long long)B * a.tiles_x * a.tiles_y;
     if (n > INT_MAX - 1) return cudaErrorInvalidValue;
     a.n_tiles = (int)n;
-    kern<<<(unsigned)((n + 1) / 2), C::NT, smem, s>>>(a);
+    kern<<<(unsigned)((n + 1) / 2), Geo<K, C>::NT, smem, s>>>(a);
     return cudaGetLastError();
 }
 
