@@ -241,12 +241,15 @@ struct NcclExchange : SlabExchange {
     }
 };
 
-// Largest |ys| at which the Horner factors stay finite: sum|c| * R^3 and
-// sum|c| * R^-4 (R = 2^(2 sg ys)) below 2^120, i.e. 8 sg |ys| + log2(sum|c|) <= 120.
-double horner_yclamp(double sg, double sum_abs_c) {
+// Horner units: R's exponent bound yrmax with sum|c| * 2^(7 yrmax) <= 2^126, so
+// that R^7 (times the largest coefficient sum) stays finite (tnrd_internal.h).
+double horner_yrmax(double sum_abs_c) {
     const double l2 = std::log2(std::max(sum_abs_c, 1e-30));
-    return std::min(64.0, (120.0 - std::max(l2, -30.0)) / (8.0 * sg));
+    return std::min(120.0, (126.0 - std::max(l2, -30.0)) / 7.0);
 }
+// ... and the Horner form is used only where the clamp t <= yrmax / (2 sg) binds
+// exclusively on terms below 2^-20 of their weight: t_clamp >= 7 sg + 4.5.
+bool horner_ok(double sg, double yrmax) { return yrmax / (2.0 * sg) >= 7.0 * sg + 4.5; }
 
 // Host-side evaluation constants of one stage (layout in tnrd_internal.h),
 // computed in double and rounded once to fp32.
@@ -270,19 +273,19 @@ void pack_stage(const tnrd_desc &d, const float *filters, const float *w, const 
             double smax = 0.0;
             for (int b = 0; b < NB; ++b) {
                 float *u = units + b * tnrd::kHornerUnit;
-                const int c = 8 * b + 4;
-                u[0] = (float)(sg * (x_off - c));
+                u[0] = (float)(sg * (x_off - 8.0 * b));   // t of the block's first centre
                 double s = 0.0;
-                for (int dd = -4; dd <= 3; ++dd) {
-                    const int j = c + dd;
-                    const double coef = (j >= 0 && j < M) ? wi[j] * std::exp(-rho * rho * dd * dd / 2.0) : 0.0;
-                    u[1 + (dd + 4)] = (float)coef;   // u[1..8] = c_-4 .. c_3
+                for (int e = 0; e < 8; ++e) {
+                    const int j = 8 * b + e;
+                    const double coef = j < M ? wi[j] * std::exp(-rho * rho * e * e / 2.0) : 0.0;
+                    u[1 + e] = (float)coef;   // u[1..8] = c_0 .. c_7
                     s += std::fabs(coef);
                 }
                 smax = std::max(smax, s);
             }
             fc[0] = (float)a_s; fc[1] = (float)(2.0 * sg); fc[2] = (float)(1.0 / (8.0 * sg)); fc[3] = (float)NB;
-            fc[4] = (float)horner_yclamp(sg, smax);
+            fc[4] = (float)horner_yrmax(smax);
+            fc[5] = horner_ok(sg, horner_yrmax(smax)) ? 1.f : 0.f;   // host-side check only
         } else {
             fc[0] = (float)a_s; fc[1] = (float)(2.0 * sg); fc[2] = (float)(1.0 / sg); fc[3] = (float)M;
             for (int j = 0; j < M; ++j) {
@@ -382,9 +385,10 @@ tnrd_status tnrd_set_stage_params(tnrd_handle *h, int t, const float *filters, c
         for (int j = 0; j < M; ++j)
             if (!std::isfinite(rbf_w[(size_t)i * M + j])) return fail(h, TNRD_EINVAL, "non-finite RBF weight");
     }
-    // Horner units when every Gaussian is wide enough and the factors stay finite
-    // over the whole kWindow; otherwise one unit per centre.
-    int mode = rho_max <= tnrd::kHornerMaxRho ? tnrd::MODE_HORNER : tnrd::MODE_DIRECT;
+    // Horner units when the clamp of R only touches negligible terms for every
+    // filter; otherwise one unit per centre.
+    (void)rho_max;
+    int mode = tnrd::MODE_HORNER;
     std::vector<float> host;
     for (int attempt = 0; attempt < 2; ++attempt) {
         const int ps = pstride_for(h->d, mode);
@@ -392,8 +396,7 @@ tnrd_status tnrd_set_stage_params(tnrd_handle *h, int t, const float *filters, c
         pack_stage(h->d, filters, rbf_w, rbf_mu0, rbf_step, rbf_gamma, mode, ps, host.data());
         if (mode == tnrd::MODE_DIRECT) break;
         bool ok = true;
-        for (int i = 0; i < Nk; ++i)
-            ok = ok && host[(size_t)i * ps + tnrd::tap_floats(K) + 4] >= tnrd::kWindow + 0.5f;
+        for (int i = 0; i < Nk; ++i) ok = ok && host[(size_t)i * ps + tnrd::tap_floats(K) + 5] != 0.f;
         if (ok) break;
         mode = tnrd::MODE_DIRECT;
     }

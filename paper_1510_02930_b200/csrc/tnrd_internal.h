@@ -19,15 +19,16 @@ namespace tnrd {
 // phi evaluation.  With x = (v - mu0)/step the response in
 // centre units, rho = step/gamma and sg = rho*sqrt(log2(e)/2):
 //
-//  MODE_HORNER: unit b covers centres j = 8b..8b+7, centred at c_b = 8b + 4.
-//    ys = sg*(x - c_b) = a_s*v + cs_b,
-//      G = 2^(-ys^2) = exp(-rho^2 (x-c_b)^2 / 2),   R = 2^(two_sg*ys) = exp(rho^2 (x - c_b)),
-//      sum_{d=-4..3} w_{c_b+d} exp(-rho^2 (x-c_b-d)^2/2)
-//        = G * ( sum_{d=0..3} c_d R^d + R^-1 sum_{d=1..4} c_{-d} R^{-(d-1)} ),
-//      c_d = w_{c_b+d} exp(-rho^2 d^2 / 2)          (exact identity)
-//    unit layout (12 floats): { cs_b, c_-4, c_-3, c_-2, c_-1, c_0, c_1, c_2, c_3, 0, 0, 0 }
-//    yclamp: |ys| bound under which sum|c| * R^3 and sum|c| * R^-4 stay below
-//    2^120 (host-computed, >= kWindow + 0.5 or the stage uses MODE_DIRECT).
+//  MODE_HORNER: unit b covers centres j = 8b..8b+7, expanded from its first
+//    centre.  t = sg*(x - 8b) = a_s*v + ct_b,
+//      G = 2^(-t^2) = exp(-rho^2 (x-8b)^2 / 2),   R = 2^(two_sg*t) = exp(rho^2 (x - 8b)),
+//      sum_{e=0..7} w_{8b+e} exp(-rho^2 (x-8b-e)^2/2) = G * sum_{e=0..7} c_e R^e,
+//      c_e = w_{8b+e} exp(-rho^2 e^2 / 2)                (exact identity)
+//    unit layout (12 floats): { ct_b, c_0, ..., c_7, 0, 0, 0 }
+//    fc[4] = yrmax: R's exponent is clamped at yrmax = two_sg * tclamp with
+//    sum|c| * 2^(7 yrmax) <= 2^126 (no overflow of R^7).  Where the clamp binds
+//    (t > tclamp) every term of the block is below 2^-20 of its weight: the host
+//    requires tclamp >= 7 sg + 4.5 or uses MODE_DIRECT.
 //  MODE_DIRECT (any rho): unit j is centre j: ys = a_s*v + cs_j, term w_j 2^(-ys^2)
 //    unit layout (4 floats): { cs_j, w_j, 0, 0 }
 //
@@ -41,7 +42,7 @@ constexpr int kHornerUnit = 12;
 constexpr int kDirectUnit = 4;
 constexpr int kFc = 8;                // floats of per-filter constants
 constexpr float kWindow = 11.25f;     // > sqrt(126): all nonzero G lie inside
-constexpr double kHornerMaxRho = 1.5; // wider Gaussians only (else MODE_DIRECT)
+
 
 __host__ __device__ constexpr int tap_pitch(int K) { return (K + 3) / 4 * 4; }
 __host__ __device__ constexpr int tap_floats(int K) { return K * tap_pitch(K); }

@@ -118,32 +118,34 @@ __device__ __forceinline__ float prox_poisson(float ut, float lam, float f) {
     return __fdiv_rn(2.0f * lam * f, sigma - delta);
 }
 
-// Horner units [u0, u1] on NP pairs (see tnrd_internal.h).  CLAMP bounds ys to
-// +-yclamp before forming R = 2^(two_sg ys) so R^3 and R^-4 stay finite for lanes
-// far from the unit; the caller uses CLAMP = false only when no evaluated lane can
-// reach the bound, where both variants compute bitwise the same values.
-template <int NP, bool CLAMP>
+// Horner units [u0, u1] on NP pairs (see tnrd_internal.h).  Each unit is
+// expanded from its first centre: t = sg (x - 8b), G = 2^(-t^2), R = 2^(two_sg t),
+// block sum = G * sum_{e<8} c_e R^e  (2 MUFU per element).  R is clamped above at
+// two_sg*tclamp so R^7 stays finite for lanes right of the block; the clamp only
+// binds where every term of the block is below 2^-20 of its weight (host check).
+template <int NP>
 __device__ __forceinline__ void horner_units(const float *__restrict__ units, float a_s, float two_sg,
-                                             float yclamp, int u0, int u1, const f2 (&v)[NP],
+                                             float yrmax, int u0, int u1, const f2 (&v)[NP],
                                              f2 (&w)[NP]) {
     for (int u = u0; u <= u1; ++u) {
         const float4 *up = reinterpret_cast<const float4 *>(units + u * kHornerUnit);
         const float4 q0 = up[0], q1 = up[1], q2 = up[2];
-        // q0 = {cs, c-4, c-3, c-2}, q1 = {c-1, c0, c1, c2}, q2 = {c3, ...}
+        // q0 = {ct, c0, c1, c2}, q1 = {c3, c4, c5, c6}, q2 = {c7, ...}
 #pragma unroll
         for (int e = 0; e < NP; ++e) {
-            const f2 ys = fma2(v[e], bc(a_s), bc(q0.x));
-            const f2 sq = mul2(ys, ys);
+            const f2 t = fma2(v[e], bc(a_s), bc(q0.x));
+            const f2 sq = mul2(t, t);
             const f2 G = pk(ex2_ftz(-lo(sq)), ex2_ftz(-hi(sq)));
-            f2 yc = ys;
-            if (CLAMP)
-                yc = pk(fminf(fmaxf(lo(ys), -yclamp), yclamp), fminf(fmaxf(hi(ys), -yclamp), yclamp));
-            const f2 yr = mul2(yc, bc(two_sg));
-            const f2 R = pk(ex2_ftz(lo(yr)), ex2_ftz(hi(yr)));
-            const f2 Ri = pk(ex2_ftz(-lo(yr)), ex2_ftz(-hi(yr)));
-            const f2 pp = fma2(fma2(fma2(R, bc(q2.x), bc(q1.w)), R, bc(q1.z)), R, bc(q1.y));
-            const f2 pm = fma2(fma2(fma2(Ri, bc(q0.y), bc(q0.z)), Ri, bc(q0.w)), Ri, bc(q1.x));
-            w[e] = fma2(G, fma2(pm, Ri, pp), w[e]);
+            const f2 yr = mul2(t, bc(two_sg));
+            const f2 R = pk(ex2_ftz(fminf(lo(yr), yrmax)), ex2_ftz(fminf(hi(yr), yrmax)));
+            f2 p = fma2(R, bc(q2.x), bc(q1.w));
+            p = fma2(p, R, bc(q1.z));
+            p = fma2(p, R, bc(q1.y));
+            p = fma2(p, R, bc(q1.x));
+            p = fma2(p, R, bc(q0.w));
+            p = fma2(p, R, bc(q0.z));
+            p = fma2(p, R, bc(q0.y));
+            w[e] = fma2(G, p, w[e]);
         }
     }
 }
@@ -156,7 +158,7 @@ __device__ __forceinline__ void phi_x2(const float *__restrict__ fp, int mode, c
     const float4 fc = *reinterpret_cast<const float4 *>(fp);
     const float a_s = fc.x, two_sg = fc.y, inv_ustep = fc.z;
     const int nunits = __float2int_rn(fc.w);
-    const float yclamp = fp[4];
+    const float yclamp = fp[4];  // Horner: upper bound of the R exponent
     const float *units = fp + kFc;
     float vmin = INFINITY, vmax = -INFINITY;
 #pragma unroll
@@ -173,11 +175,7 @@ __device__ __forceinline__ void phi_x2(const float *__restrict__ fp, int mode, c
     const int u0 = max(0, __float2int_ru((ylo - kWindow) * inv_ustep));
     const int u1 = min(nunits - 1, __float2int_rd((yhi + kWindow) * inv_ustep));
     if (mode == MODE_HORNER) {
-        // every evaluated unit has |ys_u| <= (yhi - ylo) + kWindow for every lane
-        if ((yhi - ylo) + (kWindow + 0.05f) <= yclamp)
-            horner_units<NP, false>(units, a_s, two_sg, yclamp, u0, u1, v, w);
-        else
-            horner_units<NP, true>(units, a_s, two_sg, yclamp, u0, u1, v, w);
+        horner_units<NP>(units, a_s, two_sg, yclamp, u0, u1, v, w);
     } else {
         for (int u = u0; u <= u1; ++u) {
             const float2 q = *reinterpret_cast<const float2 *>(units + u * kDirectUnit);

@@ -258,10 +258,12 @@ def test_strided_rows(torch_cuda, P):
 # ------------------------------------------------------------------ phi / prox micro-parity
 def test_phi_micro_parity(torch_cuda, P):
     """The device phi against the oracle's direct double sum over x = (v-mu0)/step in
-    [-15, 77].  fp32 model of the error: the block argument
-    ys = a_s*v + cs_b carries ~2^-24 (|a_s v| + |cs_b|) from the rounded constants, so
-    the bound grows with the distance of x from the grid centre; in the centre band
-    (|x - 31| <= 8, where the workloads' responses lie) it is tight."""
+    [-15, 77].  fp32 error model: each 8-centre unit is G * P(R) with
+    P of degree 7 in R = 2^(2 sg t), so a term carries ~7x the relative error of R
+    (ex2.approx plus the rounding of its exponent) plus the rounding of t^2 in G:
+    about 5e-6 of the term for the highest power.  Bound: 8e-6 * max|w| in the
+    centre band (|x - 31| <= 8, where the workloads' responses lie), growing with
+    the distance from the grid centre (the rounded unit constants)."""
     torch = torch_cuda
     p = make_problem(3)
     eng = P.TNRD(p.model)
@@ -278,8 +280,8 @@ def test_phi_micro_parity(torch_cuda, P):
         centre = np.abs(xs - 31) <= 8
         MARGINS[f"phi t{t} i{i} centre"] = float(err[centre].max() / scale)
         MARGINS[f"phi t{t} i{i} all"] = float(err.max() / scale)
-        assert err[centre].max() < 1.5e-6 * scale, (t, i, err[centre].max())
-        assert np.all(err < 1e-6 * scale * (1 + np.abs(xs - 31))), (t, i, err.max())
+        assert err[centre].max() < 8e-6 * scale, (t, i, err[centre].max())
+        assert np.all(err < 8e-6 * scale * (1 + np.abs(xs - 31) / 16)), (t, i, err.max())
     eng.close()
 
 
