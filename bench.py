@@ -159,20 +159,27 @@ def workload_config(p, world, args):
 
 
 def cpu_baseline(p, budget_s=12.0):
-    """The oracle on a bounded sample (rank 0, N = 1 only)."""
+    """The oracle on a bounded sample (rank 0, N = 1 only): whole-image windows of
+    the workload, one after another, until ~budget_s of CPU time has been spent."""
     import oracle
+    B, H, W = p.f.shape
     f0 = p.f[0]
     t = time.perf_counter()
     oracle.denoise(f0[:32, :32], p.model)
     per_px = (time.perf_counter() - t) / 1024
-    side = int(np.clip(np.sqrt(budget_s / max(per_px, 1e-9)), 32, min(f0.shape)))
-    y, x = (f0.shape[0] - side) // 2, (f0.shape[1] - side) // 2
-    t = time.perf_counter()
-    oracle.denoise(f0[y:y + side, x:x + side], p.model)
-    dt = time.perf_counter() - t
-    return {"value": side * side / 1e6 / dt, "unit": "MPix/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"one {side}x{side} window of image 0 (T={p.model.T}, full model), double precision, "
-                      f"{dt:.1f} s"}
+    side = int(np.clip(np.sqrt(budget_s / max(per_px, 1e-9)), 32, min(H, W)))
+    y, x = (H - side) // 2, (W - side) // 2
+    n, px, t0 = 0, 0, time.perf_counter()
+    while True:
+        oracle.denoise(p.f[n % B][y:y + side, x:x + side], p.model)
+        n += 1
+        px += side * side
+        dt = time.perf_counter() - t0
+        if dt >= 0.8 * budget_s or n >= 8:
+            break
+    return {"value": px / 1e6 / dt, "unit": "MPix/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{n} centred {side}x{side} window(s) of images 0..{n - 1} (T={p.model.T}, full model), "
+                      f"double precision, OpenMP over rows, {dt:.1f} s"}
 
 
 def main():
