@@ -31,7 +31,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-F_ALG = lambda Nk, k, M: 4 * Nk * k * k + 2 * Nk * M + 10  # flop / pixel / stage (DESIGN.md §8.2)
+F_ALG = lambda Nk, k, M: 4 * Nk * k * k + 2 * Nk * M + 10  # flop / pixel / stage (DESIGN.md §5.4)
+# tabulated phi does not claim the RBF work it avoids: one cubic (8 flop) per response
+F_TAB = lambda Nk, k, M: 4 * Nk * k * k + 8 * Nk + 10
 METRIC = "denoised MPix/s (48x7x7, T=8, fp32) at 1/2/4/8 B200; % of FP32 roofline"
 
 
@@ -155,7 +157,8 @@ def workload_config(p, world, args):
             "batch": c["B"], "H": c["H"], "W": c["W"], "T": c["T"], "Nk": c["Nk"], "k": c["k"], "M": c["M"],
             "parallelism": ("batch-shard" if args.config != 5 else "row-slab+nccl-halo") + f"x{world}",
             "l2": "no flush: per-step working set (f, u, scratch) > 126 MB L2",
-            "flop_per_px_stage": F_ALG(c["Nk"], c["k"], c["M"])}
+            "phi": args.phi,
+            "flop_per_px_stage": (F_TAB if args.phi == "table" else F_ALG)(c["Nk"], c["k"], c["M"])}
 
 
 def cpu_baseline(p, budget_s=12.0):
@@ -189,6 +192,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4, choices=[3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--phi", default="exact", choices=["exact", "table"],
+                    help="exact RBF sum (the headline) or the tabulated variant (reported separately)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -209,7 +214,7 @@ def main():
     p = make_problem(args.config)
     model = p.model
     B, H, W = p.f.shape
-    eng = P.TNRD(model, device=local)
+    eng = P.TNRD(model, device=local, phi_mode=P.PHI_TABLE if args.phi == "table" else P.PHI_EXACT)
     stream = torch.cuda.current_stream()
 
     if args.config == 5:
@@ -305,7 +310,7 @@ def main():
         n_sm = props.multi_processor_count
         max_mhz = (clocks or {}).get("sm_max_mhz") or 1965.0
         peak = fp32_peak_tflops(n_sm, max_mhz)
-        flop_launch = F_ALG(model.Nk, model.k, model.M) * px_rank
+        flop_launch = (F_TAB if args.phi == "table" else F_ALG)(model.Nk, model.k, model.M) * px_rank
         achieved = flop_launch / (mean_launch_ms / 1e3) / 1e12 if mean_launch_ms > 0 else None
         traffic = None
         tf = os.path.join(ROOT, "profiles", "traffic.json")

@@ -68,8 +68,10 @@ typedef enum {
 } tnrd_boundary;
 
 typedef enum {
-    TNRD_PHI_EXACT = 0,    /* exact RBF sum (all terms above 2^-126 of their weight)   */
-    TNRD_PHI_TABLE = 1     /* tabulated phi -- not in this build: TNRD_EUNSUPPORTED    */
+    TNRD_PHI_EXACT = 0,    /* exact RBF sum (blocked Horner)            */
+    TNRD_PHI_TABLE = 1     /* tabulated phi: per-filter cubic Hermite table, 16 intervals
+                              per centre, built on the host in double from the exact phi
+                              (DESIGN.md §5.6); an optional variant, reported separately */
 } tnrd_phi_mode;
 
 /* Model shape.  T >= 1 stages, n_filters = N_k >= 1 (P l.423: N_k = m^2 - 1 if
@@ -94,8 +96,7 @@ TNRD_API const char *tnrd_status_string(tnrd_status s);
 
 /* Create a handle for model shape *d on d->device.  *out receives the handle
  * (owned by the caller, released with tnrd_destroy).  Allocates the device
- * parameter store.  EINVAL: bad shape; EUNSUPPORTED: phi_mode TABLE or ksize
- * outside {3,5,7}; ECUDA/ENOMEM: device errors.  Synchronous. */
+ * parameter store.  EINVAL: bad shape; EUNSUPPORTED: ksize outside {3,5,7}; ECUDA/ENOMEM: device errors.  Synchronous. */
 TNRD_API tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out);
 
 /* Set Theta^t = {lambda^t, phi_i^t, k_i^t} of stage t in [0, T) (P l.206-207).

@@ -247,12 +247,12 @@ class TNRD:
     rbf_mu0 / rbf_step / rbf_gamma [T][Nk], lam [T] (e.g. synth.Model).
     """
 
-    def __init__(self, model, boundary: int = BC_SYMMETRIC_EXPLICIT, device: int = 0):
+    def __init__(self, model, boundary: int = BC_SYMMETRIC_EXPLICIT, device: int = 0, phi_mode: int = PHI_EXACT):
         T, Nk, k, _ = np.shape(model.filters)
         M = np.shape(model.rbf_w)[2]
         self.T, self.Nk, self.k, self.M = int(T), int(Nk), int(k), int(M)
         self.device = device
-        self.h = tnrd_create(self.T, self.Nk, self.k, self.M, boundary, PHI_EXACT, device)
+        self.h = tnrd_create(self.T, self.Nk, self.k, self.M, boundary, phi_mode, device)
         for t in range(self.T):
             tnrd_set_stage_params(self.h, t, model.filters[t], model.rbf_w[t], model.rbf_mu0[t],
                                   model.rbf_step[t], model.rbf_gamma[t], model.lam[t])

@@ -81,6 +81,8 @@ struct tnrd_handle {
     std::vector<float> lambda;    // per stage
     std::vector<char> is_set;     // per stage
     float *d_params = nullptr;    // [T][Nk][pstride_max]
+    float4 *d_table = nullptr;    // MODE_TABLE: [T][Nk][table_stride] cubic intervals
+    int table_stride = 0;
     float *scratch = nullptr;
     size_t scratch_bytes = 0;
     float *e2e_f = nullptr, *e2e_u = nullptr;
@@ -161,6 +163,8 @@ tnrd_status launch_one(tnrd_handle *h, int t, int tile, StageArgs &a, int B, cud
     a.Nk = h->d.n_filters;
     a.pstride = h->pstride[t];
     a.mode = h->mode[t];
+    a.table = h->d_table ? h->d_table + (size_t)t * h->d.n_filters * h->table_stride : nullptr;
+    a.table_stride = h->table_stride;
     a.boundary = h->d.boundary;
     a.lambda = h->lambda[t];
     if (h->profile) {
@@ -241,6 +245,35 @@ struct NcclExchange : SlabExchange {
     }
 };
 
+// MODE_TABLE geometry and construction (tnrd_internal.h).
+int table_intervals(int M) { return (M - 1 + 2 * tnrd::kTabPad) * tnrd::kTabPerCentre; }
+
+// Cubic Hermite intervals of phi(x) = sum_j w_j exp(-rho^2 (x - j)^2 / 2) in centre
+// units (the same function as P l.145 / S l.107 with x = (z - mu0)/step), from the
+// exact values and slopes at the nodes, in double; out[n_int] = 0 (out of range).
+void build_table(const float *w, int M, double rho, float4 *out) {
+    const int S = tnrd::kTabPerCentre, n = table_intervals(M);
+    const double h = 1.0 / S, x_lo = -tnrd::kTabPad;
+    std::vector<double> f(n + 1), df(n + 1);
+    for (int k = 0; k <= n; ++k) {
+        const double x = x_lo + k * h;
+        double s0 = 0.0, s1 = 0.0;
+        for (int j = 0; j < M; ++j) {
+            const double d = x - j, g = std::exp(-rho * rho * d * d / 2.0);
+            s0 += w[j] * g;
+            s1 += -w[j] * rho * rho * d * g;
+        }
+        f[k] = s0;
+        df[k] = s1 * h;  // slope per interval length
+    }
+    for (int k = 0; k < n; ++k) {
+        const double p0 = f[k], p1 = f[k + 1], m0 = df[k], m1 = df[k + 1];
+        out[k] = make_float4((float)p0, (float)m0, (float)(3.0 * (p1 - p0) - 2.0 * m0 - m1),
+                             (float)(2.0 * (p0 - p1) + m0 + m1));
+    }
+    out[n] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
 // Horner units: R's exponent bound yrmax with sum|c| * 2^(7 yrmax) <= 2^126, so
 // that R^7 (times the largest coefficient sum) stays finite (tnrd_internal.h).
 double horner_yrmax(double sum_abs_c) {
@@ -286,6 +319,13 @@ void pack_stage(const tnrd_desc &d, const float *filters, const float *w, const 
             fc[0] = (float)a_s; fc[1] = (float)(2.0 * sg); fc[2] = (float)(1.0 / (8.0 * sg)); fc[3] = (float)NB;
             fc[4] = (float)horner_yrmax(smax);
             fc[5] = horner_ok(sg, horner_yrmax(smax)) ? 1.f : 0.f;   // host-side check only
+        } else if (mode == tnrd::MODE_TABLE) {
+            const double S = tnrd::kTabPerCentre, x_lo = -tnrd::kTabPad;
+            const double b = -(m0 / st + x_lo) * S;
+            fc[0] = (float)(S / st);
+            fc[1] = (float)b;                       // hi word of the offset
+            fc[2] = (float)table_intervals(M);
+            fc[3] = (float)(b - (double)fc[1]);     // lo word: the rounding of fc[1]
         } else {
             fc[0] = (float)a_s; fc[1] = (float)(2.0 * sg); fc[2] = (float)(1.0 / sg); fc[3] = (float)M;
             for (int j = 0; j < M; ++j) {
@@ -298,7 +338,8 @@ void pack_stage(const tnrd_desc &d, const float *filters, const float *w, const 
 
 int pstride_for(const tnrd_desc &d, int mode) {
     const int M = d.n_rbf;
-    const int units = mode == tnrd::MODE_HORNER ? ((M + 7) / 8) * tnrd::kHornerUnit : M * tnrd::kDirectUnit;
+    const int units = mode == tnrd::MODE_HORNER ? ((M + 7) / 8) * tnrd::kHornerUnit
+                      : mode == tnrd::MODE_TABLE ? 0 : M * tnrd::kDirectUnit;
     return (tnrd::tap_floats(d.ksize) + tnrd::kFc + units + 3) / 4 * 4;
 }
 
@@ -330,8 +371,8 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
         return fail(nullptr, TNRD_EINVAL, "ksize must be odd and >= 3 (got %d)", d->ksize);
     if (d->ksize > 7) return fail(nullptr, TNRD_EUNSUPPORTED, "ksize %d not built (3, 5, 7)", d->ksize);
     if (d->boundary != 0 && d->boundary != 1) return fail(nullptr, TNRD_EINVAL, "bad boundary %d", d->boundary);
-    if (d->phi_mode == TNRD_PHI_TABLE) return fail(nullptr, TNRD_EUNSUPPORTED, "tabulated phi not in this build");
-    if (d->phi_mode != TNRD_PHI_EXACT) return fail(nullptr, TNRD_EINVAL, "bad phi_mode %d", d->phi_mode);
+    if (d->phi_mode != TNRD_PHI_EXACT && d->phi_mode != TNRD_PHI_TABLE)
+        return fail(nullptr, TNRD_EINVAL, "bad phi_mode %d", d->phi_mode);
     if (d->reserved != 0) return fail(nullptr, TNRD_EINVAL, "reserved field must be 0");
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -361,6 +402,15 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
         delete h;
         return fail(nullptr, TNRD_ENOMEM, "cudaMalloc params: %s", cudaGetErrorString(e));
     }
+    if (d->phi_mode == TNRD_PHI_TABLE) {
+        h->table_stride = table_intervals(d->n_rbf) + 1;
+        e = cudaMalloc(&h->d_table, sizeof(float4) * (size_t)d->T * d->n_filters * h->table_stride);
+        if (e != cudaSuccess) {
+            cudaFree(h->d_params);
+            delete h;
+            return fail(nullptr, TNRD_ENOMEM, "cudaMalloc phi tables: %s", cudaGetErrorString(e));
+        }
+    }
     *out = h;
     return TNRD_OK;
 }
@@ -386,19 +436,28 @@ tnrd_status tnrd_set_stage_params(tnrd_handle *h, int t, const float *filters, c
             if (!std::isfinite(rbf_w[(size_t)i * M + j])) return fail(h, TNRD_EINVAL, "non-finite RBF weight");
     }
     // Horner units when the clamp of R only touches negligible terms for every
-    // filter; otherwise one unit per centre.
+    // filter; otherwise one unit per centre.  TNRD_PHI_TABLE:
+    // cubic tables built here in double.
     (void)rho_max;
-    int mode = tnrd::MODE_HORNER;
+    int mode = h->d.phi_mode == TNRD_PHI_TABLE ? tnrd::MODE_TABLE : tnrd::MODE_HORNER;
     std::vector<float> host;
     for (int attempt = 0; attempt < 2; ++attempt) {
         const int ps = pstride_for(h->d, mode);
         host.assign((size_t)Nk * ps, 0.f);
         pack_stage(h->d, filters, rbf_w, rbf_mu0, rbf_step, rbf_gamma, mode, ps, host.data());
-        if (mode == tnrd::MODE_DIRECT) break;
+        if (mode != tnrd::MODE_HORNER) break;
         bool ok = true;
         for (int i = 0; i < Nk; ++i) ok = ok && host[(size_t)i * ps + tnrd::tap_floats(K) + 5] != 0.f;
         if (ok) break;
         mode = tnrd::MODE_DIRECT;
+    }
+    if (mode == tnrd::MODE_TABLE) {
+        std::vector<float4> tab((size_t)Nk * h->table_stride);
+        for (int i = 0; i < Nk; ++i)
+            build_table(rbf_w + (size_t)i * M, M, (double)rbf_step[i] / rbf_gamma[i], tab.data() + (size_t)i * h->table_stride);
+        DeviceGuard g(h->d.device);
+        TNRD_CUDA(h, cudaMemcpy(h->d_table + (size_t)t * Nk * h->table_stride, tab.data(),
+                                sizeof(float4) * tab.size(), cudaMemcpyHostToDevice));
     }
     const int ps = pstride_for(h->d, mode);
     DeviceGuard g(h->d.device);
@@ -481,6 +540,7 @@ tnrd_status tnrd_destroy(tnrd_handle *h) {
         DeviceGuard g(h->d.device);
         cudaDeviceSynchronize();
         cudaFree(h->d_params);
+        cudaFree(h->d_table);
         cudaFree(h->scratch);
         cudaFree(h->e2e_f);
         cudaFree(h->e2e_u);
@@ -524,8 +584,9 @@ tnrd_status tnrd_debug_phi(tnrd_handle *h, int t, int i, const float *v, float *
     if (t < 0 || t >= h->d.T || !h->is_set[t]) return fail(h, TNRD_ESTATE, "stage %d not set", t);
     if (i < 0 || i >= h->d.n_filters) return fail(h, TNRD_EINVAL, "filter index");
     DeviceGuard g(h->d.device);
+    const float4 *tab = h->d_table ? h->d_table + ((size_t)t * h->d.n_filters + i) * h->table_stride : nullptr;
     cudaError_t e = tnrd::launch_debug_phi(h->d_params + (size_t)t * h->d.n_filters * h->pstride_max,
-                                           h->pstride[t], h->mode[t], h->d.ksize, i, v, out, n,
+                                           h->pstride[t], h->mode[t], tab, h->d.ksize, i, v, out, n,
                                            reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(h, e, "debug phi");
     h->launches++;

@@ -37,7 +37,17 @@ namespace tnrd {
 //  whose |ys| <= kWindow for some lane, so every unit it skips contributes
 //  exactly 0 as well: the result does not depend on which pixels share a warp.
 // ---------------------------------------------------------------------------
-enum { MODE_HORNER = 0, MODE_DIRECT = 1 };
+//  MODE_TABLE (TNRD_PHI_TABLE, reported separately): per filter a cubic Hermite
+//    table on nodes x_k = x_lo + k/kTabPerCentre, x_lo = -kTabPad, built on the
+//    host in double from the exact phi and phi'; interval k holds {c0, c1, c2, c3}
+//    with phi(x_k + f/S) ~= c0 + f (c1 + f (c2 + f c3)), f in [0, 1).  Interval
+//    n_int (one past the last) is all zeros and serves every out-of-range x.
+//    fc = { a_t = S/step, b_t, n_int, b_lo, ... } with b_t + b_lo = -(mu0/step + x_lo) * S
+//    split into fp32 hi/lo words: xs = a_t v + b_t, k = floor(xs),
+//    f = fma(v, a_t, b_t - k) + b_lo (b_t - k is exact).
+enum { MODE_HORNER = 0, MODE_DIRECT = 1, MODE_TABLE = 2 };
+constexpr int kTabPerCentre = 16;     // table intervals per RBF centre spacing
+constexpr int kTabPad = 14;           // centres of zero-free margin on each side
 constexpr int kHornerUnit = 12;
 constexpr int kDirectUnit = 4;
 constexpr int kFc = 8;                // floats of per-filter constants
@@ -68,6 +78,8 @@ struct StageArgs {
     int Nk, pstride, mode;
     int boundary;          // 0 = R1, 1 = R2
     float lambda;
+    const float4 *table;   // MODE_TABLE: this stage's tables, filter i at table + i*table_stride
+    int table_stride;      // float4s per filter (n_int + 1)
     // tiling (filled by launch_stage): tiles in x-fastest, then y, then image order
     int tiles_x, tiles_y, n_tiles;
 };
@@ -76,7 +88,7 @@ struct StageArgs {
 size_t stage_smem_bytes(int ksize, int tile, int Nk, int pstride);
 int choose_tile(int ksize, int B, int H, int W, int num_sms);
 cudaError_t launch_stage(int ksize, int tile, StageArgs &a, int B, cudaStream_t s);
-cudaError_t launch_debug_phi(const float *params, int pstride, int mode, int ksize, int i,
+cudaError_t launch_debug_phi(const float *params, int pstride, int mode, const float4 *table, int ksize, int i,
                              const float *v, float *out, long long n, cudaStream_t s);
 cudaError_t launch_debug_prox(const float *ut, const float *f, float lambda, float *out,
                               long long n, cudaStream_t s);

@@ -152,10 +152,37 @@ __device__ __forceinline__ void horner_units(const float *__restrict__ units, fl
 
 // phi_i on NP value pairs of one lane.  Warp-collective: all lanes must call it
 // with the same `fp` and `mode`.
+// Tabulated phi (MODE_TABLE): one 16-byte table read and a cubic per value.
 template <int NP>
-__device__ __forceinline__ void phi_x2(const float *__restrict__ fp, int mode, const f2 (&v)[NP],
-                                       f2 (&w)[NP]) {
+__device__ __forceinline__ void phi_table_x2(const float4 fc, const float4 *__restrict__ tab, const f2 (&v)[NP],
+                                             f2 (&w)[NP]) {
+    const float a_t = fc.x, b_t = fc.y, b_lo = fc.w;  // b = b_t + b_lo (hi/lo split)
+    const unsigned nint = (unsigned)__float2int_rn(fc.z);
+#pragma unroll
+    for (int e = 0; e < NP; ++e) {
+        float r[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float vv = h ? hi(v[e]) : lo(v[e]);
+            const float kf = floorf(fmaf(vv, a_t, b_t));
+            // b_t - kf is exact, so f carries the full fp32 precision of the fraction
+            const float f = fmaf(vv, a_t, b_t - kf) + b_lo;
+            const int k = __float2int_rz(kf);
+            const float4 c = __ldg(tab + ((unsigned)k < nint ? (unsigned)k : nint));
+            r[h] = fmaf(fmaf(fmaf(c.w, f, c.z), f, c.y), f, c.x);
+        }
+        w[e] = pk(r[0], r[1]);
+    }
+}
+
+template <int NP>
+__device__ __forceinline__ void phi_x2(const float *__restrict__ fp, int mode, const float4 *__restrict__ tab,
+                                       const f2 (&v)[NP], f2 (&w)[NP]) {
     const float4 fc = *reinterpret_cast<const float4 *>(fp);
+    if (mode == MODE_TABLE) {
+        phi_table_x2<NP>(fc, tab, v, w);
+        return;
+    }
     const float a_s = fc.x, two_sg = fc.y, inv_ustep = fc.z;
     const int nunits = __float2int_rn(fc.w);
     const float yclamp = fp[4];  // Horner: upper bound of the R exponent
@@ -353,7 +380,8 @@ __device__ __forceinline__ void phase_conv(const float *__restrict__ fpar, const
 // reads as an in-image v).  Warp-collective per run.
 template <class G>
 __device__ __forceinline__ void phase_phi(const StageArgs &a, const TileGeo &gA, const TileGeo &gB,
-                                          const float *__restrict__ fpar, f2 *Wb, int yt) {
+                                          const float *__restrict__ fpar, const float4 *__restrict__ tab, f2 *Wb,
+                                          int yt) {
     constexpr int R = G::R, KT = G::KT, RUNW = G::RUNWY;
     constexpr int WWc = G::WWc, RPR = G::RPRY, WH = G::WH, NRUN = G::NRUNY, PW = G::PW;
     constexpr bool AL = RUNW % 2 == 0;  // runs start 16-byte aligned
@@ -372,7 +400,7 @@ __device__ __forceinline__ void phase_phi(const StageArgs &a, const TileGeo &gA,
 #pragma unroll
         for (int e = 0; e < RUNW; ++e) w[e] = v[e];
 #else
-        phi_x2<RUNW>(fpar + KT, a.mode, v, w);
+        phi_x2<RUNW>(fpar + KT, a.mode, tab, v, w);
 #endif
         if (valid) {
             const int pyA = gA.y0 - R + wr, pyB = gB.y0 - R + wr;
@@ -558,7 +586,8 @@ __global__ void __launch_bounds__(32 * (C::XW + C::YW), C::MINB) stage_kernel(co
         for (int i = 0; i < Nk; ++i) {
             const int slot = i % NSLOT;
             named_sync(BAR_VFULL + slot, NT);
-            phase_phi<G>(a, gA, gB, s_par + i * a.pstride, s_w + slot * SLOT, yt);
+            phase_phi<G>(a, gA, gB, s_par + i * a.pstride, a.table + (size_t)i * a.table_stride,
+                         s_w + slot * SLOT, yt);
             named_arrive(BAR_WFULL + slot, NT);
         }
         return;
@@ -685,13 +714,13 @@ cudaError_t launch(StageArgs &a, int B, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-__global__ void debug_phi_kernel(const float *__restrict__ fp, int mode, const float *__restrict__ v,
-                                 float *__restrict__ out, long long n) {
+__global__ void debug_phi_kernel(const float *__restrict__ fp, int mode, const float4 *__restrict__ tab,
+                                 const float *__restrict__ v, float *__restrict__ out, long long n) {
     // each thread evaluates a pair (elements 2t, 2t+1) through the stage kernel's phi_x2
     const long long i = 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
     f2 vv[1] = {pk(i < n ? v[i] : 0.0f, i + 1 < n ? v[i + 1] : 0.0f)};
     f2 ww[1];
-    phi_x2<1>(fp, mode, vv, ww);  // every lane participates (warp-collective)
+    phi_x2<1>(fp, mode, tab, vv, ww);  // every lane participates (warp-collective)
     if (i < n) out[i] = lo(ww[0]);
     if (i + 1 < n) out[i + 1] = hi(ww[0]);
 }
@@ -734,12 +763,12 @@ cudaError_t launch_stage(int ksize, int tile, StageArgs &a, int B, cudaStream_t 
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_debug_phi(const float *params, int pstride, int mode, int ksize, int i,
+cudaError_t launch_debug_phi(const float *params, int pstride, int mode, const float4 *table, int ksize, int i,
                              const float *v, float *out, long long n, cudaStream_t s) {
     const float *fp = params + (long long)i * pstride + tap_floats(ksize);
     const int threads = 256;
     const long long blocks = ((n + 1) / 2 + threads - 1) / threads;
-    if (blocks > 0) debug_phi_kernel<<<(unsigned)blocks, threads, 0, s>>>(fp, mode, v, out, n);
+    if (blocks > 0) debug_phi_kernel<<<(unsigned)blocks, threads, 0, s>>>(fp, mode, table, v, out, n);
     return cudaGetLastError();
 }
 

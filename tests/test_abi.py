@@ -49,8 +49,8 @@ def test_create_rejects_bad_shapes_before_touching_the_device():
             P.tnrd_create(*args)
         assert ei.value.status == status, (args, str(ei.value))
     with pytest.raises(P.TNRDError) as ei:
-        P.tnrd_create(2, 8, 3, 63, phi_mode=1)
-    assert ei.value.status == 6
+        P.tnrd_create(2, 8, 3, 63, phi_mode=7)  # unknown phi mode (0 exact, 1 table)
+    assert ei.value.status == 1
 
 
 def test_null_handle_calls_fail_cleanly():

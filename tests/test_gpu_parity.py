@@ -45,8 +45,8 @@ def P():
     return P
 
 
-def _gpu_denoise(P, torch, model, f, boundary=0, peak=None):
-    eng = P.TNRD(model, boundary=boundary)
+def _gpu_denoise(P, torch, model, f, boundary=0, peak=None, phi_mode=0):
+    eng = P.TNRD(model, boundary=boundary, phi_mode=phi_mode)
     ft = torch.from_numpy(np.ascontiguousarray(f, np.float32)).cuda()
     u = eng.denoise(ft, peak=peak)
     torch.cuda.synchronize()
@@ -318,4 +318,54 @@ def test_invalid_arguments_on_device(torch_cuda, P):
         P.tnrd_set_stage_params(h, 0, p.model.filters[0], p.model.rbf_w[0], p.model.rbf_mu0[0],
                                 p.model.rbf_step[0], p.model.rbf_gamma[0], -1.0)
     P.tnrd_destroy(h)
+    eng.close()
+
+
+# ------------------------------------------------------------------ tabulated phi (TNRD_PHI_TABLE)
+# The optional variant of BASELINE.json north_star item 2, held to the same
+# tolerance as the exact path.
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_table_phi_full_config_parity(torch_cuda, P, cfg):
+    p = make_problem(cfg)
+    u_ref = oracle.denoise(p.f[0], p.model)
+    u = _gpu_denoise(P, torch_cuda, p.model, p.f, peak=p.peaks, phi_mode=P.PHI_TABLE)[0]
+    _assert_parity(u, u_ref, float(p.peaks[0]), p.clean[0], f"table C{cfg}")
+
+
+def test_table_phi_c4_windows(torch_cuda, P):
+    p = make_problem(4)
+    u = _gpu_denoise(P, torch_cuda, p.model, p.f, peak=p.peaks, phi_mode=P.PHI_TABLE)
+    rng = np.random.default_rng(44)
+    for b in [0, 1, 2, 3, 4, 200]:
+        for (y0, y1, x0, x1) in _windows(512, 512, 1, rng)[:3]:
+            ref = oracle.denoise_window(p.f[b], p.model, y0, y1, x0, x1)
+            _assert_parity(u[b, y0:y1, x0:x1], ref, float(p.peaks[b]), what=f"table C4 b={b} win=({y0},{x0})")
+
+
+def test_table_phi_stress_and_micro(torch_cuda, P):
+    """phi-stress stage (narrow grid, large weights) and the table against the
+    oracle's direct sum over the whole grid, including out-of-range values."""
+    torch = torch_cuda
+    rng = np.random.default_rng(17)
+    f = rng.poisson(3.0, size=(96, 96)).astype(np.float32)
+    m = stress_model(rng, 1, 24, 5, 63, float(f.max()))
+    u = _gpu_denoise(P, torch, m, f[None], phi_mode=P.PHI_TABLE)[0]
+    _assert_parity(u, oracle.denoise(f, m), 4.0, what="table stress k=5")
+    p = make_problem(3)
+    eng = P.TNRD(p.model, phi_mode=P.PHI_TABLE)
+    for (t, i) in [(0, 0), (5, 31)]:
+        mu0, step = float(p.model.rbf_mu0[t, i]), float(p.model.rbf_step[t, i])
+        xs = np.linspace(-20, 82, 30001)
+        v = (mu0 + step * xs).astype(np.float32)
+        out = torch.empty(v.shape, device="cuda")
+        P.tnrd_debug_phi(eng.h, t, i, torch.from_numpy(v).cuda(), out)
+        ref = oracle.phi(p.model.rbf_w[t, i], mu0, step, float(p.model.rbf_gamma[t, i]), v.astype(np.float64))
+        got = out.cpu().numpy()
+        err = np.abs(got - ref)
+        scale = float(np.abs(p.model.rbf_w[t, i]).max())
+        MARGINS[f"table phi t{t} i{i}"] = float(err.max() / scale)
+        # cubic Hermite error h^4/384 * max|phi^(4)| with h = 1/16 centre is ~1e-8 of
+        # scale; the fp32 cubic and fraction add a few ulp of phi (DESIGN.md §5.6)
+        assert err.max() < 1e-6 * scale, (t, i, err.max())
+        assert np.all(got[np.abs(xs - 31) > 45.5] == 0.0)  # outside the table: exactly 0
     eng.close()
