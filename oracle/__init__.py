@@ -31,6 +31,9 @@ BOUNDARY_EXPLICIT = 0  # R1: symmetric-extension rotated-kernel convolution (P l
 BOUNDARY_ADJOINT = 1   # R2: exact transpose K^T (P l.298-301; S l.57-65)
 PHI_RBF = 0
 PHI_LINEAR = 1
+REACTION_PROX = 0      # Poisson proximal step, P Eq.13 (the method)
+REACTION_GAUSSIAN = 1  # psi = lambda (u_t - f), P Eq.3 with A = I (l.150-158)
+REACTION_POISSON_GRADIENT = 2  # psi = lambda (1 - f/u_t), the rejected direct step (l.247-252)
 
 
 def build(force: bool = False) -> str:
@@ -59,8 +62,10 @@ def lib() -> ctypes.CDLL:
             L.oracle_prox.argtypes = [ctypes.c_double] * 3
             L.oracle_prox.restype = ctypes.c_double
             L.oracle_stage.argtypes = [i, i, dp, dp, i, i, i, dp, dp, dp, dp, dp, ctypes.c_double,
-                                       i, i, dp, dp]
-            L.oracle_denoise.argtypes = [i, i, dp, i, i, i, i, dp, dp, dp, dp, dp, dp, i, i, dp]
+                                       i, i, i, dp, dp]
+            L.oracle_denoise.argtypes = [i, i, dp, i, i, i, i, dp, dp, dp, dp, dp, dp, i, i, i, dp]
+            L.oracle_reaction.argtypes = [ctypes.c_double] * 4 + [i]
+            L.oracle_reaction.restype = ctypes.c_double
             _lib = L
     return _lib
 
@@ -103,6 +108,15 @@ def phi(w, mu0: float, step: float, gamma: float, z) -> np.ndarray:
     return out.reshape(zz.shape)
 
 
+def reaction(u, ut, f, lam, kind: int) -> np.ndarray:
+    """The stage's pointwise reaction (oracle_reaction) on arrays."""
+    u, ut, f = np.broadcast_arrays(*(np.asarray(x, np.float64) for x in (u, ut, f)))
+    L = lib()
+    out = np.array([L.oracle_reaction(float(a), float(b), float(c), float(lam), int(kind))
+                    for a, b, c in zip(u.ravel(), ut.ravel(), f.ravel())])
+    return out.reshape(u.shape)
+
+
 def prox(ut, lam, f) -> np.ndarray:
     ut, lam, f = np.broadcast_arrays(np.asarray(ut, np.float64), np.asarray(lam, np.float64),
                                      np.asarray(f, np.float64))
@@ -118,8 +132,8 @@ def _model_arrays(model):
 
 
 def stage(u, f, model, t: int = 0, boundary: int = BOUNDARY_EXPLICIT, phi_mode: int = PHI_RBF,
-          return_u_tilde: bool = False):
-    """One stage of Eq.13 with params[t]."""
+          return_u_tilde: bool = False, reaction: int = REACTION_PROX):
+    """One stage of Eq.13 (or Eq.3 with another reaction) with params[t]."""
     u, f = _d(u), _d(f)
     H, W = u.shape
     filt, w, mu0, step, gam, lam = _model_arrays(model)
@@ -128,26 +142,27 @@ def stage(u, f, model, t: int = 0, boundary: int = BOUNDARY_EXPLICIT, phi_mode: 
     ut = np.empty_like(u)
     lib().oracle_stage(H, W, _p(u), _p(f), Nk, m, M, _p(_d(filt[t])), _p(_d(w[t])),
                        _p(_d(mu0[t])), _p(_d(step[t])), _p(_d(gam[t])), float(lam[t]),
-                       boundary, phi_mode, _p(out), _p(ut))
+                       boundary, phi_mode, reaction, _p(out), _p(ut))
     return (out, ut) if return_u_tilde else out
 
 
-def denoise(f, model, boundary: int = BOUNDARY_EXPLICIT, phi_mode: int = PHI_RBF) -> np.ndarray:
+def denoise(f, model, boundary: int = BOUNDARY_EXPLICIT, phi_mode: int = PHI_RBF,
+            reaction: int = REACTION_PROX) -> np.ndarray:
     """u_T for one image f [H][W] (or a batch [B][H][W], looped)."""
     f = _d(f)
     if f.ndim == 3:
-        return np.stack([denoise(fi, model, boundary, phi_mode) for fi in f])
+        return np.stack([denoise(fi, model, boundary, phi_mode, reaction) for fi in f])
     H, W = f.shape
     filt, w, mu0, step, gam, lam = _model_arrays(model)
     T, Nk, m, M = filt.shape[0], filt.shape[1], filt.shape[2], w.shape[2]
     out = np.empty_like(f)
     lib().oracle_denoise(H, W, _p(f), T, Nk, m, M, _p(filt), _p(w), _p(mu0), _p(step), _p(gam),
-                         _p(lam), boundary, phi_mode, _p(out))
+                         _p(lam), boundary, phi_mode, reaction, _p(out))
     return out
 
 
 def denoise_window(f, model, y0: int, y1: int, x0: int, x1: int,
-                   boundary: int = BOUNDARY_EXPLICIT) -> np.ndarray:
+                   boundary: int = BOUNDARY_EXPLICIT, reaction: int = REACTION_PROX) -> np.ndarray:
     """u_T on the window [y0,y1) x [x0,x1) of a large image, computed exactly on a
     crop with a 2rT dependency margin (pin P12: the output depends on the input
     only within radius 2rT; crop edges on true image edges need no margin)."""
@@ -156,7 +171,7 @@ def denoise_window(f, model, y0: int, y1: int, x0: int, x1: int,
     R = 2 * (model.k // 2) * model.T
     cy0, cy1 = max(0, y0 - R), min(H, y1 + R)
     cx0, cx1 = max(0, x0 - R), min(W, x1 + R)
-    u = denoise(f[cy0:cy1, cx0:cx1], model, boundary)
+    u = denoise(f[cy0:cy1, cx0:cx1], model, boundary, reaction=reaction)
     return u[y0 - cy0:y1 - cy0, x0 - cx0:x1 - cx0]
 
 

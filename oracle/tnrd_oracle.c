@@ -101,6 +101,22 @@ EXPORT double oracle_prox(double ut, double lam, double f) {
     return 2.0 * lam * f / (sigma - delta);
 }
 
+/* Reaction of one stage (pointwise), given u_t, the diffusion result
+ * ut = u_t - sum_i kbar_i * phi_i(k_i * u_t) and f:
+ *   reaction 0: Poisson proximal step, P Eq.13 (l.326-333): prox_lambda(ut).
+ *   reaction 1: Gaussian denoising, P Eq.3 (l.134-141) with the reaction
+ *               psi(u_t, f) = lambda A^T (A u_t - f), A = I (l.150-158):
+ *               ut - lambda (u_t - f).
+ *   reaction 2: the direct Poisson gradient the paper rejects (l.247-252):
+ *               P Eq.3 with psi = grad of D = lambda <u - f log u, 1> (Eq.4,
+ *               l.163-167), i.e. ut - lambda (1 - f / u_t); where f = 0 the data
+ *               term is lambda u, so f / u_t is taken as 0 there. */
+EXPORT double oracle_reaction(double u, double ut, double f, double lam, int reaction) {
+    if (reaction == 1) return ut - lam * (u - f);
+    if (reaction == 2) return ut - lam * (1.0 - (f == 0.0 ? 0.0 : f / u));
+    return oracle_prox(ut, lam, f);
+}
+
 /* One diffusion stage, P Eq.13 (l.326-333):
  *   ut = u - sum_i kbar_i * phi_i(k_i * u),   u_next = prox_lambda(ut).
  * boundary 0 (R1, default): the second convolution is the explicit rotated-kernel
@@ -115,7 +131,7 @@ EXPORT void oracle_stage(int H, int W, const double *u, const double *f,
                          const double *filters, /* [Nk][m][m] */
                          const double *rbf_w,   /* [Nk][M] */
                          const double *mu0, const double *step, const double *gamma, /* [Nk] */
-                         double lam, int boundary, int phi_mode,
+                         double lam, int boundary, int phi_mode, int reaction,
                          double *u_next, double *u_tilde_out /* may be NULL */) {
     size_t N = (size_t)H * W;
     double *v = (double *)malloc(sizeof(double) * N);
@@ -140,7 +156,7 @@ EXPORT void oracle_stage(int H, int W, const double *u, const double *f,
     for (size_t p = 0; p < N; ++p) {
         double ut = u[p] - d[p];                                  /* tau = 1, l.333  */
         if (u_tilde_out) u_tilde_out[p] = ut;
-        u_next[p] = oracle_prox(ut, lam, f[p]);
+        u_next[p] = oracle_reaction(u[p], ut, f[p], lam, reaction);
     }
     free(v); free(d); free(t); free(kbar);
 }
@@ -150,7 +166,7 @@ EXPORT void oracle_stage(int H, int W, const double *u, const double *f,
 EXPORT void oracle_denoise(int H, int W, const double *f, int T, int Nk, int m, int M,
                            const double *filters, const double *rbf_w, const double *mu0,
                            const double *step, const double *gamma, const double *lam,
-                           int boundary, int phi_mode, double *u_out) {
+                           int boundary, int phi_mode, int reaction, double *u_out) {
     size_t N = (size_t)H * W;
     double *a = (double *)malloc(sizeof(double) * N);
     double *b = (double *)malloc(sizeof(double) * N);
@@ -159,7 +175,7 @@ EXPORT void oracle_denoise(int H, int W, const double *f, int T, int Nk, int m, 
         oracle_stage(H, W, a, f, Nk, m, M,
                      filters + (size_t)s * Nk * m * m, rbf_w + (size_t)s * Nk * M,
                      mu0 + (size_t)s * Nk, step + (size_t)s * Nk, gamma + (size_t)s * Nk,
-                     lam[s], boundary, phi_mode, b, NULL);
+                     lam[s], boundary, phi_mode, reaction, b, NULL);
         double *tmp = a; a = b; b = tmp;
     }
     memcpy(u_out, a, sizeof(double) * N);

@@ -378,3 +378,54 @@ def test_psnr_golden():
     (peak, off, expect), = _golden("psnr_examples.txt")
     ref = np.full((8, 8), 100.0)
     assert abs(oracle.psnr(ref + off, ref, peak) - expect) < 1e-9
+
+
+# ---------------------------------------------------------------- reaction variants
+def test_gaussian_reaction_linear_phi_is_dense_linear_update():
+    """P Eq.3 with psi = lambda (u - f) (A = I, P l.150-158) and linear phi_i(z) = c_i z:
+    u1 = (I - sum_i c_i Kbar_i K_i) u0 - lambda (u0 - f), dense matrices built here."""
+    rng = _rng(21)
+    H, W, m, Nk = 9, 8, 3, 3
+    f = rng.poisson(3.0, size=(H, W)).astype(np.float64)
+    u0 = f + rng.normal(0, 0.3, size=(H, W))
+    model = make_model(rng, 1, Nk, m, 5, 4.0)
+    model.rbf_w[0, :, 0] = rng.normal(0, 0.2, Nk)
+    c = model.rbf_w[0, :, 0].astype(np.float64)  # the oracle sees the fp32-rounded slopes
+    A = np.eye(H * W)
+    for i in range(Nk):
+        k = model.filters[0, i].astype(np.float64)
+        A -= c[i] * _dense_conv_matrix(H, W, k[::-1, ::-1]) @ _dense_conv_matrix(H, W, k)
+    lam = float(model.lam[0])
+    ref = (A @ u0.ravel() - lam * (u0.ravel() - f.ravel())).reshape(H, W)
+    got = oracle.stage(u0, f, model, 0, phi_mode=oracle.PHI_LINEAR, reaction=oracle.REACTION_GAUSSIAN)
+    assert np.max(np.abs(got - ref)) < 1e-12
+
+
+def test_reactions_with_zero_filters_are_scalar_iterations():
+    """Zero filters leave only the reaction: Gaussian u_{t+1} - f = (1 - lambda)(u_t - f);
+    direct Poisson gradient u_{t+1} = u_t - lambda (1 - f/u_t), and lambda u alone where f = 0."""
+    rng = _rng(22)
+    m = zero_model(3, 4, 3, 9, "filters", [0.3, 0.5, 0.7])
+    f = rng.integers(0, 6, size=(6, 7)).astype(np.float64)
+    u = f + rng.uniform(0.5, 1.0, size=f.shape)
+    ug, up = u.copy(), u.copy()
+    for t in range(3):
+        lam = float(m.lam[t])
+        ug = oracle.stage(ug, f, m, t, reaction=oracle.REACTION_GAUSSIAN)
+        up = oracle.stage(up, f, m, t, reaction=oracle.REACTION_POISSON_GRADIENT)
+    g = np.prod(1.0 - np.asarray(m.lam, np.float64))
+    assert np.max(np.abs(ug - (f + g * (u - f)))) < 1e-12
+    v = u.copy()
+    for t in range(3):
+        lam = float(m.lam[t])
+        v = v - lam * (1.0 - np.where(f == 0, 0.0, f / v))
+    assert np.max(np.abs(up - v)) < 1e-12
+
+
+def test_direct_poisson_gradient_loses_positivity_and_prox_does_not():
+    """P l.247-252: the direct step 1 - f/u 'can not guarantee that the output image
+    after one diffusion step is positive'; the prox (Eq.12) keeps u > 0 for f > 0."""
+    lam = 2.0
+    assert oracle.reaction(1.0, 1.0, 0.0, lam, oracle.REACTION_POISSON_GRADIENT) == -1.0
+    assert oracle.reaction(0.5, 0.5, 3.0, lam, oracle.REACTION_POISSON_GRADIENT) < 12.0
+    assert oracle.reaction(1.0, -5.0, 3.0, lam, oracle.REACTION_PROX) > 0.0
