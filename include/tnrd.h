@@ -74,9 +74,21 @@ typedef enum {
                               (DESIGN.md §5.6); an optional variant, reported separately */
 } tnrd_phi_mode;
 
+typedef enum {
+    /* Poisson denoising (the method): proximal step of P Eq.12-13 (l.313-333). */
+    TNRD_REACTION_POISSON_PROX = 0,
+    /* Gaussian denoising: P Eq.3 (l.134-141) with psi(u_t, f) = lambda (u_t - f),
+     * i.e. lambda A^T (A u - f) with A = I (l.150-158). */
+    TNRD_REACTION_GAUSSIAN = 1,
+    /* Ablation: the direct Poisson gradient psi = lambda (1 - f / u_t) that the
+     * paper rejects (l.247-252); f / u_t is taken as 0 where f = 0.  Not
+     * positivity preserving; undefined (IEEE inf/NaN) where u_t = 0 < f. */
+    TNRD_REACTION_POISSON_GRADIENT = 2
+} tnrd_reaction;
+
 /* Model shape.  T >= 1 stages, n_filters = N_k >= 1 (P l.423: N_k = m^2 - 1 if
  * not specified, not enforced), ksize = m in {3, 5, 7}, n_rbf = M in [1, 256],
- * device = CUDA ordinal. */
+ * device = CUDA ordinal, reaction = tnrd_reaction (0 = the paper's Eq.13). */
 typedef struct {
     int T;
     int n_filters;
@@ -85,7 +97,7 @@ typedef struct {
     int boundary;   /* tnrd_boundary */
     int phi_mode;   /* tnrd_phi_mode */
     int device;
-    int reserved;   /* must be 0 */
+    int reaction;   /* tnrd_reaction (was a reserved 0 field: 0 keeps Eq.13) */
 } tnrd_desc;
 
 /* ABI version this library implements (TNRD_ABI_VERSION). */

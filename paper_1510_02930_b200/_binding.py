@@ -27,6 +27,9 @@ BC_SYMMETRIC_EXPLICIT = 0
 BC_SYMMETRIC_ADJOINT = 1
 PHI_EXACT = 0
 PHI_TABLE = 1
+REACTION_POISSON_PROX = 0
+REACTION_GAUSSIAN = 1
+REACTION_POISSON_GRADIENT = 2
 
 
 class TNRDError(RuntimeError):
@@ -38,7 +41,7 @@ class TNRDError(RuntimeError):
 class tnrd_desc(ctypes.Structure):
     _fields_ = [("T", ctypes.c_int), ("n_filters", ctypes.c_int), ("ksize", ctypes.c_int),
                 ("n_rbf", ctypes.c_int), ("boundary", ctypes.c_int), ("phi_mode", ctypes.c_int),
-                ("device", ctypes.c_int), ("reserved", ctypes.c_int)]
+                ("device", ctypes.c_int), ("reaction", ctypes.c_int)]
 
 
 def _load() -> ctypes.CDLL:
@@ -133,8 +136,8 @@ def tnrd_status_string(status: int) -> str:
 
 
 def tnrd_create(T: int, n_filters: int, ksize: int, n_rbf: int, boundary: int = 0,
-                phi_mode: int = 0, device: int = 0) -> int:
-    d = tnrd_desc(T, n_filters, ksize, n_rbf, boundary, phi_mode, device, 0)
+                phi_mode: int = 0, device: int = 0, reaction: int = 0) -> int:
+    d = tnrd_desc(T, n_filters, ksize, n_rbf, boundary, phi_mode, device, reaction)
     h = ctypes.c_void_p()
     _check(_lib.tnrd_create(ctypes.byref(d), ctypes.byref(h)))
     return h.value
@@ -247,12 +250,13 @@ class TNRD:
     rbf_mu0 / rbf_step / rbf_gamma [T][Nk], lam [T] (e.g. synth.Model).
     """
 
-    def __init__(self, model, boundary: int = BC_SYMMETRIC_EXPLICIT, device: int = 0, phi_mode: int = PHI_EXACT):
+    def __init__(self, model, boundary: int = BC_SYMMETRIC_EXPLICIT, device: int = 0, phi_mode: int = PHI_EXACT,
+                 reaction: int = REACTION_POISSON_PROX):
         T, Nk, k, _ = np.shape(model.filters)
         M = np.shape(model.rbf_w)[2]
         self.T, self.Nk, self.k, self.M = int(T), int(Nk), int(k), int(M)
         self.device = device
-        self.h = tnrd_create(self.T, self.Nk, self.k, self.M, boundary, phi_mode, device)
+        self.h = tnrd_create(self.T, self.Nk, self.k, self.M, boundary, phi_mode, device, reaction)
         for t in range(self.T):
             tnrd_set_stage_params(self.h, t, model.filters[t], model.rbf_w[t], model.rbf_mu0[t],
                                   model.rbf_step[t], model.rbf_gamma[t], model.lam[t])

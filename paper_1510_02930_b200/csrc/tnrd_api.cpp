@@ -166,6 +166,7 @@ tnrd_status launch_one(tnrd_handle *h, int t, int tile, StageArgs &a, int B, cud
     a.table = h->d_table ? h->d_table + (size_t)t * h->d.n_filters * h->table_stride : nullptr;
     a.table_stride = h->table_stride;
     a.boundary = h->d.boundary;
+    a.reaction = h->d.reaction;
     a.lambda = h->lambda[t];
     if (h->profile) {
         if ((size_t)h->ev_used + 2 > h->ev.size()) {
@@ -373,7 +374,8 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
     if (d->boundary != 0 && d->boundary != 1) return fail(nullptr, TNRD_EINVAL, "bad boundary %d", d->boundary);
     if (d->phi_mode != TNRD_PHI_EXACT && d->phi_mode != TNRD_PHI_TABLE)
         return fail(nullptr, TNRD_EINVAL, "bad phi_mode %d", d->phi_mode);
-    if (d->reserved != 0) return fail(nullptr, TNRD_EINVAL, "reserved field must be 0");
+    if (d->reaction < TNRD_REACTION_POISSON_PROX || d->reaction > TNRD_REACTION_POISSON_GRADIENT)
+        return fail(nullptr, TNRD_EINVAL, "bad reaction %d", d->reaction);
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess) return fail(nullptr, TNRD_ECUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));

@@ -77,6 +77,7 @@ struct StageArgs {
     int avail_lo, avail_hi;// rows of u_in that may be read
     int Nk, pstride, mode;
     int boundary;          // 0 = R1, 1 = R2
+    int reaction;          // tnrd_reaction
     float lambda;
     const float4 *table;   // MODE_TABLE: this stage's tables, filter i at table + i*table_stride
     int table_stride;      // float4s per filter (n_int + 1)

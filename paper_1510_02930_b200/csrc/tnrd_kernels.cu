@@ -118,6 +118,16 @@ __device__ __forceinline__ float prox_poisson(float ut, float lam, float f) {
     return __fdiv_rn(2.0f * lam * f, sigma - delta);
 }
 
+// Reaction of the stage (tnrd_reaction), pointwise, after the diffusion
+// ut = u - d: the Poisson prox of Eq.13 (P l.326-333), or P Eq.3 with
+// psi = lambda (u - f) (Gaussian, l.150-158) or psi = lambda (1 - f/u) (the
+// direct Poisson gradient, l.247-252; f/u taken as 0 where f = 0).
+__device__ __forceinline__ float reaction_step(int kind, float u, float ut, float lam, float f) {
+    if (kind == 1) return fmaf(-lam, u - f, ut);
+    if (kind == 2) return fmaf(-lam, 1.0f - (f == 0.0f ? 0.0f : __fdiv_rn(f, u)), ut);
+    return prox_poisson(ut, lam, f);
+}
+
 // Horner units [u0, u1] on NP pairs (see tnrd_internal.h).  Each unit is
 // expanded from its first centre: t = sg (x - 8b), G = 2^(-t^2), R = 2^(two_sg t),
 // block sum = G * sum_{e<8} c_e R^e  (2 MUFU per element).  R is clamped above at
@@ -677,7 +687,7 @@ __global__ void __launch_bounds__(32 * (C::XW + C::YW), C::MINB) stage_kernel(co
                 const float u = h ? hi(u2) : lo(u2);
                 const float d = h ? hi(acc[ry][e]) : lo(acc[ry][e]);
                 const float fv = __ldg(fb + (long long)(oy - a.f.row_base) * a.f.ld + ox);
-                ob[(long long)(oy - a.out_row_base) * a.out_ld + ox] = prox_poisson(u - d, a.lambda, fv);
+                ob[(long long)(oy - a.out_row_base) * a.out_ld + ox] = reaction_step(a.reaction, u, u - d, a.lambda, fv);
             }
         }
     }

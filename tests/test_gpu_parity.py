@@ -45,8 +45,8 @@ def P():
     return P
 
 
-def _gpu_denoise(P, torch, model, f, boundary=0, peak=None, phi_mode=0):
-    eng = P.TNRD(model, boundary=boundary, phi_mode=phi_mode)
+def _gpu_denoise(P, torch, model, f, boundary=0, peak=None, phi_mode=0, reaction=0):
+    eng = P.TNRD(model, boundary=boundary, phi_mode=phi_mode, reaction=reaction)
     ft = torch.from_numpy(np.ascontiguousarray(f, np.float32)).cuda()
     u = eng.denoise(ft, peak=peak)
     torch.cuda.synchronize()
@@ -369,3 +369,25 @@ def test_table_phi_stress_and_micro(torch_cuda, P):
         assert err.max() < 1e-6 * scale, (t, i, err.max())
         assert np.all(got[np.abs(xs - 31) > 45.5] == 0.0)  # outside the table: exactly 0
     eng.close()
+
+
+# ------------------------------------------------------------------ reaction variants
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_gaussian_reaction_parity(torch_cuda, P, cfg):
+    """P Eq.3 with psi = lambda (u_t - f) (Gaussian denoising, A = I, P l.150-158)."""
+    p = make_problem(cfg)
+    u_ref = oracle.denoise(p.f[0], p.model, reaction=oracle.REACTION_GAUSSIAN)
+    u = _gpu_denoise(P, torch_cuda, p.model, p.f, reaction=P.REACTION_GAUSSIAN)[0]
+    _assert_parity(u, u_ref, float(p.peaks[0]), what=f"gaussian C{cfg}")
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_poisson_gradient_reaction_parity(torch_cuda, P, cfg):
+    """The direct Poisson gradient step (P l.247-252), on counts shifted to be
+    positive so that the step stays defined."""
+    p = make_problem(cfg)
+    f = p.f + 1.0
+    u_ref = oracle.denoise(f[0], p.model, reaction=oracle.REACTION_POISSON_GRADIENT)
+    assert np.all(np.isfinite(u_ref))
+    u = _gpu_denoise(P, torch_cuda, p.model, f, reaction=P.REACTION_POISSON_GRADIENT)[0]
+    _assert_parity(u, u_ref, float(p.peaks[0]) + 1.0, what=f"poisson-gradient C{cfg}")
