@@ -64,6 +64,9 @@ def lib() -> ctypes.CDLL:
             L.oracle_stage.argtypes = [i, i, dp, dp, i, i, i, dp, dp, dp, dp, dp, ctypes.c_double,
                                        i, i, i, dp, dp]
             L.oracle_denoise.argtypes = [i, i, dp, i, i, i, i, dp, dp, dp, dp, dp, dp, i, i, i, dp]
+            L.oracle_loss_grad.argtypes = [i, i, dp, dp, i, i, i, i, dp, dp, dp, dp, dp, dp, i, dp, dp, dp]
+            L.oracle_loss_grad.restype = ctypes.c_double
+            L.oracle_kernel_grad.argtypes = [i, i, dp, dp, i, dp]
             L.oracle_reaction.argtypes = [ctypes.c_double] * 4 + [i]
             L.oracle_reaction.restype = ctypes.c_double
             _lib = L
@@ -159,6 +162,24 @@ def denoise(f, model, boundary: int = BOUNDARY_EXPLICIT, phi_mode: int = PHI_RBF
     lib().oracle_denoise(H, W, _p(f), T, Nk, m, M, _p(filt), _p(w), _p(mu0), _p(step), _p(gam),
                          _p(lam), boundary, phi_mode, reaction, _p(out))
     return out
+
+
+def loss_grad(f, u_gt, model, boundary: int = BOUNDARY_EXPLICIT):
+    """Loss 1/2 ||u_T - u_gt||^2 (P Eq.6) and its gradient (P Eq.14-20) for one image.
+    Returns (loss, d_filters [T][Nk][k][k], d_rbf_w [T][Nk][M], d_lambda [T]).  Summed
+    over a batch [B][H][W] when given."""
+    f, g = _d(f), _d(u_gt)
+    if f.ndim == 3:
+        parts = [loss_grad(fi, gi, model, boundary) for fi, gi in zip(f, g)]
+        return (sum(p[0] for p in parts), sum(p[1] for p in parts), sum(p[2] for p in parts),
+                sum(p[3] for p in parts))
+    H, W = f.shape
+    filt, w, mu0, step, gam, lam = _model_arrays(model)
+    T, Nk, m, M = filt.shape[0], filt.shape[1], filt.shape[2], w.shape[2]
+    gf, gw, gl = np.zeros_like(filt), np.zeros_like(w), np.zeros_like(lam)
+    loss = lib().oracle_loss_grad(H, W, _p(f), _p(g), T, Nk, m, M, _p(filt), _p(w), _p(mu0), _p(step),
+                                  _p(gam), _p(lam), boundary, _p(gf), _p(gw), _p(gl))
+    return float(loss), gf, gw, gl
 
 
 def denoise_window(f, model, y0: int, y1: int, x0: int, x1: int,

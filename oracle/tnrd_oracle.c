@@ -181,3 +181,114 @@ EXPORT void oracle_denoise(int H, int W, const double *f, int T, int Nk, int m, 
     memcpy(u_out, a, sizeof(double) * N);
     free(a); free(b);
 }
+
+/* ------------------------------------------------------------------ training gradient
+ * Loss l = 1/2 ||u_T - u_gt||^2 (P Eq.6, l.199-222) and its gradient w.r.t.
+ * Theta_t = {lambda_t, phi_i^t (RBF weights), k_i^t} by the chain rule of
+ * P l.343-420 (Eq.14-20), reaction 0 (Eq.13), in double.  Pinned against
+ * central finite differences of oracle_denoise (tests/test_oracle_pins.py). */
+
+/* out[a][b] = d/dk[a][b] <e, conv2d_sym(x, k)> = sum_p e(p) E(x)(p - (a-r, b-r)). */
+EXPORT void oracle_kernel_grad(int H, int W, const double *x, const double *e, int m, double *out) {
+    int r = m / 2;
+    for (int a = 0; a < m; ++a)
+        for (int b = 0; b < m; ++b) {
+            double s = 0.0;
+#pragma omp parallel for reduction(+ : s) schedule(static)
+            for (int p = 0; p < H; ++p) {
+                long pp = mirror_index((long)p - (a - r), H);
+                for (int q = 0; q < W; ++q)
+                    s += e[(long)p * W + q] * x[pp * W + mirror_index((long)q - (b - r), W)];
+            }
+            out[a * m + b] = s;
+        }
+}
+
+/* phi'(z) = sum_j w_j (-(z - mu_j) / gamma^2) exp(-(z - mu_j)^2 / (2 gamma^2))
+ * (the diagonal of Lambda_i, P l.369-371); G_out[j] = exp(-(z - mu_j)^2/(2 gamma^2)),
+ * the derivative of phi w.r.t. w_j. */
+EXPORT double oracle_phi_prime(int M, const double *w, double mu0, double step, double gamma, double z,
+                               double *G_out /* [M] or NULL */) {
+    double s = 0.0;
+    for (int j = 0; j < M; ++j) {
+        double d = z - (mu0 + j * step);
+        double g = exp(-d * d / (2.0 * gamma * gamma));
+        if (G_out) G_out[j] = g;
+        s += w[j] * (-d / (gamma * gamma)) * g;
+    }
+    return s;
+}
+
+EXPORT double oracle_loss_grad(int H, int W, const double *f, const double *u_gt, int T, int Nk, int m, int M,
+                               const double *filters, const double *rbf_w, const double *mu0,
+                               const double *step, const double *gamma, const double *lam, int boundary,
+                               double *g_filters /* [T][Nk][m][m] */, double *g_w /* [T][Nk][M] */,
+                               double *g_lam /* [T] */) {
+    size_t N = (size_t)H * W, mm = (size_t)m * m;
+    double *u = (double *)malloc(sizeof(double) * N * (T + 1));   /* tape u_0..u_T  */
+    double *ut = (double *)malloc(sizeof(double) * N * T);         /* tape ut_0..    */
+    memcpy(u, f, sizeof(double) * N);
+    for (int s = 0; s < T; ++s)
+        oracle_stage(H, W, u + s * N, f, Nk, m, M, filters + s * Nk * mm, rbf_w + (size_t)s * Nk * M,
+                     mu0 + (size_t)s * Nk, step + (size_t)s * Nk, gamma + (size_t)s * Nk, lam[s], boundary, 0, 0,
+                     u + (s + 1) * N, ut + s * N);
+    double loss = 0.0;
+    double *g = (double *)malloc(sizeof(double) * N);
+    for (size_t p = 0; p < N; ++p) {                               /* dl/du_T = u_T - u_gt (l.348-353) */
+        g[p] = u[T * N + p] - u_gt[p];
+        loss += 0.5 * g[p] * g[p];
+    }
+    double *e = (double *)malloc(sizeof(double) * N), *gn = (double *)malloc(sizeof(double) * N);
+    double *v = (double *)malloc(sizeof(double) * N), *wv = (double *)malloc(sizeof(double) * N);
+    double *av = (double *)malloc(sizeof(double) * N), *bv = (double *)malloc(sizeof(double) * N);
+    double *tmp = (double *)malloc(sizeof(double) * N), *kbar = (double *)malloc(sizeof(double) * mm);
+    double *kg = (double *)malloc(sizeof(double) * mm), *G = (double *)malloc(sizeof(double) * M);
+    for (int s = T - 1; s >= 0; --s) {
+        const double L = lam[s];
+        const double *us = u + s * N, *uts = ut + s * N;
+        g_lam[s] = 0.0;
+        for (size_t p = 0; p < N; ++p) {
+            double delta = uts[p] - L, sigma = sqrt(delta * delta + 4.0 * L * f[p]);
+            double y = sigma > 0.0 ? 0.5 * (1.0 + delta / sigma) : 0.5;          /* Eq.16 */
+            double z = sigma > 0.0 ? 0.5 * (-1.0 + (-delta + 2.0 * f[p]) / sigma) : -0.5; /* Eq.19 */
+            e[p] = y * g[p];                                       /* dl/d ut                */
+            g_lam[s] += z * g[p];
+            gn[p] = e[p];                                          /* identity part of Eq.15 */
+        }
+        for (int i = 0; i < Nk; ++i) {
+            const double *k = filters + (s * Nk + i) * mm;
+            const double *wi = rbf_w + ((size_t)s * Nk + i) * M;
+            const double m0 = mu0[(size_t)s * Nk + i], st = step[(size_t)s * Nk + i], ga = gamma[(size_t)s * Nk + i];
+            double *gwi = g_w + ((size_t)s * Nk + i) * M, *gki = g_filters + (s * Nk + i) * mm;
+            for (int j = 0; j < M; ++j) gwi[j] = 0.0;
+            for (size_t q = 0; q < mm; ++q) gki[q] = 0.0;
+            oracle_conv2d_sym(H, W, us, m, k, v);                  /* x = k_i * u_t          */
+            oracle_rot180(m, k, kbar);
+            /* a = (outer operator)^T e: R1 outer = conv with kbar (symmetric ext.), R2 outer = K^T */
+            if (boundary == 1) oracle_conv2d_sym(H, W, e, m, k, av);
+            else oracle_conv2d_adjoint(H, W, e, m, kbar, av);
+            for (size_t p = 0; p < N; ++p) {
+                double dphi = oracle_phi_prime(M, wi, m0, st, ga, v[p], G);
+                wv[p] = oracle_phi(M, wi, m0, st, ga, v[p]);
+                for (int j = 0; j < M; ++j) gwi[j] -= av[p] * G[j];   /* d ut / d w_ij = -outer(G_j) */
+                bv[p] = dphi * av[p];                              /* Lambda_i outer^T e     */
+            }
+            oracle_conv2d_adjoint(H, W, bv, m, k, tmp);           /* K_i^T Lambda_i outer^T e (Eq.15) */
+            for (size_t p = 0; p < N; ++p) gn[p] -= tmp[p];
+            oracle_kernel_grad(H, W, us, bv, m, kg);              /* inner: x = k_i * u_t   */
+            for (size_t q = 0; q < mm; ++q) gki[q] -= kg[q];
+            if (boundary == 1) {                                  /* outer K^T w: <e, K^T w> = <K e, w> */
+                oracle_kernel_grad(H, W, e, wv, m, kg);
+                for (size_t q = 0; q < mm; ++q) gki[q] -= kg[q];
+            } else {                                              /* outer conv(w, kbar)    */
+                oracle_kernel_grad(H, W, wv, e, m, kg);
+                for (int a = 0; a < m; ++a)
+                    for (int b = 0; b < m; ++b) gki[(m - 1 - a) * m + (m - 1 - b)] -= kg[a * m + b];
+            }
+        }
+        memcpy(g, gn, sizeof(double) * N);                         /* dl/du_s                */
+    }
+    free(u); free(ut); free(g); free(e); free(gn); free(v); free(wv); free(av); free(bv);
+    free(tmp); free(kbar); free(kg); free(G);
+    return loss;
+}

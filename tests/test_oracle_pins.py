@@ -429,3 +429,55 @@ def test_direct_poisson_gradient_loses_positivity_and_prox_does_not():
     assert oracle.reaction(1.0, 1.0, 0.0, lam, oracle.REACTION_POISSON_GRADIENT) == -1.0
     assert oracle.reaction(0.5, 0.5, 3.0, lam, oracle.REACTION_POISSON_GRADIENT) < 12.0
     assert oracle.reaction(1.0, -5.0, 3.0, lam, oracle.REACTION_PROX) > 0.0
+
+
+# ---------------------------------------------------------------- training gradient
+def _f64_model(m):
+    return Model(*(np.asarray(a, np.float64).copy() for a in (m.filters, m.rbf_w, m.rbf_mu0, m.rbf_step,
+                                                                 m.rbf_gamma, m.lam)))
+
+
+@pytest.mark.parametrize("boundary", [oracle.BOUNDARY_EXPLICIT, oracle.BOUNDARY_ADJOINT])
+def test_loss_grad_matches_central_finite_differences(boundary):
+    """The analytic chain rule of P Eq.14-20 (oracle.loss_grad) against central
+    differences of l = 1/2 ||u_T - u_gt||^2 (P Eq.6) through the forward oracle, for
+    every filter tap, RBF weight and lambda.  f >= 1 keeps the prox smooth."""
+    rng = _rng(30)
+    H, W, T, Nk, m, M = 10, 9, 2, 3, 3, 7
+    f = (1 + rng.poisson(3.0, size=(H, W))).astype(np.float64)
+    gt = f + rng.normal(0, 0.5, size=(H, W))
+    mdl = _f64_model(make_model(rng, T, Nk, m, M, float(f.max())))
+    mdl.rbf_w *= 4.0  # a visibly nonlinear phi
+    loss, gf, gw, gl = oracle.loss_grad(f, gt, mdl, boundary)
+
+    def L(md):
+        u = oracle.denoise(f, md, boundary)
+        return 0.5 * float(np.sum((u - gt) ** 2))
+
+    assert abs(loss - L(mdl)) < 1e-12 * max(1.0, loss)
+    h = 1e-6
+    for name, grad in (("filters", gf), ("rbf_w", gw), ("lam", gl)):
+        arr = getattr(mdl, name)
+        for idx in np.ndindex(arr.shape):
+            old = arr[idx]
+            arr[idx] = old + h
+            lp = L(mdl)
+            arr[idx] = old - h
+            lm = L(mdl)
+            arr[idx] = old
+            fd = (lp - lm) / (2 * h)
+            assert abs(grad[idx] - fd) < 1e-6 * (1.0 + abs(fd)), (name, idx, grad[idx], fd)
+
+
+def test_kernel_grad_is_the_derivative_of_the_convolution():
+    """d/dk <e, conv2d_sym(x, k)> is linear in k: check against the dense matrix."""
+    rng = _rng(31)
+    H, W, m = 7, 6, 5
+    x, e = rng.normal(size=(H, W)), rng.normal(size=(H, W))
+    out = np.zeros((m, m))
+    oracle.lib().oracle_kernel_grad(H, W, oracle._p(oracle._d(x)), oracle._p(oracle._d(e)), m, oracle._p(out))
+    for a in range(m):
+        for b in range(m):
+            k = np.zeros((m, m))
+            k[a, b] = 1.0
+            assert abs(out[a, b] - float(np.sum(e * oracle.conv2d_sym(x, k)))) < 1e-12
