@@ -185,6 +185,43 @@ def cpu_baseline(p, budget_s=12.0):
                       f"double precision, OpenMP over rows, {dt:.1f} s"}
 
 
+def grad_bench(args):
+    """Training gradient: one tnrd_loss_grad call per step on image 0 of the config
+    (loss against its clean image), CUDA events around each synchronous call."""
+    import torch
+    import paper_1510_02930_b200 as P
+    from synth import make_problem
+    cfg = 3 if args.config == 4 else args.config
+    p = make_problem(cfg)
+    torch.cuda.set_device(0)
+    f = torch.from_numpy(p.f[:1]).cuda()
+    gt = torch.from_numpy(p.clean[:1]).cuda()
+    eng = P.TNRD(p.model, device=0)
+    for _ in range(args.warmup):
+        eng.loss_grad(f, gt)
+    torch.cuda.synchronize()
+    n0 = P.tnrd_launch_count(eng.h)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            eng.loss_grad(f, gt)
+        ev1.record()
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    _, H, W = p.f.shape
+    line = {"metric": "training-gradient MPix/s (loss + dl/dTheta, P Eq.14-20, fp32)", "mode": "grad",
+            "value": H * W / 1e6 / (ms / 1e3), "unit": "MPix/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": f"{p.cfg['name']} image 0 vs its clean image, "
+                                                        f"T={p.model.T}, Nk={p.model.Nk}, k={p.model.k}, M={p.model.M}"},
+            "stage_launches_per_step": (P.tnrd_launch_count(eng.h) - n0) // args.steps,
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+    eng.close()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -192,6 +229,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4, choices=[3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="infer", choices=["infer", "grad"],
+                    help="infer: the inference pass (the headline); grad: the training gradient "
+                         "(tnrd_loss_grad, P Eq.14-20) on one image of --config (default C3), reported separately")
     ap.add_argument("--phi", default="exact", choices=["exact", "table"],
                     help="exact RBF sum (the headline) or the tabulated variant (reported separately)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -200,6 +240,8 @@ def main():
     rank, world, local = dist_env()
     if args.impl == "reference":
         return reference_arm(args, rank, world)
+    if args.mode == "grad":
+        return grad_bench(args)
 
     import torch
     import torch.distributed as dist

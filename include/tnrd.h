@@ -156,6 +156,26 @@ TNRD_API const char *tnrd_last_error(const tnrd_handle *h);
  * gpu_launches count). */
 TNRD_API unsigned long long tnrd_launch_count(const tnrd_handle *h);
 
+/* ---------------- training gradient (P Eq.6-7, 14-20) ----------------
+ * loss = 1/2 sum_b ||u_T^b - u_gt^b||^2 over the batch (P Eq.6, l.199-222) and its
+ * gradient w.r.t. Theta_t = {lambda_t, phi_i^t, k_i^t} by the chain rule of
+ * P l.343-420: dl/du_T = u_T - u_gt (l.348-353), the prox Jacobian y (Eq.16),
+ * Eq.15's K_i^T Lambda_i Kbar_i^T with the exact transposes of the symmetric-
+ * boundary convolutions (R1 and R2), the RBF-weight and filter derivatives, and
+ * z = du/dlambda (Eq.19).  For lambda = e^beta (Eq.20) dl/dbeta = lambda dl/dlambda.
+ *   f_dev, u_gt_dev  device [B][H][ld]
+ *   grad_filters     host [T][N_k][m][m]   dl/dk_i^t
+ *   grad_rbf_w       host [T][N_k][M]      dl/dw_ij^t
+ *   grad_lambda      host [T]              dl/dlambda_t
+ *   loss             host                  the loss (double)
+ * Reaction 0 and TNRD_PHI_EXACT only (else EUNSUPPORTED).  Runs the forward pass
+ * with a tape (2T+1 images of scratch, owned by the handle), then the backward
+ * stages; all sums are fixed-order (bitwise reproducible).  Synchronous: returns
+ * after the host outputs are written. */
+TNRD_API tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f_dev, const float *u_gt_dev, int B, int H,
+                                    int W, long long ld, float *grad_filters, float *grad_rbf_w,
+                                    float *grad_lambda, double *loss, void *cuda_stream);
+
 /* ---------------- multi-GPU: row slabs of one large image ----------------
  * Rank rho of N owns rows [row0, row0 + rows) of an H_global x W image.
  * Before every stage each rank exchanges 2r = ksize-1 rows of u_t with each

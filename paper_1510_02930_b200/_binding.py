@@ -77,6 +77,7 @@ def _load() -> ctypes.CDLL:
         "tnrd_get_launch_times": ([vp, fp, i, ctypes.POINTER(i)], i),
         "tnrd_debug_phi": ([vp, i, i, vp, vp, ll, vp], i),
         "tnrd_debug_prox": ([vp, vp, f, vp, ll, vp], i),
+        "tnrd_loss_grad": ([vp, vp, vp, i, i, i, ll, fp, fp, fp, ctypes.POINTER(ctypes.c_double), vp], i),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -90,7 +91,7 @@ EXPORTED = (
     "tnrd_abi_version", "tnrd_status_string", "tnrd_create", "tnrd_set_stage_params",
     "tnrd_denoise", "tnrd_denoise_host", "tnrd_destroy", "tnrd_last_error", "tnrd_launch_count",
     "tnrd_nccl_unique_id", "tnrd_comm_init", "tnrd_denoise_slab", "tnrd_denoise_slabs_loopback",
-    "tnrd_set_profiling", "tnrd_get_launch_times", "tnrd_debug_phi", "tnrd_debug_prox",
+    "tnrd_set_profiling", "tnrd_get_launch_times", "tnrd_debug_phi", "tnrd_debug_prox", "tnrd_loss_grad",
 )
 
 
@@ -242,6 +243,24 @@ def tnrd_debug_prox(ut, f, lam: float, out, stream=None) -> None:
                                 _stream_ptr(stream)))
 
 
+def tnrd_loss_grad(h: int, f, u_gt, T: int, Nk: int, k: int, M: int, stream=None):
+    """loss = 1/2 ||u_T - u_gt||^2 and its gradient (P Eq.14-20) for f, u_gt float32
+    CUDA tensors [B][H][W] or [H][W].  Returns (loss, d_filters [T][Nk][k][k],
+    d_rbf_w [T][Nk][M], d_lambda [T]) as numpy arrays."""
+    if f.dim() == 2:
+        f, u_gt = f.unsqueeze(0), u_gt.unsqueeze(0)
+    B, H, W = f.shape
+    if f.stride(2) != 1 or u_gt.stride() != f.stride() or u_gt.shape != f.shape:
+        raise ValueError("f and u_gt must be [B][H][W] with equal strides")
+    gf = np.zeros((T, Nk, k, k), np.float32)
+    gw = np.zeros((T, Nk, M), np.float32)
+    gl = np.zeros(T, np.float32)
+    loss = ctypes.c_double(0.0)
+    _check(_lib.tnrd_loss_grad(h, _dev_ptr(f), _dev_ptr(u_gt), B, H, W, f.stride(1), _f32p(gf), _f32p(gw),
+                               _f32p(gl), ctypes.byref(loss), _stream_ptr(stream)), h)
+    return loss.value, gf, gw, gl
+
+
 # ------------------------------------------------------------------ convenience wrapper
 class TNRD:
     """A handle plus its model: TNRD(model).denoise(f) -> u (torch CUDA tensors).
@@ -272,6 +291,10 @@ class TNRD:
         u = np.empty_like(f_host)
         tnrd_denoise_host(self.h, f_host, u, peak)
         return u
+
+    def loss_grad(self, f, u_gt, stream=None):
+        """(loss, d_filters, d_rbf_w, d_lambda) of 1/2 ||u_T - u_gt||^2 (P Eq.6, 14-20)."""
+        return tnrd_loss_grad(self.h, f, u_gt, self.T, self.Nk, self.k, self.M, stream)
 
     @property
     def launches(self) -> int:

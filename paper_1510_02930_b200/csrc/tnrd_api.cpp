@@ -83,6 +83,15 @@ struct tnrd_handle {
     float *d_params = nullptr;    // [T][Nk][pstride_max]
     float4 *d_table = nullptr;    // MODE_TABLE: [T][Nk][table_stride] cubic intervals
     int table_stride = 0;
+    // raw stage parameters (training gradient, tnrd_loss_grad)
+    std::vector<float> raw_mu0, raw_step, raw_gamma;   // host [T][Nk]
+    float *d_raw = nullptr;       // device: k [T][Nk][m*m], kbar [T][Nk][m*m], w [T][Nk][M]
+    float *g_buf = nullptr;       // tape + work images
+    size_t g_buf_bytes = 0;
+    float *g_partial = nullptr;   // per-block partial sums
+    size_t g_partial_bytes = 0;
+    double *g_red = nullptr;      // reduced sums
+    size_t g_red_bytes = 0;
     float *scratch = nullptr;
     size_t scratch_bytes = 0;
     float *e2e_f = nullptr, *e2e_u = nullptr;
@@ -404,6 +413,18 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
         delete h;
         return fail(nullptr, TNRD_ENOMEM, "cudaMalloc params: %s", cudaGetErrorString(e));
     }
+    {
+        const size_t mm = (size_t)d->ksize * d->ksize;
+        e = cudaMalloc(&h->d_raw, sizeof(float) * (size_t)d->T * d->n_filters * (2 * mm + d->n_rbf));
+        if (e != cudaSuccess) {
+            cudaFree(h->d_params);
+            delete h;
+            return fail(nullptr, TNRD_ENOMEM, "cudaMalloc raw params: %s", cudaGetErrorString(e));
+        }
+        h->raw_mu0.assign((size_t)d->T * d->n_filters, 0.f);
+        h->raw_step = h->raw_mu0;
+        h->raw_gamma = h->raw_mu0;
+    }
     if (d->phi_mode == TNRD_PHI_TABLE) {
         h->table_stride = table_intervals(d->n_rbf) + 1;
         e = cudaMalloc(&h->d_table, sizeof(float4) * (size_t)d->T * d->n_filters * h->table_stride);
@@ -452,6 +473,26 @@ tnrd_status tnrd_set_stage_params(tnrd_handle *h, int t, const float *filters, c
         for (int i = 0; i < Nk; ++i) ok = ok && host[(size_t)i * ps + tnrd::tap_floats(K) + 5] != 0.f;
         if (ok) break;
         mode = tnrd::MODE_DIRECT;
+    }
+    {   // raw parameters for the training gradient: k, kbar = rot180(k), w; grid scalars on the host
+        const size_t mm = (size_t)K * K, TN = (size_t)h->d.T * Nk;
+        std::vector<float> kbar(mm * Nk);
+        for (int i = 0; i < Nk; ++i)
+            for (int a = 0; a < K; ++a)
+                for (int b = 0; b < K; ++b)
+                    kbar[i * mm + a * K + b] = filters[i * mm + (K - 1 - a) * K + (K - 1 - b)];
+        DeviceGuard g(h->d.device);
+        TNRD_CUDA(h, cudaMemcpy(h->d_raw + (size_t)t * Nk * mm, filters, sizeof(float) * mm * Nk,
+                                cudaMemcpyHostToDevice));
+        TNRD_CUDA(h, cudaMemcpy(h->d_raw + TN * mm + (size_t)t * Nk * mm, kbar.data(), sizeof(float) * mm * Nk,
+                                cudaMemcpyHostToDevice));
+        TNRD_CUDA(h, cudaMemcpy(h->d_raw + 2 * TN * mm + (size_t)t * Nk * M, rbf_w, sizeof(float) * (size_t)Nk * M,
+                                cudaMemcpyHostToDevice));
+        for (int i = 0; i < Nk; ++i) {
+            h->raw_mu0[(size_t)t * Nk + i] = rbf_mu0[i];
+            h->raw_step[(size_t)t * Nk + i] = rbf_step[i];
+            h->raw_gamma[(size_t)t * Nk + i] = rbf_gamma[i];
+        }
     }
     if (mode == tnrd::MODE_TABLE) {
         std::vector<float4> tab((size_t)Nk * h->table_stride);
@@ -543,6 +584,10 @@ tnrd_status tnrd_destroy(tnrd_handle *h) {
         cudaDeviceSynchronize();
         cudaFree(h->d_params);
         cudaFree(h->d_table);
+        cudaFree(h->d_raw);
+        cudaFree(h->g_buf);
+        cudaFree(h->g_partial);
+        cudaFree(h->g_red);
         cudaFree(h->scratch);
         cudaFree(h->e2e_f);
         cudaFree(h->e2e_u);
@@ -599,6 +644,106 @@ tnrd_status tnrd_debug_prox(const float *ut, const float *f, float lambda, float
     if (!(lambda > 0.f)) return fail(nullptr, TNRD_EINVAL, "lambda must be > 0");
     cudaError_t e = tnrd::launch_debug_prox(ut, f, lambda, out, n, reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return fail(nullptr, TNRD_ECUDA, "debug prox: %s", cudaGetErrorString(e));
+    return TNRD_OK;
+}
+
+// ------------------------------------------------------------------ training gradient
+tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, int B, int H, int W, long long ld,
+                           float *grad_filters, float *grad_rbf_w, float *grad_lambda, double *loss, void *stream) {
+    tnrd_status st = check_ready(h);
+    if (st != TNRD_OK) return st;
+    if (!f || !u_gt || !grad_filters || !grad_rbf_w || !grad_lambda || !loss)
+        return fail(h, TNRD_EINVAL, "null pointer");
+    if (h->d.reaction != TNRD_REACTION_POISSON_PROX || h->d.phi_mode != TNRD_PHI_EXACT)
+        return fail(h, TNRD_EUNSUPPORTED, "the training gradient is built for reaction 0 and exact phi");
+    if (B < 1 || H < h->d.ksize || W < h->d.ksize || ld < W) return fail(h, TNRD_EINVAL, "bad image size");
+    DeviceGuard g(h->d.device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int T = h->d.T, Nk = h->d.n_filters, K = h->d.ksize, M = h->d.n_rbf;
+    const size_t mm = (size_t)K * K, n = (size_t)B * H * W, TN = (size_t)T * Nk;
+    // tape u_0..u_T (2T+1 images incl. ut_0..ut_{T-1}) + work g, gn, e, x, w, a, b
+    const size_t imgs = 2 * (size_t)T + 1 + 7;
+    st = grow(h, &h->g_buf, &h->g_buf_bytes, sizeof(float) * n * imgs, "gradient tape");
+    if (st != TNRD_OK) return st;
+    const int grid = tnrd::grad_grid((long long)n, h->num_sms);
+    st = grow(h, &h->g_partial, &h->g_partial_bytes, sizeof(float) * (size_t)grid * std::max<size_t>(mm, 32), "partials");
+    if (st != TNRD_OK) return st;
+    const size_t per_f = 2 * mm + M, nred = TN * per_f + T + 1;
+    {
+        float *tmp = reinterpret_cast<float *>(h->g_red);
+        size_t have = h->g_red_bytes;
+        st = grow(h, &tmp, &have, sizeof(double) * nred, "reductions");
+        if (st != TNRD_OK) return st;
+        h->g_red = reinterpret_cast<double *>(tmp);
+        h->g_red_bytes = have;
+    }
+    float *tape_u = h->g_buf;                       // [T+1][n]
+    float *tape_ut = tape_u + (size_t)(T + 1) * n;  // [T][n]
+    float *wk = tape_ut + (size_t)T * n;
+    float *gb = wk, *gn = wk + n, *e = wk + 2 * n, *x = wk + 3 * n, *wv = wk + 4 * n, *av = wk + 5 * n, *bv = wk + 6 * n;
+    double *red_f = h->g_red, *red_lam = h->g_red + TN * per_f, *red_loss = red_lam + T;
+    float *part = h->g_partial;
+#define TNRD_K(call) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) return cuda_fail(h, e_, #call); } while (0)
+    // ---- forward with tape (the fused stage kernel also writes ut)
+    TNRD_K(cudaMemcpy2DAsync(tape_u, sizeof(float) * W, f, sizeof(float) * ld, sizeof(float) * W, (size_t)B * H,
+                             cudaMemcpyDeviceToDevice, s));
+    const int tile = h->allow_large_tile ? tnrd::choose_tile(K, B, H, W, h->num_sms) : 1;
+    for (int t = 0; t < T; ++t) {
+        StageArgs a{};
+        a.u_in = {tape_u + (size_t)t * n, W, (long long)H * W, 0};
+        a.f = {f, ld, (long long)H * ld, 0};
+        a.u_out = tape_u + (size_t)(t + 1) * n; a.out_ld = W; a.out_img_stride = (long long)H * W; a.out_row_base = 0;
+        a.ut_out = tape_ut + (size_t)t * n;
+        a.H = H; a.W = W; a.y_begin = 0; a.y_end = H; a.avail_lo = 0; a.avail_hi = H;
+        st = launch_one(h, t, tile, a, B, s);
+        if (st != TNRD_OK) return st;
+    }
+    TNRD_K(tnrd::grad_loss(tape_u + (size_t)T * n, u_gt, ld, B, H, W, gb, part, grid, s));
+    TNRD_K(tnrd::grad_reduce(part, grid, 1, 1, red_loss, s));
+    // ---- backward, P Eq.14-20
+    const float *raw_k = h->d_raw, *raw_kbar = h->d_raw + TN * mm, *raw_w = h->d_raw + 2 * TN * mm;
+    for (int t = T - 1; t >= 0; --t) {
+        const float *ut = tape_u + (size_t)t * n;
+        TNRD_K(tnrd::grad_bw_prox(tape_ut + (size_t)t * n, f, ld, B, H, W, h->lambda[t], gb, e, gn, part, grid, s));
+        TNRD_K(tnrd::grad_reduce(part, grid, 1, 1, red_lam + t, s));
+        for (int i = 0; i < Nk; ++i) {
+            const size_t fi = (size_t)t * Nk + i;
+            const float *k = raw_k + fi * mm, *kbar = raw_kbar + fi * mm, *rw = raw_w + fi * M;
+            double *rf = red_f + fi * per_f;  // [inner mm][outer mm][w M]
+            TNRD_K(tnrd::grad_conv_sym(ut, k, K, B, H, W, x, grid, s));                  // x = k_i * u_t
+            if (h->d.boundary == 1) TNRD_K(tnrd::grad_conv_sym(e, k, K, B, H, W, av, grid, s));       // (K^T)^T e
+            else TNRD_K(tnrd::grad_conv_adjoint(e, kbar, K, B, H, W, av, 0, grid, s));                // Kbar^T e
+            for (int j0 = 0; j0 < M; j0 += 32) {
+                TNRD_K(tnrd::grad_phi_point(x, av, (long long)n, rw, M, h->raw_mu0[fi], h->raw_step[fi],
+                                            h->raw_gamma[fi], j0, wv, bv, part, grid, s));
+                TNRD_K(tnrd::grad_reduce(part, grid, 32, std::min(32, M - j0), rf + 2 * mm + j0, s));
+            }
+            TNRD_K(tnrd::grad_conv_adjoint(bv, k, K, B, H, W, gn, 1, grid, s));          // gn -= K_i^T b
+            TNRD_K(tnrd::grad_kernel(ut, bv, K, B, H, W, part, grid, s));                 // inner
+            TNRD_K(tnrd::grad_reduce(part, grid, (int)mm, (int)mm, rf, s));
+            if (h->d.boundary == 1) TNRD_K(tnrd::grad_kernel(e, wv, K, B, H, W, part, grid, s));
+            else TNRD_K(tnrd::grad_kernel(wv, e, K, B, H, W, part, grid, s));
+            TNRD_K(tnrd::grad_reduce(part, grid, (int)mm, (int)mm, rf + mm, s));
+        }
+        std::swap(gb, gn);
+    }
+#undef TNRD_K
+    std::vector<double> red(nred);
+    TNRD_CUDA(h, cudaMemcpyAsync(red.data(), h->g_red, sizeof(double) * nred, cudaMemcpyDeviceToHost, s));
+    TNRD_CUDA(h, cudaStreamSynchronize(s));
+    for (size_t fi = 0; fi < TN; ++fi) {
+        const double *rf = red.data() + fi * per_f;
+        float *gk = grad_filters + fi * mm;
+        for (int a = 0; a < K; ++a)
+            for (int b = 0; b < K; ++b) {
+                // d l / d k = -(inner) - (outer): R1's outer kernel is kbar, so its taps map back by rot180
+                const double outer = h->d.boundary == 1 ? rf[mm + a * K + b] : rf[mm + (K - 1 - a) * K + (K - 1 - b)];
+                gk[a * K + b] = (float)(-(rf[a * K + b] + outer));
+            }
+        for (int j = 0; j < M; ++j) grad_rbf_w[fi * M + j] = (float)rf[2 * mm + j];
+    }
+    for (int t = 0; t < T; ++t) grad_lambda[t] = (float)red[TN * per_f + t];
+    *loss = red[TN * per_f + T];
     return TNRD_OK;
 }
 

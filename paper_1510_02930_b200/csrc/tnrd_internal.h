@@ -69,6 +69,7 @@ struct StageArgs {
     Image u_in;            // u_t  (rows [avail_lo, avail_hi) addressable)
     Image f;               // f    (rows [y_begin, y_end) addressable)
     float *u_out;          // u_{t+1}, addressed like out_* below
+    float *ut_out;         // optional (training tape): ut = u - d, addressed like u_out
     long long out_ld;
     long long out_img_stride;
     int out_row_base;
@@ -95,5 +96,22 @@ cudaError_t launch_debug_prox(const float *ut, const float *f, float lambda, flo
                               long long n, cudaStream_t s);
 cudaError_t launch_copy_rows(const float *src, long long src_ld, float *dst, long long dst_ld,
                              int rows, int W, cudaStream_t s);
+
+// Training-gradient kernels (tnrd_grad.cu); all images dense [B][H][W] unless an ld is given.
+int grad_grid(long long n, int num_sms);
+cudaError_t grad_loss(const float *uT, const float *gt, long long gt_ld, int B, int H, int W, float *g,
+                      float *partial, int grid, cudaStream_t s);
+cudaError_t grad_bw_prox(const float *ut, const float *f, long long f_ld, int B, int H, int W, float lam,
+                         const float *g, float *e, float *gn, float *partial, int grid, cudaStream_t s);
+cudaError_t grad_conv_sym(const float *x, const float *k, int m, int B, int H, int W, float *out, int grid,
+                          cudaStream_t s);
+cudaError_t grad_conv_adjoint(const float *y, const float *k, int m, int B, int H, int W, float *out, int mode,
+                              int grid, cudaStream_t s);
+cudaError_t grad_phi_point(const float *x, const float *a, long long n, const float *rw, int M, float mu0,
+                           float step, float gamma, int j0, float *wout, float *bout, float *partial, int grid,
+                           cudaStream_t s);
+cudaError_t grad_kernel(const float *x, const float *e, int m, int B, int H, int W, float *partial, int grid,
+                        cudaStream_t s);
+cudaError_t grad_reduce(const float *partial, int nblk, int stride, int np, double *out, cudaStream_t s);
 
 }  // namespace tnrd

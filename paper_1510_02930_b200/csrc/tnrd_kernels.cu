@@ -687,7 +687,9 @@ __global__ void __launch_bounds__(32 * (C::XW + C::YW), C::MINB) stage_kernel(co
                 const float u = h ? hi(u2) : lo(u2);
                 const float d = h ? hi(acc[ry][e]) : lo(acc[ry][e]);
                 const float fv = __ldg(fb + (long long)(oy - a.f.row_base) * a.f.ld + ox);
-                ob[(long long)(oy - a.out_row_base) * a.out_ld + ox] = reaction_step(a.reaction, u, u - d, a.lambda, fv);
+                const long long oi = (long long)(oy - a.out_row_base) * a.out_ld + ox;
+                ob[oi] = reaction_step(a.reaction, u, u - d, a.lambda, fv);
+                if (a.ut_out) a.ut_out[(long long)g.b * a.out_img_stride + oi] = u - d;
             }
         }
     }
