@@ -67,6 +67,10 @@ def lib() -> ctypes.CDLL:
             L.oracle_loss_grad.argtypes = [i, i, dp, dp, i, i, i, i, dp, dp, dp, dp, dp, dp, i, dp, dp, dp]
             L.oracle_loss_grad.restype = ctypes.c_double
             L.oracle_kernel_grad.argtypes = [i, i, dp, dp, i, dp]
+            L.oracle_sample_poisson.argtypes = [i, i, i, dp, ctypes.c_uint64, dp]
+            L.oracle_philox4x32.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint32)]
+            L.oracle_exp_fixed.argtypes = [ctypes.c_double]
+            L.oracle_exp_fixed.restype = ctypes.c_double
             L.oracle_reaction.argtypes = [ctypes.c_double] * 4 + [i]
             L.oracle_reaction.restype = ctypes.c_double
             _lib = L
@@ -194,6 +198,28 @@ def denoise_window(f, model, y0: int, y1: int, x0: int, x1: int,
     cx0, cx1 = max(0, x0 - R), min(W, x1 + R)
     u = denoise(f[cy0:cy1, cx0:cx1], model, boundary, reaction=reaction)
     return u[y0 - cy0:y1 - cy0, x0 - cx0:x1 - cx0]
+
+
+def sample_poisson(u, seed: int) -> np.ndarray:
+    """f ~ Poisson(u) per pixel (P Eq.1) with the shared counter-based generator
+    (Philox4x32-10, counter = flat pixel index of the [B][H][W] array)."""
+    u = _d(u)
+    shp = u.shape
+    u3 = u.reshape((-1,) + shp[-2:]) if u.ndim >= 2 else u.reshape(1, 1, -1)
+    out = np.empty_like(u3)
+    lib().oracle_sample_poisson(u3.shape[0], u3.shape[1], u3.shape[2], _p(np.ascontiguousarray(u3)),
+                                ctypes.c_uint64(seed), _p(out))
+    return out.reshape(shp)
+
+
+def philox4x32(counter: int, seed: int) -> np.ndarray:
+    out = (ctypes.c_uint32 * 4)()
+    lib().oracle_philox4x32(ctypes.c_uint64(counter), ctypes.c_uint64(seed), out)
+    return np.array(list(out), dtype=np.uint32)
+
+
+def exp_fixed(x: float) -> float:
+    return lib().oracle_exp_fixed(float(x))
 
 
 def psnr(u, clean, peak: float) -> float:

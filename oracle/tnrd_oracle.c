@@ -292,3 +292,67 @@ EXPORT double oracle_loss_grad(int H, int W, const double *f, const double *u_gt
     free(tmp); free(kbar); free(kg); free(G);
     return loss;
 }
+
+/* ------------------------------------------------------------------ data generation
+ * Poisson sampling (P Eq.1, l.103-111: f_i ~ Poisson(u_i), u_i = 0 gives f_i = 0)
+ * with a counter-based generator both sides implement: Philox4x32-10 (Salmon et al.,
+ * SC'11) keyed by the 64-bit seed, counter = (pixel index, 0, 0, 0); the uniform
+ * U = (w0 * 2^21 + (w1 >> 11)) * 2^-53 in [0,1); inversion by sequential search of
+ * the Poisson CDF in double: k = 0, p = exp(-u), F = p; while U >= F: k += 1,
+ * p *= u / k, F += p (capped at u + 40 sqrt(u) + 40).  exp is a fixed fma-only
+ * routine (2^k * Horner polynomial), so the integer decision is taken in the same
+ * precision with the same operations on both sides. */
+#include <stdint.h>
+
+static void philox_round(uint32_t c[4], const uint32_t k[2]) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0, hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c[1] ^ k[0], n1 = lo1, n2 = hi0 ^ c[3] ^ k[1], n3 = lo0;
+    c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+}
+
+EXPORT void oracle_philox4x32(uint64_t counter, uint64_t seed, uint32_t out[4]) {
+    uint32_t c[4] = {(uint32_t)counter, (uint32_t)(counter >> 32), 0u, 0u};
+    uint32_t k[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    for (int r = 0; r < 10; ++r) {
+        philox_round(c, k);
+        k[0] += 0x9E3779B9u;
+        k[1] += 0xBB67AE85u;
+    }
+    out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[3] = c[3];
+}
+
+/* exp(x) for x in [-745, 0]: x = n ln2 + r (Cody-Waite, hi/lo ln2), exp(r) by a
+ * degree-13 Taylor Horner in fma, times 2^n.  Only IEEE fma / mul / add. */
+EXPORT double oracle_exp_fixed(double x) {
+    if (x < -745.0) return 0.0;
+    const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+    const double n = nearbyint(x * 1.44269504088896338700e+00);
+    const double r = fma(-n, ln2_lo, fma(-n, ln2_hi, x));
+    double p = 1.0 / 6227020800.0;  /* 1/13! */
+    const double inv[13] = {1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0, 1.0 / 40320.0,
+                            1.0 / 5040.0, 1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5, 1.0, 1.0};
+    for (int i = 0; i < 13; ++i) p = fma(p, r, inv[i]);
+    return ldexp(p, (int)n);
+}
+
+EXPORT double oracle_poisson_draw(double u, uint64_t counter, uint64_t seed) {
+    if (!(u > 0.0)) return 0.0;
+    uint32_t w[4];
+    oracle_philox4x32(counter, seed, w);
+    const double U = ((double)w[0] * 2097152.0 + (double)(w[1] >> 11)) * (1.0 / 9007199254740992.0);
+    double p = oracle_exp_fixed(-u), F = p, k = 0.0;
+    const double kmax = floor(u + 40.0 * sqrt(u) + 40.0);
+    while (U >= F && k < kmax) {
+        k += 1.0;
+        p *= u / k;
+        F += p;
+    }
+    return k;
+}
+
+/* f[b][y][x] = Poisson(u[b][y][x]), counter = (b*H + y)*W + x. */
+EXPORT void oracle_sample_poisson(int B, int H, int W, const double *u, uint64_t seed, double *f) {
+#pragma omp parallel for schedule(static)
+    for (long i = 0; i < (long)B * H * W; ++i) f[i] = oracle_poisson_draw(u[i], (uint64_t)i, seed);
+}

@@ -481,3 +481,48 @@ def test_kernel_grad_is_the_derivative_of_the_convolution():
             k = np.zeros((m, m))
             k[a, b] = 1.0
             assert abs(out[a, b] - float(np.sum(e * oracle.conv2d_sym(x, k)))) < 1e-12
+
+
+# ---------------------------------------------------------------- data generation
+def test_philox_known_answer():
+    words = None
+    with open(os.path.join(GOLD, "philox4x32_10_kat.txt")) as fh:
+        for line in fh:
+            if line.strip() and not line.startswith("#"):
+                words = [int(x, 16) for x in line.split()]
+    assert list(oracle.philox4x32(0, 0)) == words
+
+
+def test_exp_fixed_matches_libm():
+    import math
+    xs = np.concatenate([np.linspace(-745, 0, 20001), -np.logspace(-12, 2.8, 2001), [0.0, -1e-300]])
+    for x in xs:
+        ref = math.exp(x)
+        got = oracle.exp_fixed(x)
+        assert abs(got - ref) <= 4e-16 * ref + 1e-320, (x, got, ref)
+
+
+@pytest.mark.parametrize("mean", [0.5, 1.0, 4.0, 20.0, 40.0])
+def test_poisson_sampler_moments(mean):
+    """Mean and variance both equal u (Poisson property; S l.402), within 4 sigma of
+    their sampling errors over 2e5 draws."""
+    n = 200_000
+    f = oracle.sample_poisson(np.full((1, 200, 1000), mean), seed=1234 + int(mean * 10))
+    assert np.all(f == np.round(f)) and f.min() >= 0
+    m, v = f.mean(), f.var()
+    assert abs(m - mean) < 4 * np.sqrt(mean / n)
+    assert abs(v - mean) < 4 * np.sqrt((2 * mean * mean + mean) / n)
+
+
+def test_poisson_sampler_zero_mean_determinism_and_pmf():
+    u = np.zeros((2, 5, 7))
+    assert np.all(oracle.sample_poisson(u, 3) == 0)  # Eq.1 delta_0 branch
+    u = np.full((1, 300, 300), 2.5)
+    a, b = oracle.sample_poisson(u, 9), oracle.sample_poisson(u, 9)
+    assert np.array_equal(a, b) and not np.array_equal(a, oracle.sample_poisson(u, 10))
+    # empirical pmf against the Poisson pmf (scipy) at k = 0..8
+    import scipy.stats
+    n = a.size
+    for k in range(9):
+        p = scipy.stats.poisson.pmf(k, 2.5)
+        assert abs(np.mean(a == k) - p) < 5 * np.sqrt(p * (1 - p) / n)
