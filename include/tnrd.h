@@ -176,6 +176,24 @@ TNRD_API tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f_dev, const fl
                                     int W, long long ld, float *grad_filters, float *grad_rbf_w,
                                     float *grad_lambda, double *loss, void *cuda_stream);
 
+/* ---------------- steps either side of the path ----------------
+ * Poisson noise (P Eq.1, l.103-111): f_dev[b][y][x] ~ Poisson(u_dev[b][y][x]) as
+ * exact integer-valued fp32 counts; u = 0 gives 0.  Counter-based and reproducible:
+ * Philox4x32-10 keyed by `seed`, counter = (b*H + y)*W + x, one 53-bit uniform per
+ * pixel, exact inversion of the Poisson CDF in double with a fixed fma-only exp --
+ * the same draw as the oracle's oracle_sample_poisson, bit for bit.
+ *   u_dev, f_dev  device [B][H][ld] (may alias)
+ * EINVAL if any mean is negative or NaN (checked on the device; synchronous). */
+TNRD_API tnrd_status tnrd_sample_poisson(const float *u_dev, float *f_dev, int B, int H, int W, long long ld,
+                                         unsigned long long seed, void *cuda_stream);
+
+/* PSNR per image (reading C15: 10 log10(peak_b^2 / MSE(u_b, clean_b)), unclamped;
+ * +inf for equal images): u_dev, clean_dev device [B][H][ld]; peak host [B];
+ * psnr_out host [B].  Squared errors summed in double in a fixed order.
+ * Synchronous. */
+TNRD_API tnrd_status tnrd_psnr(const float *u_dev, const float *clean_dev, int B, int H, int W, long long ld,
+                               const float *peak, double *psnr_out, void *cuda_stream);
+
 /* ---------------- multi-GPU: row slabs of one large image ----------------
  * Rank rho of N owns rows [row0, row0 + rows) of an H_global x W image.
  * Before every stage each rank exchanges 2r = ksize-1 rows of u_t with each

@@ -78,6 +78,8 @@ def _load() -> ctypes.CDLL:
         "tnrd_debug_phi": ([vp, i, i, vp, vp, ll, vp], i),
         "tnrd_debug_prox": ([vp, vp, f, vp, ll, vp], i),
         "tnrd_loss_grad": ([vp, vp, vp, i, i, i, ll, fp, fp, fp, ctypes.POINTER(ctypes.c_double), vp], i),
+        "tnrd_sample_poisson": ([vp, vp, i, i, i, ll, ctypes.c_ulonglong, vp], i),
+        "tnrd_psnr": ([vp, vp, i, i, i, ll, fp, ctypes.POINTER(ctypes.c_double), vp], i),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -92,6 +94,7 @@ EXPORTED = (
     "tnrd_denoise", "tnrd_denoise_host", "tnrd_destroy", "tnrd_last_error", "tnrd_launch_count",
     "tnrd_nccl_unique_id", "tnrd_comm_init", "tnrd_denoise_slab", "tnrd_denoise_slabs_loopback",
     "tnrd_set_profiling", "tnrd_get_launch_times", "tnrd_debug_phi", "tnrd_debug_prox", "tnrd_loss_grad",
+    "tnrd_sample_poisson", "tnrd_psnr",
 )
 
 
@@ -259,6 +262,31 @@ def tnrd_loss_grad(h: int, f, u_gt, T: int, Nk: int, k: int, M: int, stream=None
     _check(_lib.tnrd_loss_grad(h, _dev_ptr(f), _dev_ptr(u_gt), B, H, W, f.stride(1), _f32p(gf), _f32p(gw),
                                _f32p(gl), ctypes.byref(loss), _stream_ptr(stream)), h)
     return loss.value, gf, gw, gl
+
+
+def tnrd_sample_poisson(u, f=None, seed: int = 0, stream=None):
+    """f ~ Poisson(u) (P Eq.1), float32 CUDA tensors [B][H][W] or [H][W]; returns f."""
+    import torch
+    if f is None:
+        f = torch.empty_like(u)
+    u3, f3 = (u, f) if u.dim() == 3 else (u.unsqueeze(0), f.unsqueeze(0))
+    B, H, W = u3.shape
+    if u3.stride(2) != 1 or f3.stride() != u3.stride():
+        raise ValueError("u and f must have unit column stride and equal strides")
+    _check(_lib.tnrd_sample_poisson(_dev_ptr(u3), _dev_ptr(f3), B, H, W, u3.stride(1), int(seed),
+                                    _stream_ptr(stream)))
+    return f
+
+
+def tnrd_psnr(u, clean, peak, stream=None) -> np.ndarray:
+    """PSNR per image, 10 log10(peak^2 / MSE) (reading C15)."""
+    u3, c3 = (u, clean) if u.dim() == 3 else (u.unsqueeze(0), clean.unsqueeze(0))
+    B, H, W = u3.shape
+    pk = _host_f32(np.broadcast_to(np.asarray(peak, np.float32), (B,)))
+    out = np.zeros(B, np.float64)
+    _check(_lib.tnrd_psnr(_dev_ptr(u3), _dev_ptr(c3), B, H, W, u3.stride(1), _f32p(pk),
+                          out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream_ptr(stream)))
+    return out
 
 
 # ------------------------------------------------------------------ convenience wrapper

@@ -747,6 +747,56 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
     return TNRD_OK;
 }
 
+// ------------------------------------------------------------------ data generation / evaluation
+tnrd_status tnrd_sample_poisson(const float *u, float *f, int B, int H, int W, long long ld, unsigned long long seed,
+                                void *stream) {
+    if (!u || !f) return fail(nullptr, TNRD_EINVAL, "null pointer");
+    if (B < 1 || H < 1 || W < 1 || ld < W) return fail(nullptr, TNRD_EINVAL, "bad size");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int *bad = nullptr;
+    cudaError_t e = cudaMallocAsync(&bad, sizeof(int), s);
+    if (e != cudaSuccess) return fail(nullptr, TNRD_ENOMEM, "cudaMallocAsync: %s", cudaGetErrorString(e));
+    int hbad = 0;
+    e = cudaMemsetAsync(bad, 0, sizeof(int), s);
+    if (e == cudaSuccess) e = tnrd::data_sample_poisson(u, f, B, H, W, ld, seed, bad, sms, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(bad, s);
+    if (e != cudaSuccess) return fail(nullptr, TNRD_ECUDA, "sample_poisson: %s", cudaGetErrorString(e));
+    if (hbad) return fail(nullptr, TNRD_EINVAL, "negative or NaN Poisson mean");
+    return TNRD_OK;
+}
+
+tnrd_status tnrd_psnr(const float *u, const float *c, int B, int H, int W, long long ld, const float *peak,
+                      double *out, void *stream) {
+    if (!u || !c || !peak || !out) return fail(nullptr, TNRD_EINVAL, "null pointer");
+    if (B < 1 || H < 1 || W < 1 || ld < W) return fail(nullptr, TNRD_EINVAL, "bad size");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int nb = tnrd::data_sq_err_blocks((long long)H * W, sms);
+    double *part = nullptr;
+    cudaError_t e = cudaMallocAsync(&part, sizeof(double) * (size_t)B * nb, s);
+    if (e != cudaSuccess) return fail(nullptr, TNRD_ENOMEM, "cudaMallocAsync: %s", cudaGetErrorString(e));
+    std::vector<double> hp((size_t)B * nb);
+    e = tnrd::data_sq_err(u, c, B, H, W, ld, part, nb, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hp.data(), part, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(part, s);
+    if (e != cudaSuccess) return fail(nullptr, TNRD_ECUDA, "psnr: %s", cudaGetErrorString(e));
+    for (int b = 0; b < B; ++b) {
+        double sse = 0.0;
+        for (int j = 0; j < nb; ++j) sse += hp[(size_t)b * nb + j];
+        const double mse = sse / ((double)H * W);
+        out[b] = mse > 0.0 ? 10.0 * std::log10((double)peak[b] * peak[b] / mse) : INFINITY;
+    }
+    return TNRD_OK;
+}
+
 // ------------------------------------------------------------------ slabs
 tnrd_status tnrd_nccl_unique_id(void *id128) {
     if (!id128) return fail(nullptr, TNRD_EINVAL, "null id");

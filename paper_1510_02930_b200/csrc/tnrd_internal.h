@@ -114,4 +114,11 @@ cudaError_t grad_kernel(const float *x, const float *e, int m, int B, int H, int
                         cudaStream_t s);
 cudaError_t grad_reduce(const float *partial, int nblk, int stride, int np, double *out, cudaStream_t s);
 
+// Data generation and evaluation (tnrd_data.cu).
+cudaError_t data_sample_poisson(const float *u, float *f, int B, int H, int W, long long ld, uint64_t seed,
+                                int *bad, int num_sms, cudaStream_t s);
+int data_sq_err_blocks(long long per_image, int num_sms);
+cudaError_t data_sq_err(const float *u, const float *c, int B, int H, int W, long long ld, double *partial,
+                        int blocks, cudaStream_t s);
+
 }  // namespace tnrd
