@@ -415,7 +415,7 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
     }
     {
         const size_t mm = (size_t)d->ksize * d->ksize;
-        e = cudaMalloc(&h->d_raw, sizeof(float) * (size_t)d->T * d->n_filters * (2 * mm + d->n_rbf));
+        e = cudaMalloc(&h->d_raw, sizeof(float) * (size_t)d->T * d->n_filters * (2 * mm + d->n_rbf + 3));
         if (e != cudaSuccess) {
             cudaFree(h->d_params);
             delete h;
@@ -488,11 +488,15 @@ tnrd_status tnrd_set_stage_params(tnrd_handle *h, int t, const float *filters, c
                                 cudaMemcpyHostToDevice));
         TNRD_CUDA(h, cudaMemcpy(h->d_raw + 2 * TN * mm + (size_t)t * Nk * M, rbf_w, sizeof(float) * (size_t)Nk * M,
                                 cudaMemcpyHostToDevice));
+        std::vector<float> g3((size_t)Nk * 3);
         for (int i = 0; i < Nk; ++i) {
             h->raw_mu0[(size_t)t * Nk + i] = rbf_mu0[i];
             h->raw_step[(size_t)t * Nk + i] = rbf_step[i];
             h->raw_gamma[(size_t)t * Nk + i] = rbf_gamma[i];
+            g3[3 * i] = rbf_mu0[i]; g3[3 * i + 1] = rbf_step[i]; g3[3 * i + 2] = rbf_gamma[i];
         }
+        TNRD_CUDA(h, cudaMemcpy(h->d_raw + 2 * TN * mm + TN * M + (size_t)t * Nk * 3, g3.data(),
+                                sizeof(float) * 3 * Nk, cudaMemcpyHostToDevice));
     }
     if (mode == tnrd::MODE_TABLE) {
         std::vector<float4> tab((size_t)Nk * h->table_stride);
@@ -661,12 +665,17 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int T = h->d.T, Nk = h->d.n_filters, K = h->d.ksize, M = h->d.n_rbf;
     const size_t mm = (size_t)K * K, n = (size_t)B * H * W, TN = (size_t)T * Nk;
-    // tape u_0..u_T (2T+1 images incl. ut_0..ut_{T-1}) + work g, gn, e, x, w, a, b
-    const size_t imgs = 2 * (size_t)T + 1 + 7;
+    if (M > 64) return fail(h, TNRD_EUNSUPPORTED, "training gradient built for n_rbf <= 64");
+    // filters per backward chunk: 5 per-filter images (x, a, b, w, t) within ~1 GB
+    const int F = (int)std::max<size_t>(1, std::min<size_t>((size_t)Nk, ((size_t)1 << 30) / (5 * n * sizeof(float))));
+    // tape u_0..u_T and ut_0..ut_{T-1} (2T+1 images) + g, gn, e + the chunk images
+    const size_t imgs = 2 * (size_t)T + 1 + 3 + 5 * (size_t)F;
     st = grow(h, &h->g_buf, &h->g_buf_bytes, sizeof(float) * n * imgs, "gradient tape");
     if (st != TNRD_OK) return st;
     const int grid = tnrd::grad_grid((long long)n, h->num_sms);
-    st = grow(h, &h->g_partial, &h->g_partial_bytes, sizeof(float) * (size_t)grid * std::max<size_t>(mm, 32), "partials");
+    const int gx = tnrd::grad_chunk_grid((long long)n, F, h->num_sms);
+    const size_t part_floats = std::max((size_t)grid, (size_t)F * gx * std::max<size_t>(64, 2 * mm));
+    st = grow(h, &h->g_partial, &h->g_partial_bytes, sizeof(float) * part_floats, "partials");
     if (st != TNRD_OK) return st;
     const size_t per_f = 2 * mm + M, nred = TN * per_f + T + 1;
     {
@@ -680,7 +689,9 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
     float *tape_u = h->g_buf;                       // [T+1][n]
     float *tape_ut = tape_u + (size_t)(T + 1) * n;  // [T][n]
     float *wk = tape_ut + (size_t)T * n;
-    float *gb = wk, *gn = wk + n, *e = wk + 2 * n, *x = wk + 3 * n, *wv = wk + 4 * n, *av = wk + 5 * n, *bv = wk + 6 * n;
+    float *gb = wk, *gn = wk + n, *e = wk + 2 * n;
+    float *cx = wk + 3 * n, *ca = cx + (size_t)F * n, *cb = ca + (size_t)F * n, *cw = cb + (size_t)F * n,
+          *ct = cw + (size_t)F * n;
     double *red_f = h->g_red, *red_lam = h->g_red + TN * per_f, *red_loss = red_lam + T;
     float *part = h->g_partial;
 #define TNRD_K(call) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) return cuda_fail(h, e_, #call); } while (0)
@@ -700,30 +711,21 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
     }
     TNRD_K(tnrd::grad_loss(tape_u + (size_t)T * n, u_gt, ld, B, H, W, gb, part, grid, s));
     TNRD_K(tnrd::grad_reduce(part, grid, 1, 1, red_loss, s));
-    // ---- backward, P Eq.14-20
+    // ---- backward, P Eq.14-20: per stage the prox backward, then chunks of F filters
     const float *raw_k = h->d_raw, *raw_kbar = h->d_raw + TN * mm, *raw_w = h->d_raw + 2 * TN * mm;
+    const float *raw_g3 = raw_w + TN * M;
     for (int t = T - 1; t >= 0; --t) {
-        const float *ut = tape_u + (size_t)t * n;
         TNRD_K(tnrd::grad_bw_prox(tape_ut + (size_t)t * n, f, ld, B, H, W, h->lambda[t], gb, e, gn, part, grid, s));
         TNRD_K(tnrd::grad_reduce(part, grid, 1, 1, red_lam + t, s));
-        for (int i = 0; i < Nk; ++i) {
-            const size_t fi = (size_t)t * Nk + i;
-            const float *k = raw_k + fi * mm, *kbar = raw_kbar + fi * mm, *rw = raw_w + fi * M;
-            double *rf = red_f + fi * per_f;  // [inner mm][outer mm][w M]
-            TNRD_K(tnrd::grad_conv_sym(ut, k, K, B, H, W, x, grid, s));                  // x = k_i * u_t
-            if (h->d.boundary == 1) TNRD_K(tnrd::grad_conv_sym(e, k, K, B, H, W, av, grid, s));       // (K^T)^T e
-            else TNRD_K(tnrd::grad_conv_adjoint(e, kbar, K, B, H, W, av, 0, grid, s));                // Kbar^T e
-            for (int j0 = 0; j0 < M; j0 += 32) {
-                TNRD_K(tnrd::grad_phi_point(x, av, (long long)n, rw, M, h->raw_mu0[fi], h->raw_step[fi],
-                                            h->raw_gamma[fi], j0, wv, bv, part, grid, s));
-                TNRD_K(tnrd::grad_reduce(part, grid, 32, std::min(32, M - j0), rf + 2 * mm + j0, s));
-            }
-            TNRD_K(tnrd::grad_conv_adjoint(bv, k, K, B, H, W, gn, 1, grid, s));          // gn -= K_i^T b
-            TNRD_K(tnrd::grad_kernel(ut, bv, K, B, H, W, part, grid, s));                 // inner
-            TNRD_K(tnrd::grad_reduce(part, grid, (int)mm, (int)mm, rf, s));
-            if (h->d.boundary == 1) TNRD_K(tnrd::grad_kernel(e, wv, K, B, H, W, part, grid, s));
-            else TNRD_K(tnrd::grad_kernel(wv, e, K, B, H, W, part, grid, s));
-            TNRD_K(tnrd::grad_reduce(part, grid, (int)mm, (int)mm, rf + mm, s));
+        for (int i0 = 0; i0 < Nk; i0 += F) {
+            tnrd::GradChunk c{};
+            c.k = raw_k; c.kbar = raw_kbar; c.rw = raw_w; c.grid3 = raw_g3;
+            c.fi0 = t * Nk + i0; c.F = std::min(F, Nk - i0);
+            c.m = K; c.M = M; c.B = B; c.H = H; c.W = W; c.boundary = h->d.boundary; c.gx = gx;
+            c.u = tape_u + (size_t)t * n; c.e = e;
+            c.gn = gn; c.x = cx; c.a = ca; c.b = cb; c.w = cw; c.t = ct; c.partial = part;
+            c.red = red_f + (size_t)(t * Nk + i0) * per_f; c.red_stride = (int)per_f;
+            TNRD_K(tnrd::grad_chunk(c, s));
         }
         std::swap(gb, gn);
     }

@@ -97,118 +97,214 @@ __global__ void __launch_bounds__(kGradThreads) bw_prox_kernel(const float *__re
     block_sum<1>(v, partial + blockIdx.x);
 }
 
-// out = conv2d_sym(x, k): out(p) = sum_{a,b} k[a][b] x(mirror(p - (a - r, b - r))).
-__global__ void __launch_bounds__(kGradThreads) conv_sym_kernel(const float *__restrict__ x, const float *__restrict__ k,
-                                                                int m, int B, int H, int W, float *__restrict__ out) {
-    const long long n = (long long)B * H * W;
-    const int r = m / 2;
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
-        const long long b = p / ((long long)H * W), rr = p - b * H * W;
-        const int y = (int)(rr / W), xq = (int)(rr - (long long)y * W);
-        const float *xb = x + b * H * W;
-        float s = 0.0f;
+// ---- filter-batched backward kernels: blockIdx.y = filter f of the chunk [i0, i0 + F)
+// of stage t; per-filter parameters at raw + (t*Nk + i0 + f) * stride.
+
+struct GradFilterArgs {
+    const float *k, *kbar, *rw, *grid3;  // [T*Nk][m*m], [T*Nk][m*m], [T*Nk][M], [T*Nk][3] (mu0, step, gamma)
+    int fi0;                             // t*Nk + i0
+    int m, M, B, H, W;
+    long long n;                         // B*H*W
+};
+
+// conv2d_sym at pixel (y, x) of image xb (dense H x W): sum_{a,c} k[a][c] E(x)(y-(a-r), x-(c-r)).
+template <int m>
+__device__ __forceinline__ float conv_at(const float *__restrict__ xb, const float *__restrict__ k, int y, int x,
+                                         int H, int W, bool interior) {
+    constexpr int r = m / 2;
+    float s = 0.0f;
+    if (interior) {
+#pragma unroll
+        for (int a = 0; a < m; ++a) {
+            const float *row = xb + (long long)(y - (a - r)) * W + x + r;
+#pragma unroll
+            for (int c = 0; c < m; ++c) s = fmaf(k[a * m + c], row[-c], s);
+        }
+    } else {
+#pragma unroll
         for (int a = 0; a < m; ++a) {
             const float *row = xb + (long long)mirror(y - (a - r), H) * W;
-            for (int c = 0; c < m; ++c) s = fmaf(k[a * m + c], row[mirror(xq - (c - r), W)], s);
+#pragma unroll
+            for (int c = 0; c < m; ++c) s = fmaf(k[a * m + c], row[mirror(x - (c - r), W)], s);
         }
-        out[p] = s;
     }
+    return s;
 }
 
-// Exact transpose of conv2d_sym: out(q) = sum_p y(p) sum_{taps} k[tap] [mirror(p - tap) == q],
-// gathered per output: along each axis the sources are q + d, d - 1 - q and 2n - 1 - q + d.
-// mode 0: out = K^T y;  mode 1: out -= K^T y.
-__global__ void __launch_bounds__(kGradThreads) conv_adjoint_kernel(const float *__restrict__ yv,
-                                                                    const float *__restrict__ k, int m, int B, int H,
-                                                                    int W, float *__restrict__ out, int mode) {
-    const long long n = (long long)B * H * W;
-    const int r = m / 2;
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
-        const long long b = p / ((long long)H * W), rr = p - b * H * W;
-        const int qy = (int)(rr / W), qx = (int)(rr - (long long)qy * W);
-        const float *yb = yv + b * H * W;
-        float s = 0.0f;
+// (K^T y)(q): the exact transpose of conv2d_sym; interior outputs see only the
+// direct sources q + d (a correlation), edge outputs also the mirror preimages.
+template <int m>
+__device__ __forceinline__ float adj_at(const float *__restrict__ yb, const float *__restrict__ k, int qy, int qx,
+                                        int H, int W, bool interior) {
+    constexpr int r = m / 2;
+    float s = 0.0f;
+    if (interior) {
+#pragma unroll
         for (int a = 0; a < m; ++a) {
-            const int dy = a - r;
-            const int cy[3] = {qy + dy, dy - 1 - qy, 2 * H - 1 - qy + dy};
-            for (int iy = 0; iy < 3; ++iy) {
-                const int py = cy[iy];
-                if (py < 0 || py >= H || mirror(py - dy, H) != qy) continue;
-                if (iy > 0 && py == cy[0]) continue;
-                if (iy > 1 && py == cy[1]) continue;
-                for (int c = 0; c < m; ++c) {
-                    const int dx = c - r;
-                    const int cx[3] = {qx + dx, dx - 1 - qx, 2 * W - 1 - qx + dx};
-                    for (int ix = 0; ix < 3; ++ix) {
-                        const int px = cx[ix];
-                        if (px < 0 || px >= W || mirror(px - dx, W) != qx) continue;
-                        if (ix > 0 && px == cx[0]) continue;
-                        if (ix > 1 && px == cx[1]) continue;
-                        s = fmaf(k[a * m + c], yb[(long long)py * W + px], s);
-                    }
+            const float *row = yb + (long long)(qy + a - r) * W + qx - r;
+#pragma unroll
+            for (int c = 0; c < m; ++c) s = fmaf(k[a * m + c], row[c], s);
+        }
+        return s;
+    }
+    for (int a = 0; a < m; ++a) {
+        const int dy = a - r;
+        const int cy[3] = {qy + dy, dy - 1 - qy, 2 * H - 1 - qy + dy};
+        for (int iy = 0; iy < 3; ++iy) {
+            const int py = cy[iy];
+            if (py < 0 || py >= H || mirror(py - dy, H) != qy) continue;
+            for (int c = 0; c < m; ++c) {
+                const int dx = c - r;
+                const int cx[3] = {qx + dx, dx - 1 - qx, 2 * W - 1 - qx + dx};
+                for (int ix = 0; ix < 3; ++ix) {
+                    const int px = cx[ix];
+                    if (px < 0 || px >= W || mirror(px - dx, W) != qx) continue;
+                    s = fmaf(k[a * m + c], yb[(long long)py * W + px], s);
                 }
             }
         }
-        out[p] = mode ? out[p] - s : s;
+    }
+    return s;
+}
+
+// x_f = k_f * u  and  a_f = outer_f^T e  (R1: Kbar_f^T e, R2: K_f e).
+template <int m>
+__global__ void __launch_bounds__(kGradThreads) fwd_pair_kernel(GradFilterArgs g, const float *__restrict__ u,
+                                                                const float *__restrict__ e, int boundary,
+                                                                float *__restrict__ xo, float *__restrict__ ao) {
+    constexpr int r = m / 2;
+    __shared__ float sk[2][m * m];
+    const int f = blockIdx.y;
+    for (int j = threadIdx.x; j < m * m; j += blockDim.x) {
+        sk[0][j] = g.k[(long long)(g.fi0 + f) * m * m + j];
+        sk[1][j] = g.kbar[(long long)(g.fi0 + f) * m * m + j];
+    }
+    __syncthreads();
+    const int H = g.H, W = g.W;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += (long long)gridDim.x * blockDim.x) {
+        const long long b = p / ((long long)H * W), rr = p - b * H * W;
+        const int y = (int)(rr / W), x = (int)(rr - (long long)y * W);
+        const bool in = y >= r && y < H - r && x >= r && x < W - r;
+        xo[(long long)f * g.n + p] = conv_at<m>(u + b * H * W, sk[0], y, x, H, W, in);
+        ao[(long long)f * g.n + p] = boundary == 1 ? conv_at<m>(e + b * H * W, sk[0], y, x, H, W, in)
+                                                   : adj_at<m>(e + b * H * W, sk[1], y, x, H, W, in);
     }
 }
 
-// w = phi(x), b = phi'(x) a; partial sums of -a G_j(x), j in [j0, j0 + 32).
-__global__ void __launch_bounds__(kGradThreads) phi_point_kernel(const float *__restrict__ xv, const float *__restrict__ av,
-                                                                 long long n, const float *__restrict__ rw, int M,
-                                                                 float mu0, float step, float gamma, int j0,
-                                                                 float *__restrict__ wout, float *__restrict__ bout,
-                                                                 float *__restrict__ partial /* [grid][32] */) {
-    float acc[32];
+// w_f = phi(x_f), b_f = phi'(x_f) a_f (Lambda, P l.369-371), partial sums of
+// -a_f G_j(x_f) (d l / d w_j) for j < M <= 64: every Gaussian evaluated once.
+__global__ void __launch_bounds__(kGradThreads) phi_all_kernel(GradFilterArgs g, const float *__restrict__ xv,
+                                                               const float *__restrict__ av, float *__restrict__ wo,
+                                                               float *__restrict__ bo, float *__restrict__ partial) {
+    __shared__ float sw[64];
+    const int f = blockIdx.y, M = g.M;
+    for (int j = threadIdx.x; j < 64; j += blockDim.x) sw[j] = j < M ? g.rw[(long long)(g.fi0 + f) * M + j] : 0.0f;
+    __syncthreads();
+    const float mu0 = g.grid3[(g.fi0 + f) * 3], step = g.grid3[(g.fi0 + f) * 3 + 1], gam = g.grid3[(g.fi0 + f) * 3 + 2];
+    const float inv2g2 = 1.0f / (2.0f * gam * gam), invg2 = 1.0f / (gam * gam);
+    float acc[64];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
-    const float inv2g2 = 1.0f / (2.0f * gamma * gamma), invg2 = 1.0f / (gamma * gamma);
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
-        const float x = xv[p], a = av[p];
-        if (j0 == 0) {
-            float phi = 0.0f, dphi = 0.0f;
-            for (int j = 0; j < M; ++j) {
+    for (int j = 0; j < 64; ++j) acc[j] = 0.0f;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += (long long)gridDim.x * blockDim.x) {
+        const float x = xv[(long long)f * g.n + p], a = av[(long long)f * g.n + p];
+        float phi = 0.0f, dphi = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+            if (j < M) {
                 const float d = x - fmaf((float)j, step, mu0);
                 const float G = __expf(-d * d * inv2g2);
-                phi = fmaf(rw[j], G, phi);
-                dphi = fmaf(-rw[j] * d * invg2, G, dphi);
-            }
-            wout[p] = phi;
-            bout[p] = dphi * a;
-        }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            if (j0 + j < M) {
-                const float d = x - fmaf((float)(j0 + j), step, mu0);
-                acc[j] = fmaf(-a, __expf(-d * d * inv2g2), acc[j]);
+                phi = fmaf(sw[j], G, phi);
+                dphi = fmaf(-sw[j] * d * invg2, G, dphi);
+                acc[j] = fmaf(-a, G, acc[j]);
             }
         }
+        wo[(long long)f * g.n + p] = phi;
+        bo[(long long)f * g.n + p] = dphi * a;
     }
-    block_sum<32>(acc, partial + (long long)blockIdx.x * 32);
+    block_sum<64>(acc, partial + ((long long)f * gridDim.x + blockIdx.x) * 64);
 }
 
-// partial sums of e(p) E(x)(p - (a - r, c - r)) for every tap (a, c).
-template <int MM>
-__global__ void __launch_bounds__(kGradThreads) kernel_grad_kernel(const float *__restrict__ x, const float *__restrict__ e,
-                                                                   int B, int H, int W, float *__restrict__ partial) {
-    constexpr int m = MM, r = MM / 2;
-    float acc[m * m];
-#pragma unroll
-    for (int j = 0; j < m * m; ++j) acc[j] = 0.0f;
-    const long long n = (long long)B * H * W;
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+// t_f = K_f^T b_f.
+template <int m>
+__global__ void __launch_bounds__(kGradThreads) adj_b_kernel(GradFilterArgs g, const float *__restrict__ bv,
+                                                             float *__restrict__ to) {
+    constexpr int r = m / 2;
+    __shared__ float sk[m * m];
+    const int f = blockIdx.y;
+    for (int j = threadIdx.x; j < m * m; j += blockDim.x) sk[j] = g.k[(long long)(g.fi0 + f) * m * m + j];
+    __syncthreads();
+    const int H = g.H, W = g.W;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += (long long)gridDim.x * blockDim.x) {
         const long long b = p / ((long long)H * W), rr = p - b * H * W;
-        const int y = (int)(rr / W), xq = (int)(rr - (long long)y * W);
-        const float ev = e[p];
-        const float *xb = x + b * H * W;
+        const int y = (int)(rr / W), x = (int)(rr - (long long)y * W);
+        const bool in = y >= r && y < H - r && x >= r && x < W - r;
+        to[(long long)f * g.n + p] = adj_at<m>(bv + (long long)f * g.n + b * H * W, sk, y, x, H, W, in);
+    }
+}
+
+// gn -= sum_{f < F} t_f, filters in ascending order.
+__global__ void __launch_bounds__(kGradThreads) sub_sum_kernel(const float *__restrict__ t, int F, long long n,
+                                                               float *__restrict__ gn) {
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+        float v = gn[p];
+        for (int f = 0; f < F; ++f) v -= t[(long long)f * n + p];
+        gn[p] = v;
+    }
+}
+
+// partial sums of the filter derivatives: inner b_f(p) E(u)(p - tap), outer
+// R1: e(p) E(w_f)(p - tap) (kbar's taps), R2: w_f(p) E(e)(p - tap).
+template <int m>
+__global__ void __launch_bounds__(kGradThreads) kgrad_pair_kernel(GradFilterArgs g, const float *__restrict__ u,
+                                                                  const float *__restrict__ e, int boundary,
+                                                                  const float *__restrict__ bv,
+                                                                  const float *__restrict__ wv,
+                                                                  float *__restrict__ partial) {
+    constexpr int r = m / 2, mm = m * m;
+    const int f = blockIdx.y, H = g.H, W = g.W;
+    float acc[2 * mm];
+#pragma unroll
+    for (int j = 0; j < 2 * mm; ++j) acc[j] = 0.0f;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += (long long)gridDim.x * blockDim.x) {
+        const long long b = p / ((long long)H * W), rr = p - b * H * W;
+        const int y = (int)(rr / W), x = (int)(rr - (long long)y * W);
+        const bool in = y >= r && y < H - r && x >= r && x < W - r;
+        const float bp = bv[(long long)f * g.n + p];
+        const float *ub = u + b * H * W;
+        const float *wb = wv + (long long)f * g.n + b * H * W;
+        const float *eb = e + b * H * W;
+        const float op = boundary == 1 ? wb[rr] : eb[rr];     // the weight of the outer sum
+        const float *ob = boundary == 1 ? eb : wb;            // the image it correlates with
 #pragma unroll
         for (int a = 0; a < m; ++a) {
-            const float *row = xb + (long long)mirror(y - (a - r), H) * W;
+            const int yy = in ? y - (a - r) : mirror(y - (a - r), H);
 #pragma unroll
-            for (int c = 0; c < m; ++c) acc[a * m + c] = fmaf(ev, row[mirror(xq - (c - r), W)], acc[a * m + c]);
+            for (int c = 0; c < m; ++c) {
+                const int xx = in ? x - (c - r) : mirror(x - (c - r), W);
+                const long long o = (long long)yy * W + xx;
+                acc[a * m + c] = fmaf(bp, ub[o], acc[a * m + c]);
+                acc[mm + a * m + c] = fmaf(op, ob[o], acc[mm + a * m + c]);
+            }
         }
     }
-    block_sum<m * m>(acc, partial + (long long)blockIdx.x * m * m);
+    block_sum<2 * mm>(acc, partial + ((long long)f * gridDim.x + blockIdx.x) * 2 * mm);
+}
+
+// out[f*np + j] = sum_b partial[(f*nblk + b)*np + j] (fixed order, double).
+__global__ void __launch_bounds__(kGradThreads) reduce_f_kernel(const float *__restrict__ partial, int nblk, int np,
+                                                                double *__restrict__ out, int out_stride,
+                                                                int out_off) {
+    __shared__ double red[kGradThreads];
+    const int f = blockIdx.y, j = blockIdx.x;
+    double s = 0.0;
+    for (int b = threadIdx.x; b < nblk; b += kGradThreads) s += (double)partial[((long long)f * nblk + b) * np + j];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = kGradThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[(long long)f * out_stride + out_off + j] = red[0];
 }
 
 // out[j] = sum over blocks of partial[blk * stride + j], j < np, in double: block j
@@ -250,32 +346,32 @@ cudaError_t grad_bw_prox(const float *ut, const float *f, long long f_ld, int B,
     return cudaGetLastError();
 }
 
-cudaError_t grad_conv_sym(const float *x, const float *k, int m, int B, int H, int W, float *out, int grid,
-                          cudaStream_t s) {
-    conv_sym_kernel<<<grid, kGradThreads, 0, s>>>(x, k, m, B, H, W, out);
-    return cudaGetLastError();
+int grad_chunk_grid(long long n, int F, int num_sms) {
+    const long long want = (n + kGradThreads - 1) / kGradThreads;
+    const long long cap = std::max<long long>(1, ((long long)num_sms * 4 + F - 1) / F);
+    return (int)std::min<long long>(std::max<long long>(want, 1), cap);
 }
 
-cudaError_t grad_conv_adjoint(const float *y, const float *k, int m, int B, int H, int W, float *out, int mode,
-                              int grid, cudaStream_t s) {
-    conv_adjoint_kernel<<<grid, kGradThreads, 0, s>>>(y, k, m, B, H, W, out, mode);
-    return cudaGetLastError();
-}
-
-cudaError_t grad_phi_point(const float *x, const float *a, long long n, const float *rw, int M, float mu0, float step,
-                           float gamma, int j0, float *wout, float *bout, float *partial, int grid, cudaStream_t s) {
-    phi_point_kernel<<<grid, kGradThreads, 0, s>>>(x, a, n, rw, M, mu0, step, gamma, j0, wout, bout, partial);
-    return cudaGetLastError();
-}
-
-cudaError_t grad_kernel(const float *x, const float *e, int m, int B, int H, int W, float *partial, int grid,
-                        cudaStream_t s) {
-    switch (m) {
-        case 3: kernel_grad_kernel<3><<<grid, kGradThreads, 0, s>>>(x, e, B, H, W, partial); break;
-        case 5: kernel_grad_kernel<5><<<grid, kGradThreads, 0, s>>>(x, e, B, H, W, partial); break;
-        case 7: kernel_grad_kernel<7><<<grid, kGradThreads, 0, s>>>(x, e, B, H, W, partial); break;
-        default: return cudaErrorInvalidValue;
+cudaError_t grad_chunk(const GradChunk &c, cudaStream_t s) {
+    GradFilterArgs g{c.k, c.kbar, c.rw, c.grid3, c.fi0, c.m, c.M, c.B, c.H, c.W, (long long)c.B * c.H * c.W};
+    const dim3 grid(c.gx, c.F);
+    const int mm = c.m * c.m;
+#define TNRD_M(NAME, ...)                                                         \
+    switch (c.m) {                                                                \
+        case 3: NAME<3><<<grid, kGradThreads, 0, s>>>(__VA_ARGS__); break;        \
+        case 5: NAME<5><<<grid, kGradThreads, 0, s>>>(__VA_ARGS__); break;        \
+        case 7: NAME<7><<<grid, kGradThreads, 0, s>>>(__VA_ARGS__); break;        \
+        default: return cudaErrorInvalidValue;                                    \
     }
+    if (c.M > 64) return cudaErrorInvalidValue;
+    TNRD_M(fwd_pair_kernel, g, c.u, c.e, c.boundary, c.x, c.a)
+    phi_all_kernel<<<grid, kGradThreads, 0, s>>>(g, c.x, c.a, c.w, c.b, c.partial);
+    reduce_f_kernel<<<dim3(c.M, c.F), kGradThreads, 0, s>>>(c.partial, c.gx, 64, c.red, c.red_stride, 2 * mm);
+    TNRD_M(adj_b_kernel, g, c.b, c.t)
+    sub_sum_kernel<<<c.gx * c.F, kGradThreads, 0, s>>>(c.t, c.F, g.n, c.gn);
+    TNRD_M(kgrad_pair_kernel, g, c.u, c.e, c.boundary, c.b, c.w, c.partial)
+    reduce_f_kernel<<<dim3(2 * mm, c.F), kGradThreads, 0, s>>>(c.partial, c.gx, 2 * mm, c.red, c.red_stride, 0);
+#undef TNRD_M
     return cudaGetLastError();
 }
 

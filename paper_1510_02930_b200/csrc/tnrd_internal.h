@@ -103,15 +103,19 @@ cudaError_t grad_loss(const float *uT, const float *gt, long long gt_ld, int B, 
                       float *partial, int grid, cudaStream_t s);
 cudaError_t grad_bw_prox(const float *ut, const float *f, long long f_ld, int B, int H, int W, float lam,
                          const float *g, float *e, float *gn, float *partial, int grid, cudaStream_t s);
-cudaError_t grad_conv_sym(const float *x, const float *k, int m, int B, int H, int W, float *out, int grid,
-                          cudaStream_t s);
-cudaError_t grad_conv_adjoint(const float *y, const float *k, int m, int B, int H, int W, float *out, int mode,
-                              int grid, cudaStream_t s);
-cudaError_t grad_phi_point(const float *x, const float *a, long long n, const float *rw, int M, float mu0,
-                           float step, float gamma, int j0, float *wout, float *bout, float *partial, int grid,
-                           cudaStream_t s);
-cudaError_t grad_kernel(const float *x, const float *e, int m, int B, int H, int W, float *partial, int grid,
-                        cudaStream_t s);
+// One chunk of F filters of stage t (filters t*Nk + fi0 .. + F): every per-filter
+// step of the backward in 7 launches (tnrd_grad.cu).  Per-filter images x, a, b, w, t
+// are [F][B*H*W]; red[f*red_stride + ...] receives {inner taps, outer taps, -a G_j}.
+struct GradChunk {
+    const float *k, *kbar, *rw, *grid3;
+    int fi0, F, m, M, B, H, W, boundary, gx;
+    const float *u, *e;
+    float *gn, *x, *a, *b, *w, *t, *partial;
+    double *red;
+    int red_stride;
+};
+int grad_chunk_grid(long long n, int F, int num_sms);
+cudaError_t grad_chunk(const GradChunk &c, cudaStream_t s);
 cudaError_t grad_reduce(const float *partial, int nblk, int stride, int np, double *out, cudaStream_t s);
 
 // Data generation and evaluation (tnrd_data.cu).
