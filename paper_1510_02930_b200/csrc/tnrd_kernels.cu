@@ -128,6 +128,12 @@ __device__ __forceinline__ float reaction_step(int kind, float u, float ut, floa
     return prox_poisson(ut, lam, f);
 }
 
+// Per-lane left cut of the Horner units: a lane with t < -kCutT
+// sees only block terms below 2^-30.25 of their weight, so G's exponent is pushed
+// below -126 there (an exact zero, decided per lane, so skipping stays warp-
+// independent); bitwise unchanged where the cut does not bind.
+constexpr float kCutT = 5.5f, kCutBig = 1048576.0f;
+
 // Horner units [u0, u1] on NP pairs (see tnrd_internal.h).  Each unit is
 // expanded from its first centre: t = sg (x - 8b), G = 2^(-t^2), R = 2^(two_sg t),
 // block sum = G * sum_{e<8} c_e R^e  (2 MUFU per element).  R is clamped above at
@@ -144,7 +150,8 @@ __device__ __forceinline__ void horner_units(const float *__restrict__ units, fl
 #pragma unroll
         for (int e = 0; e < NP; ++e) {
             const f2 t = fma2(v[e], bc(a_s), bc(q0.x));
-            const f2 sq = mul2(t, t);
+            const f2 q = fma2(t, bc(-kCutBig), bc(-kCutBig * kCutT));  // kCutBig * relu(-t - kCutT)
+            const f2 sq = fma2(t, t, pk(fmaxf(lo(q), 0.0f), fmaxf(hi(q), 0.0f)));
             const f2 G = pk(ex2_ftz(-lo(sq)), ex2_ftz(-hi(sq)));
             const f2 yr = mul2(t, bc(two_sg));
             const f2 R = pk(ex2_ftz(fminf(lo(yr), yrmax)), ex2_ftz(fminf(hi(yr), yrmax)));
@@ -210,7 +217,8 @@ __device__ __forceinline__ void phi_x2(const float *__restrict__ fp, int mode, c
     const float yhi = warp_max(fmaf(a_s, vmax, cs0));
     // unit u has ys_u = ys_0 - u*ustep; it can be nonzero only if |ys_u| <= kWindow
     const int u0 = max(0, __float2int_ru((ylo - kWindow) * inv_ustep));
-    const int u1 = min(nunits - 1, __float2int_rd((yhi + kWindow) * inv_ustep));
+    // Horner units are also exactly zero for a lane with t < -(kCutT + 0.01) (left cut)
+    const int u1 = min(nunits - 1, __float2int_rd((yhi + (mode == MODE_HORNER ? kCutT + 0.01f : kWindow)) * inv_ustep));
     if (mode == MODE_HORNER) {
         horner_units<NP>(units, a_s, two_sg, yclamp, u0, u1, v, w);
     } else {
