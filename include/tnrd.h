@@ -138,9 +138,13 @@ TNRD_API tnrd_status tnrd_denoise(tnrd_handle *h, const float *f_dev, float *u_d
                          long long ld, const float *peak, void *cuda_stream);
 
 /* End-to-end variant: f_host -> device -> denoise -> u_host, dense rows (ld = W).
- * Host->device and device->host copies are enqueued on cuda_stream; the call
- * synchronises the stream before returning (u_host is valid on return).
- * Pinned host memory gives full PCIe/NVLink-C2C bandwidth. */
+ * Large batches are pipelined in up to 8 chunks: the host-to-device copy of chunk
+ * c+1 and the device-to-host copy of chunk c-1 run on handle-owned copy streams
+ * while chunk c is denoised on cuda_stream (results identical to one call).
+ * The copy streams start after the work already enqueued on cuda_stream, and
+ * cuda_stream is ordered after the last copy; the call synchronises before
+ * returning (u_host is valid on return).  Pinned host memory is needed for the
+ * copies to overlap (and gives full PCIe bandwidth). */
 TNRD_API tnrd_status tnrd_denoise_host(tnrd_handle *h, const float *f_host, float *u_host, int B, int H,
                               int W, const float *peak, void *cuda_stream);
 

@@ -105,6 +105,8 @@ struct tnrd_handle {
     unsigned long long launches = 0;
     bool profile = false;
     std::vector<cudaEvent_t> ev;   // pairs (start, stop) per profiled launch
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;   // tnrd_denoise_host copy streams
+    std::vector<cudaEvent_t> chunk_ev;               // 2 per pipelined chunk
     int ev_used = 0;
     std::string err;
 };
@@ -584,10 +586,42 @@ tnrd_status tnrd_denoise_host(tnrd_handle *h, const float *f_host, float *u_host
     if (st != TNRD_OK) return st;
     h->e2e_bytes = std::min(have_f, have_u);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    TNRD_CUDA(h, cudaMemcpyAsync(h->e2e_f, f_host, bytes, cudaMemcpyHostToDevice, s));
-    st = tnrd_denoise(h, h->e2e_f, h->e2e_u, B, H, W, W, peak, stream);
-    if (st != TNRD_OK) return st;
-    TNRD_CUDA(h, cudaMemcpyAsync(u_host, h->e2e_u, bytes, cudaMemcpyDeviceToHost, s));
+    // Pipeline over batch chunks: H2D of chunk c+1 and D2H of chunk c-1 (own
+    // streams) overlap the stages of chunk c (caller's stream).  Chunks keep at
+    // least ~4 tile pairs per SM so each stays on the large-tile kernel; the
+    // per-pixel arithmetic does not depend on the chunking.
+    const long long tiles_img = (long long)((H + 63) / 64) * ((W + 63) / 64);
+    const int min_imgs = (int)std::max<long long>(1, (8LL * h->num_sms + tiles_img - 1) / tiles_img);
+    const int nchunk = std::max(1, std::min(8, B / min_imgs));
+    if (!h->s_h2d) {
+        TNRD_CUDA(h, cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+        TNRD_CUDA(h, cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+    }
+    while ((int)h->chunk_ev.size() < 2 * nchunk + 1) {
+        cudaEvent_t e;
+        TNRD_CUDA(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->chunk_ev.push_back(e);
+    }
+    const size_t img = (size_t)H * W;
+    for (int c = 0; c < nchunk; ++c) {
+        const int b0 = (int)((long long)B * c / nchunk), b1 = (int)((long long)B * (c + 1) / nchunk);
+        const size_t off = (size_t)b0 * img, cb = sizeof(float) * (size_t)(b1 - b0) * img;
+        cudaEvent_t in = h->chunk_ev[2 * c], out = h->chunk_ev[2 * c + 1];
+        if (c == 0) {  // the copy streams start after the caller's earlier work
+            TNRD_CUDA(h, cudaEventRecord(h->chunk_ev[2 * nchunk], s));
+            TNRD_CUDA(h, cudaStreamWaitEvent(h->s_h2d, h->chunk_ev[2 * nchunk], 0));
+        }
+        TNRD_CUDA(h, cudaMemcpyAsync(h->e2e_f + off, f_host + off, cb, cudaMemcpyHostToDevice, h->s_h2d));
+        TNRD_CUDA(h, cudaEventRecord(in, h->s_h2d));
+        TNRD_CUDA(h, cudaStreamWaitEvent(s, in, 0));
+        st = tnrd_denoise(h, h->e2e_f + off, h->e2e_u + off, b1 - b0, H, W, W, peak ? peak + b0 : nullptr, stream);
+        if (st != TNRD_OK) return st;
+        TNRD_CUDA(h, cudaEventRecord(out, s));
+        TNRD_CUDA(h, cudaStreamWaitEvent(h->s_d2h, out, 0));
+        TNRD_CUDA(h, cudaMemcpyAsync(u_host + off, h->e2e_u + off, cb, cudaMemcpyDeviceToHost, h->s_d2h));
+    }
+    TNRD_CUDA(h, cudaEventRecord(h->chunk_ev[2 * nchunk], h->s_d2h));
+    TNRD_CUDA(h, cudaStreamWaitEvent(s, h->chunk_ev[2 * nchunk], 0));  // caller's stream ordered after the copies
     TNRD_CUDA(h, cudaStreamSynchronize(s));
     return TNRD_OK;
 }
@@ -610,6 +644,9 @@ tnrd_status tnrd_destroy(tnrd_handle *h) {
         cudaFree(h->slab_buf[1]);
         for (float *p : h->lb_bufs) cudaFree(p);
         for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+        for (cudaEvent_t e : h->chunk_ev) cudaEventDestroy(e);
+        if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
+        if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
         if (h->comm && nccl().loaded) nccl().CommDestroy(h->comm);
     }
     delete h;

@@ -391,3 +391,17 @@ def test_poisson_gradient_reaction_parity(torch_cuda, P, cfg):
     assert np.all(np.isfinite(u_ref))
     u = _gpu_denoise(P, torch_cuda, p.model, f, reaction=P.REACTION_POISSON_GRADIENT)[0]
     _assert_parity(u, u_ref, float(p.peaks[0]) + 1.0, what=f"poisson-gradient C{cfg}")
+
+
+def test_host_entry_point_pipelined_chunks_bitwise(torch_cuda, P):
+    """tnrd_denoise_host pipelines large batches in chunks (copies on their own
+    streams); 40 images of 512^2 give 2 chunks.  Results equal the device path bitwise."""
+    torch = torch_cuda
+    p = make_problem(4, batch=40)
+    eng = P.TNRD(p.model)
+    u_dev = eng.denoise(torch.from_numpy(p.f).cuda()).cpu().numpy()
+    f_pin = torch.from_numpy(p.f).pin_memory()
+    u_pin = torch.empty_like(f_pin).pin_memory()
+    P.tnrd_denoise_host_ptr(eng.h, f_pin.data_ptr(), u_pin.data_ptr(), 40, 512, 512)
+    eng.close()
+    assert np.array_equal(u_pin.numpy(), u_dev)
