@@ -707,11 +707,12 @@ __global__ void __launch_bounds__(32 * (C::XW + C::YW), C::MINB) stage_kernel(co
 //  0 = "L": two 64x64 output tiles, 8 X warps + 8 Y warps (512 threads, 128
 //      registers), 3 slots, d in registers; 1 CTA per SM (~200 KB shared memory).
 //      (8 + 16 warps at 80 registers, d parked in smem, 2 slots: 27.1 vs 23.8 ms.)
-//  1 = "S": two 32x32 output tiles, 2 + 2 warps, 3 slots, d in registers, for
-//      images too small to fill the GPU with "L" tiles.
+//  1 = "S": two 32x32 output tiles, 8 + 8 warps (one conv / phi pass each per
+//      filter), 3 slots, d in registers, for images too small to fill the GPU with
+//      "L" tiles (C3, one 512^2 image: 1.66 ms; 2.34 ms with 2 + 2 warps).
 struct Cfg0 { static constexpr int TW = 64, TH = 64, XW = 8, YW = 8, RUNWY = 10, BR = 8, NSLOT = 3, MINB = 1;
               static constexpr bool ACC_SMEM = false; };
-struct Cfg1 { static constexpr int TW = 32, TH = 32, XW = 2, YW = 2, RUNWY = 10, BR = 8, NSLOT = 3, MINB = 3;
+struct Cfg1 { static constexpr int TW = 32, TH = 32, XW = 8, YW = 8, RUNWY = 10, BR = 2, NSLOT = 3, MINB = 1;
               static constexpr bool ACC_SMEM = false; };
 
 template <int K, class C>
