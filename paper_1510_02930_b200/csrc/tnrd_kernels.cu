@@ -767,9 +767,11 @@ size_t stage_smem_bytes(int ksize, int tile, int Nk, int pstride) {
 
 int choose_tile(int ksize, int B, int H, int W, int num_sms) {
     (void)ksize;
-    // "L" when its tile pairs fill every SM at least twice, else the small tiles
+    // "L" once its tile pairs fill at least half a wave: measured on 512^2 images
+    // (profiles/r01_tile_crossover.json) L takes 2.94 ms for 1..4 images (<= one
+    // wave) while S takes 1.61 / 2.80 / 3.94 ms for 1 / 2 / 3 images.
     const long long pairs = ((long long)B * ((H + 63) / 64) * ((W + 63) / 64) + 1) / 2;
-    return pairs >= 2LL * num_sms ? 0 : 1;
+    return 2 * pairs >= num_sms ? 0 : 1;
 }
 
 cudaError_t launch_stage(int ksize, int tile, StageArgs &a, int B, cudaStream_t s) {
