@@ -86,6 +86,20 @@ typedef enum {
     TNRD_REACTION_POISSON_GRADIENT = 2
 } tnrd_reaction;
 
+/* Execution engine of the stage kernel (tnrd_set_engine).  Both compute P Eq.13
+ * in fp32 storage with the same phi and reaction; they differ in the two filter-bank
+ * contractions (P l.137, l.309-311):
+ *   FP32:   fp32 FMAs on the CUDA cores (tnrd_kernels.cu);
+ *   TENSOR: tcgen05 tensor-core GEMMs in 3xTF32 (each operand split hi + lo, three
+ *           TF32 products, fp32 accumulation; tnrd_tc.cu), for
+ *           (ksize, N_k) in {(3, 8), (5, 24), (7, 48)}, boundary R1, TNRD_PHI_EXACT;
+ *   AUTO:   TENSOR where it applies, else FP32 (the default). */
+typedef enum {
+    TNRD_ENGINE_AUTO = 0,
+    TNRD_ENGINE_FP32 = 1,
+    TNRD_ENGINE_TENSOR = 2
+} tnrd_engine;
+
 /* Model shape.  T >= 1 stages, n_filters = N_k >= 1 (P l.423: N_k = m^2 - 1 if
  * not specified, not enforced), ksize = m in {3, 5, 7}, n_rbf = M in [1, 256],
  * device = CUDA ordinal, reaction = tnrd_reaction (0 = the paper's Eq.13). */
@@ -122,6 +136,14 @@ TNRD_API tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out);
  * EINVAL on non-finite values, step/gamma <= 0, lambda <= 0, t out of range.
  * Derived fp32 evaluation constants are computed on the host in double.
  * Synchronous (uploads with a blocking copy). */
+/* Select the engine (tnrd_engine) for later tnrd_denoise* calls on h; the
+ * training tape (tnrd_loss_grad) always uses FP32.  EINVAL: bad value.  Host-only. */
+TNRD_API tnrd_status tnrd_set_engine(tnrd_handle *h, int engine);
+
+/* The engine (TNRD_ENGINE_FP32 or TNRD_ENGINE_TENSOR) tnrd_denoise would use for
+ * a B x H x W batch now; -1 if h is null or a stage is unset.  Host-only. */
+TNRD_API int tnrd_engine_for(tnrd_handle *h, int B, int H, int W);
+
 TNRD_API tnrd_status tnrd_set_stage_params(tnrd_handle *h, int t, const float *filters, const float *rbf_w,
                                   const float *rbf_mu0, const float *rbf_step,
                                   const float *rbf_gamma, float lambda);

@@ -30,6 +30,9 @@ PHI_TABLE = 1
 REACTION_POISSON_PROX = 0
 REACTION_GAUSSIAN = 1
 REACTION_POISSON_GRADIENT = 2
+ENGINE_AUTO = 0      # tnrd_engine: tensor cores where they apply, else FP32
+ENGINE_FP32 = 1
+ENGINE_TENSOR = 2
 
 
 class TNRDError(RuntimeError):
@@ -80,6 +83,8 @@ def _load() -> ctypes.CDLL:
         "tnrd_loss_grad": ([vp, vp, vp, i, i, i, ll, fp, fp, fp, ctypes.POINTER(ctypes.c_double), vp], i),
         "tnrd_sample_poisson": ([vp, vp, i, i, i, ll, ctypes.c_ulonglong, vp], i),
         "tnrd_psnr": ([vp, vp, i, i, i, ll, fp, ctypes.POINTER(ctypes.c_double), vp], i),
+        "tnrd_set_engine": ([vp, i], i),
+        "tnrd_engine_for": ([vp, i, i, i], i),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -94,7 +99,7 @@ EXPORTED = (
     "tnrd_denoise", "tnrd_denoise_host", "tnrd_destroy", "tnrd_last_error", "tnrd_launch_count",
     "tnrd_nccl_unique_id", "tnrd_comm_init", "tnrd_denoise_slab", "tnrd_denoise_slabs_loopback",
     "tnrd_set_profiling", "tnrd_get_launch_times", "tnrd_debug_phi", "tnrd_debug_prox", "tnrd_loss_grad",
-    "tnrd_sample_poisson", "tnrd_psnr",
+    "tnrd_sample_poisson", "tnrd_psnr", "tnrd_set_engine", "tnrd_engine_for",
 )
 
 
@@ -226,6 +231,14 @@ def tnrd_denoise_slabs_loopback(h: int, f, u, nslabs: int, stream=None) -> None:
                                             nslabs, _stream_ptr(stream)), h)
 
 
+def tnrd_set_engine(h: int, engine: int) -> None:
+    _check(_lib.tnrd_set_engine(h, engine), h)
+
+
+def tnrd_engine_for(h: int, B: int, H: int, W: int) -> int:
+    return int(_lib.tnrd_engine_for(h, B, H, W))
+
+
 def tnrd_set_profiling(h: int, enable: bool) -> None:
     _check(_lib.tnrd_set_profiling(h, 1 if enable else 0), h)
 
@@ -298,7 +311,7 @@ class TNRD:
     """
 
     def __init__(self, model, boundary: int = BC_SYMMETRIC_EXPLICIT, device: int = 0, phi_mode: int = PHI_EXACT,
-                 reaction: int = REACTION_POISSON_PROX):
+                 reaction: int = REACTION_POISSON_PROX, engine: int = 0):
         T, Nk, k, _ = np.shape(model.filters)
         M = np.shape(model.rbf_w)[2]
         self.T, self.Nk, self.k, self.M = int(T), int(Nk), int(k), int(M)
@@ -307,6 +320,11 @@ class TNRD:
         for t in range(self.T):
             tnrd_set_stage_params(self.h, t, model.filters[t], model.rbf_w[t], model.rbf_mu0[t],
                                   model.rbf_step[t], model.rbf_gamma[t], model.lam[t])
+        tnrd_set_engine(self.h, engine)
+
+    def engine_for(self, B: int, H: int, W: int) -> int:
+        """ENGINE_FP32 or ENGINE_TENSOR: the engine a B x H x W denoise runs on."""
+        return tnrd_engine_for(self.h, B, H, W)
 
     def denoise(self, f, u=None, peak=None, stream=None):
         import torch

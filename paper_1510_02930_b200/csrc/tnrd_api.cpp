@@ -83,6 +83,11 @@ struct tnrd_handle {
     float *d_params = nullptr;    // [T][Nk][pstride_max]
     float4 *d_table = nullptr;    // MODE_TABLE: [T][Nk][table_stride] cubic intervals
     int table_stride = 0;
+    // tensor-core engine (tnrd_tc.cu): per stage operand block [T][tc_stride]
+    float *d_tc = nullptr;
+    int tc_stride = 0;
+    std::vector<char> tc_ok;      // per stage: block packed (Horner phi)
+    int engine = TNRD_ENGINE_AUTO;
     // raw stage parameters (training gradient, tnrd_loss_grad)
     std::vector<float> raw_mu0, raw_step, raw_gamma;   // host [T][Nk]
     float *d_raw = nullptr;       // device: k [T][Nk][m*m], kbar [T][Nk][m*m], w [T][Nk][M]
@@ -169,22 +174,54 @@ tnrd_status check_ready(tnrd_handle *h) {
     return TNRD_OK;
 }
 
-// Tile configuration for a launch: "L" (tile pairs of 64x64) when there are enough
-// tiles to fill the GPU, else "S".  TNRD_FORCE_TILE=L|S overrides the choice (tests
-// use it to run every code path on small, fully oracle-checkable images); the
-// result is identical either way (per-pixel arithmetic does not depend on tiling).
-int pick_tile(const tnrd_handle *h, int B, int H, int W) {
-    static const char *force = getenv("TNRD_FORCE_TILE");
-    if (force && (force[0] == 'L' || force[0] == 'l') && h->allow_large_tile) return 0;
-    if (force && (force[0] == 'S' || force[0] == 's')) return 1;
-    return h->allow_large_tile ? tnrd::choose_tile(h->d.ksize, B, H, W, h->num_sms) : 1;
+// Launch plan: engine and tile configuration.
+struct Plan {
+    int tile = 1;    // FP32 engine: 0 = "L" (tile pairs of 64x64), 1 = "S"
+    int tc_oh = 0;   // > 0: tensor-core engine with tiles of tc_oh output rows
+};
+
+// The tensor-core engine can run every stage of this handle: a built (ksize, N_k)
+// instantiation, boundary R1 and Horner-unit phi in every stage.
+bool tc_ready(const tnrd_handle *h) {
+    if (!h->d_tc || h->d.boundary != TNRD_BC_SYMMETRIC_EXPLICIT) return false;
+    for (int t = 0; t < h->d.T; ++t)
+        if (!h->tc_ok[t]) return false;
+    return true;
 }
 
-tnrd_status launch_one(tnrd_handle *h, int t, int tile, StageArgs &a, int B, cudaStream_t s) {
+// Engine: tnrd_set_engine (TNRD_ENGINE=fp32|tc in the environment overrides it
+// for tests); AUTO takes the tensor-core engine when it can run.  FP32 tile: "L"
+// when there are enough tiles to fill the GPU, else "S"; TNRD_FORCE_TILE=L|S
+// overrides (tests run every code path on small, fully oracle-checkable images).
+// Results do not depend on the tile choice (per-pixel arithmetic is tiling-free).
+Plan plan_for(const tnrd_handle *h, int B, int H, int W, bool allow_tc) {
+    Plan p;
+    static const char *env_engine = getenv("TNRD_ENGINE");
+    int engine = h->engine;
+    if (env_engine && env_engine[0] == 'f') engine = TNRD_ENGINE_FP32;
+    if (env_engine && env_engine[0] == 't') engine = TNRD_ENGINE_TENSOR;
+    if (allow_tc && engine != TNRD_ENGINE_FP32 && tc_ready(h)) {
+        p.tc_oh = tnrd::tc_choose_rows(h->d.ksize, B, H, W, h->num_sms);
+        return p;
+    }
+    static const char *force = getenv("TNRD_FORCE_TILE");
+    if (force && (force[0] == 'L' || force[0] == 'l') && h->allow_large_tile) { p.tile = 0; return p; }
+    if (force && (force[0] == 'S' || force[0] == 's')) { p.tile = 1; return p; }
+    p.tile = h->allow_large_tile ? tnrd::choose_tile(h->d.ksize, B, H, W, h->num_sms) : 1;
+    return p;
+}
+
+tnrd_status launch_one(tnrd_handle *h, int t, const Plan &plan, StageArgs &a, int B, cudaStream_t s) {
     a.params = h->d_params + (size_t)t * h->d.n_filters * h->pstride_max;
     a.Nk = h->d.n_filters;
     a.pstride = h->pstride[t];
     a.mode = h->mode[t];
+    if (plan.tc_oh > 0) {
+        a.params = h->d_tc + (size_t)t * h->tc_stride;
+        a.pstride = tnrd::tc_phi_stride(h->d.n_rbf);
+        a.tc_par_floats = h->tc_stride;
+        a.tc_oh = plan.tc_oh;
+    }
     a.table = h->d_table ? h->d_table + (size_t)t * h->d.n_filters * h->table_stride : nullptr;
     a.table_stride = h->table_stride;
     a.boundary = h->d.boundary;
@@ -200,7 +237,8 @@ tnrd_status launch_one(tnrd_handle *h, int t, int tile, StageArgs &a, int B, cud
         }
         TNRD_CUDA(h, cudaEventRecord(h->ev[h->ev_used], s));
     }
-    cudaError_t e = tnrd::launch_stage(h->d.ksize, tile, a, B, s);
+    cudaError_t e = plan.tc_oh > 0 ? tnrd::launch_stage_tc(h->d.ksize, a, B, s)
+                                   : tnrd::launch_stage(h->d.ksize, plan.tile, a, B, s);
     if (e != cudaSuccess) return cuda_fail(h, e, "stage kernel launch");
     if (h->profile) {
         TNRD_CUDA(h, cudaEventRecord(h->ev[h->ev_used + 1], s));
@@ -239,9 +277,9 @@ tnrd_status run_slab(tnrd_handle *h, const float *f_slab, long long f_ld, float 
     a.y_begin = row0; a.y_end = row0 + rows;
     a.avail_lo = row0 - halo < 0 ? 0 : row0 - halo;
     a.avail_hi = row0 + rows + halo > H ? H : row0 + rows + halo;
-    const int tile = pick_tile(h, 1, rows, W);
+    const Plan plan = plan_for(h, 1, rows, W, true);
     (void)ex; (void)k;
-    return launch_one(h, stage, tile, a, 1, s);
+    return launch_one(h, stage, plan, a, 1, s);
 }
 
 struct NcclExchange : SlabExchange {
@@ -366,6 +404,41 @@ int pstride_for(const tnrd_desc &d, int mode) {
     return (tnrd::tap_floats(d.ksize) + tnrd::kFc + units + 3) / 4 * 4;
 }
 
+// Tensor-core operand block of one stage (tnrd_internal.h): taps split as
+// hi = tf32(x), lo = tf32(x - hi) (round to nearest) in the UMMA K-major layout,
+// for the forward bank [Nk x KTP] and transposed for the adjoint bank [NZ x Nk],
+// then the Horner phi constants of `phi_host` (pack_stage layout, stride ps) with a
+// zero unit appended per filter.
+float tf32_rn_host(float x) {
+    uint32_t b;
+    std::memcpy(&b, &x, 4);
+    b = (b + 0x1000u) & 0xFFFFE000u;
+    float r;
+    std::memcpy(&r, &b, 4);
+    return r;
+}
+
+void pack_tc_stage(const tnrd_desc &d, const float *filters, const float *phi_host, int ps, float *out) {
+    const int K = d.ksize, Nk = d.n_filters, M = d.n_rbf, KT = K * K;
+    const int KTP = tnrd::tc_ktp(K), NZ = tnrd::tc_nz(K), PST = tnrd::tc_phi_stride(M);
+    std::memset(out, 0, sizeof(float) * tnrd::tc_par_floats(K, Nk, M));
+    float *bf_hi = out, *bf_lo = out + (size_t)Nk * KTP;
+    float *ba_hi = out + 2 * (size_t)Nk * KTP, *ba_lo = ba_hi + (size_t)NZ * Nk;
+    float *phi = ba_lo + (size_t)NZ * Nk;
+    for (int n = 0; n < Nk; ++n)
+        for (int t = 0; t < KT; ++t) {
+            const float x = filters[(size_t)n * KT + t];
+            const float hi = tf32_rn_host(x), lo = tf32_rn_host(x - hi);
+            bf_hi[tnrd::tc_b_index(n, t, KTP)] = hi;
+            bf_lo[tnrd::tc_b_index(n, t, KTP)] = lo;
+            ba_hi[tnrd::tc_b_index(t, n, Nk)] = hi;
+            ba_lo[tnrd::tc_b_index(t, n, Nk)] = lo;
+        }
+    const int nfl = tnrd::kFc + ((M + 7) / 8) * tnrd::kHornerUnit;
+    for (int n = 0; n < Nk; ++n)
+        std::memcpy(phi + (size_t)n * PST, phi_host + (size_t)n * ps + tnrd::tap_floats(K), sizeof(float) * nfl);
+}
+
 }  // namespace
 
 extern "C" {
@@ -431,6 +504,7 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
         e = cudaMalloc(&h->d_raw, sizeof(float) * (size_t)d->T * d->n_filters * (2 * mm + d->n_rbf + 3));
         if (e != cudaSuccess) {
             cudaFree(h->d_params);
+        cudaFree(h->d_tc);
             delete h;
             return fail(nullptr, TNRD_ENOMEM, "cudaMalloc raw params: %s", cudaGetErrorString(e));
         }
@@ -438,11 +512,24 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
         h->raw_step = h->raw_mu0;
         h->raw_gamma = h->raw_mu0;
     }
+    h->tc_ok.assign(d->T, 0);
+    if (tnrd::tc_supported(d->ksize, d->n_filters) && d->boundary == TNRD_BC_SYMMETRIC_EXPLICIT &&
+        d->phi_mode == TNRD_PHI_EXACT) {
+        h->tc_stride = tnrd::tc_par_floats(d->ksize, d->n_filters, d->n_rbf);
+        e = cudaMalloc(&h->d_tc, sizeof(float) * (size_t)d->T * h->tc_stride);
+        if (e != cudaSuccess) {
+            cudaFree(h->d_params);
+        cudaFree(h->d_tc);
+            delete h;
+            return fail(nullptr, TNRD_ENOMEM, "cudaMalloc tensor-core operands: %s", cudaGetErrorString(e));
+        }
+    }
     if (d->phi_mode == TNRD_PHI_TABLE) {
         h->table_stride = table_intervals(d->n_rbf) + 1;
         e = cudaMalloc(&h->d_table, sizeof(float4) * (size_t)d->T * d->n_filters * h->table_stride);
         if (e != cudaSuccess) {
             cudaFree(h->d_params);
+        cudaFree(h->d_tc);
             delete h;
             return fail(nullptr, TNRD_ENOMEM, "cudaMalloc phi tables: %s", cudaGetErrorString(e));
         }
@@ -523,11 +610,31 @@ tnrd_status tnrd_set_stage_params(tnrd_handle *h, int t, const float *filters, c
     DeviceGuard g(h->d.device);
     TNRD_CUDA(h, cudaMemcpy(h->d_params + (size_t)t * Nk * h->pstride_max, host.data(),
                             sizeof(float) * host.size(), cudaMemcpyHostToDevice));
+    h->tc_ok[t] = 0;
+    if (h->d_tc && mode == tnrd::MODE_HORNER) {
+        std::vector<float> tc((size_t)h->tc_stride);
+        pack_tc_stage(h->d, filters, host.data(), ps, tc.data());
+        TNRD_CUDA(h, cudaMemcpy(h->d_tc + (size_t)t * h->tc_stride, tc.data(), sizeof(float) * tc.size(),
+                                cudaMemcpyHostToDevice));
+        h->tc_ok[t] = 1;
+    }
     h->pstride[t] = ps;
     h->mode[t] = mode;
     h->lambda[t] = lambda;
     h->is_set[t] = 1;
     return TNRD_OK;
+}
+
+tnrd_status tnrd_set_engine(tnrd_handle *h, int engine) {
+    if (!h) return fail(nullptr, TNRD_EINVAL, "null handle");
+    if (engine < TNRD_ENGINE_AUTO || engine > TNRD_ENGINE_TENSOR) return fail(h, TNRD_EINVAL, "bad engine %d", engine);
+    h->engine = engine;
+    return TNRD_OK;
+}
+
+int tnrd_engine_for(tnrd_handle *h, int B, int H, int W) {
+    if (!h || check_ready(h) != TNRD_OK) return -1;
+    return plan_for(h, B, H, W, true).tc_oh > 0 ? TNRD_ENGINE_TENSOR : TNRD_ENGINE_FP32;
 }
 
 tnrd_status tnrd_denoise(tnrd_handle *h, const float *f, float *u, int B, int H, int W, long long ld,
@@ -551,7 +658,7 @@ tnrd_status tnrd_denoise(tnrd_handle *h, const float *f, float *u, int B, int H,
         st = grow(h, &h->scratch, &h->scratch_bytes, sizeof(float) * (size_t)B * H * W, "scratch");
         if (st != TNRD_OK) return st;
     }
-    const int tile = pick_tile(h, B, H, W);
+    const Plan plan = plan_for(h, B, H, W, true);
     const tnrd::Image in_f{f, ld, (long long)H * ld, 0};
     const tnrd::Image in_s{h->scratch, W, (long long)H * W, 0};
     const tnrd::Image in_u{u, ld, (long long)H * ld, 0};
@@ -565,7 +672,7 @@ tnrd_status tnrd_denoise(tnrd_handle *h, const float *f, float *u, int B, int H,
         else { a.u_out = h->scratch; a.out_ld = W; a.out_img_stride = (long long)H * W; }
         a.out_row_base = 0;
         a.H = H; a.W = W; a.y_begin = 0; a.y_end = H; a.avail_lo = 0; a.avail_hi = H;
-        st = launch_one(h, t, tile, a, B, s);
+        st = launch_one(h, t, plan, a, B, s);
         if (st != TNRD_OK) return st;
     }
     return TNRD_OK;
@@ -632,6 +739,7 @@ tnrd_status tnrd_destroy(tnrd_handle *h) {
         DeviceGuard g(h->d.device);
         cudaDeviceSynchronize();
         cudaFree(h->d_params);
+        cudaFree(h->d_tc);
         cudaFree(h->d_table);
         cudaFree(h->d_raw);
         cudaFree(h->g_buf);
@@ -746,7 +854,7 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
     // ---- forward with tape (the fused stage kernel also writes ut)
     TNRD_K(cudaMemcpy2DAsync(tape_u, sizeof(float) * W, f, sizeof(float) * ld, sizeof(float) * W, (size_t)B * H,
                              cudaMemcpyDeviceToDevice, s));
-    const int tile = pick_tile(h, B, H, W);
+    const Plan plan = plan_for(h, B, H, W, false);  // the tape comes from the FP32 engine
     for (int t = 0; t < T; ++t) {
         StageArgs a{};
         a.u_in = {tape_u + (size_t)t * n, W, (long long)H * W, 0};
@@ -754,7 +862,7 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
         a.u_out = tape_u + (size_t)(t + 1) * n; a.out_ld = W; a.out_img_stride = (long long)H * W; a.out_row_base = 0;
         a.ut_out = tape_ut + (size_t)t * n;
         a.H = H; a.W = W; a.y_begin = 0; a.y_end = H; a.avail_lo = 0; a.avail_hi = H;
-        st = launch_one(h, t, tile, a, B, s);
+        st = launch_one(h, t, plan, a, B, s);
         if (st != TNRD_OK) return st;
     }
     TNRD_K(tnrd::grad_loss(tape_u + (size_t)T * n, u_gt, ld, B, H, W, gb, part, grid, s));

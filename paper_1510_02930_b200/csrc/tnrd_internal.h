@@ -84,6 +84,9 @@ struct StageArgs {
     int table_stride;      // float4s per filter (n_int + 1)
     // tiling (filled by launch_stage): tiles in x-fastest, then y, then image order
     int tiles_x, tiles_y, n_tiles;
+    // tensor-core engine (tnrd_tc.cu): output rows per tile and floats of the
+    // stage's operand block at `params` (pstride = phi floats per filter there)
+    int tc_oh, tc_par_floats;
 };
 
 // Kernel launchers (tnrd_kernels.cu).  Return cudaSuccess or the launch error.
@@ -96,6 +99,27 @@ cudaError_t launch_debug_prox(const float *ut, const float *f, float lambda, flo
                               long long n, cudaStream_t s);
 cudaError_t launch_copy_rows(const float *src, long long src_ld, float *dst, long long dst_ld,
                              int rows, int W, cudaStream_t s);
+
+// Tensor-core engine (tnrd_tc.cu): 3xTF32 tcgen05 GEMMs for both filter banks.
+// Stage operand block (floats), built by the host (tnrd_api.cpp, pack_tc_stage):
+//   bf_hi, bf_lo [Nk x KTP]  k_i taps, UMMA K-major no-swizzle layout (tc_b_index)
+//   ba_hi, ba_lo [NZ x Nk]   the same taps transposed (tap-major rows)
+//   phi          [Nk][tc_phi_stride(M)]  {fc[8], NB Horner units, one zero unit}
+// KTP = roundup(k*k, 8) (GEMM K of the forward bank), NZ = max(16, KTP).
+constexpr int kTcVW = 64;   // v-region columns per tile (an M = 128 block is two rows)
+__host__ __device__ constexpr int tc_ktp(int K) { return (K * K + 7) / 8 * 8; }
+__host__ __device__ constexpr int tc_nz(int K) { return tc_ktp(K) < 16 ? 16 : tc_ktp(K); }
+__host__ __device__ constexpr int tc_phi_stride(int M) { return kFc + ((M + 7) / 8 + 1) * kHornerUnit; }
+__host__ __device__ constexpr int tc_par_floats(int K, int Nk, int M) {
+    return 2 * Nk * tc_ktp(K) + 2 * tc_nz(K) * Nk + Nk * tc_phi_stride(M);
+}
+// element (row n, column k) of a rows x kdim K-major operand (8-row x 4-float core matrices)
+__host__ __device__ constexpr int tc_b_index(int n, int k, int kdim) {
+    return ((n >> 3) * (kdim >> 2) + (k >> 2)) * 32 + (n & 7) * 4 + (k & 3);
+}
+bool tc_supported(int ksize, int Nk);
+int tc_choose_rows(int ksize, int B, int H, int W, int num_sms);
+cudaError_t launch_stage_tc(int ksize, StageArgs &a, int B, cudaStream_t s);
 
 // Training-gradient kernels (tnrd_grad.cu); all images dense [B][H][W] unless an ld is given.
 int grad_grid(long long n, int num_sms);

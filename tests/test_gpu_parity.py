@@ -45,8 +45,8 @@ def P():
     return P
 
 
-def _gpu_denoise(P, torch, model, f, boundary=0, peak=None, phi_mode=0, reaction=0):
-    eng = P.TNRD(model, boundary=boundary, phi_mode=phi_mode, reaction=reaction)
+def _gpu_denoise(P, torch, model, f, boundary=0, peak=None, phi_mode=0, reaction=0, engine=0):
+    eng = P.TNRD(model, boundary=boundary, phi_mode=phi_mode, reaction=reaction, engine=engine)
     ft = torch.from_numpy(np.ascontiguousarray(f, np.float32)).cuda()
     u = eng.denoise(ft, peak=peak)
     torch.cuda.synchronize()
@@ -74,6 +74,24 @@ def test_full_config_parity(torch_cuda, P, cfg):
     u_ref = oracle.denoise(p.f[0], p.model)
     u = _gpu_denoise(P, torch_cuda, p.model, p.f, peak=p.peaks)[0]
     _assert_parity(u, u_ref, float(p.peaks[0]), p.clean[0], f"C{cfg}")
+
+
+@pytest.mark.parametrize("engine", ["fp32", "tensor"])
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_engine_parity(torch_cuda, P, cfg, engine):
+    """Both engines (tnrd_engine) against the oracle on C1-C3, every pixel, and the
+    tensor-core engine is the one AUTO picks for these (ksize, N_k) under R1."""
+    p = make_problem(cfg)
+    e = P.ENGINE_FP32 if engine == "fp32" else P.ENGINE_TENSOR
+    eng = P.TNRD(p.model, engine=e)
+    assert eng.engine_for(1, *p.f.shape[1:]) == e
+    eng.close()
+    auto = P.TNRD(p.model)
+    assert auto.engine_for(1, *p.f.shape[1:]) == P.ENGINE_TENSOR
+    auto.close()
+    u_ref = oracle.denoise(p.f[0], p.model)
+    u = _gpu_denoise(P, torch_cuda, p.model, p.f, peak=p.peaks, engine=e)[0]
+    _assert_parity(u, u_ref, float(p.peaks[0]), p.clean[0], f"C{cfg} engine={engine}")
 
 
 @pytest.mark.parametrize("cfg", [1, 2])
