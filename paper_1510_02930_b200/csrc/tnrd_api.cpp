@@ -218,7 +218,7 @@ tnrd_status launch_one(tnrd_handle *h, int t, const Plan &plan, StageArgs &a, in
     a.mode = h->mode[t];
     if (plan.tc_oh > 0) {
         a.params = h->d_tc + (size_t)t * h->tc_stride;
-        a.pstride = tnrd::tc_phi_stride(h->d.n_rbf);
+        a.pstride = tnrd::tc_pair_stride(h->d.n_rbf);
         a.tc_par_floats = h->tc_stride;
         a.tc_oh = plan.tc_oh;
     }
@@ -420,7 +420,7 @@ float tf32_rn_host(float x) {
 
 void pack_tc_stage(const tnrd_desc &d, const float *filters, const float *phi_host, int ps, float *out) {
     const int K = d.ksize, Nk = d.n_filters, M = d.n_rbf, KT = K * K;
-    const int KTP = tnrd::tc_ktp(K), NZ = tnrd::tc_nz(K), PST = tnrd::tc_phi_stride(M);
+    const int KTP = tnrd::tc_ktp(K), NZ = tnrd::tc_nz(K), PPS = tnrd::tc_pair_stride(M), NB = (M + 7) / 8;
     std::memset(out, 0, sizeof(float) * tnrd::tc_par_floats(K, Nk, M));
     float *bf_hi = out, *bf_lo = out + (size_t)Nk * KTP;
     float *ba_hi = out + 2 * (size_t)Nk * KTP, *ba_lo = ba_hi + (size_t)NZ * Nk;
@@ -434,9 +434,30 @@ void pack_tc_stage(const tnrd_desc &d, const float *filters, const float *phi_ho
             ba_hi[tnrd::tc_b_index(t, n, Nk)] = hi;
             ba_lo[tnrd::tc_b_index(t, n, Nk)] = lo;
         }
-    const int nfl = tnrd::kFc + ((M + 7) / 8) * tnrd::kHornerUnit;
-    for (int n = 0; n < Nk; ++n)
-        std::memcpy(phi + (size_t)n * PST, phi_host + (size_t)n * ps + tnrd::tap_floats(K), sizeof(float) * nfl);
+    // phi of filter pairs, interleaved (tnrd_internal.h); units NB..2NB-1 stay 0.
+    // Warp unit range (FP32 engine, phi_x2): u0 = ceil((a_s vmin + ct0 - kWindow) / (8 sg)),
+    // u1 = floor((a_s vmax + ct0 + kCutT + 0.01) / (8 sg)), folded into one fma each;
+    // the fp32 rounding of the folded constants (~1e-6 units) is far inside the
+    // margins of kWindow (0.025 in t) and of the cut (0.0099 in t).
+    for (int p = 0; p < Nk / 2; ++p) {
+        float *q = phi + (size_t)p * PPS;
+        for (int h = 0; h < 2; ++h) {
+            const float *fc = phi_host + (size_t)(2 * p + h) * ps + tnrd::tap_floats(K);
+            const float *units = fc + tnrd::kFc;
+            const double inv = fc[2], a_s = fc[0], ct0 = units[0];
+            q[0 + h] = fc[0];                                   // a_s
+            q[2 + h] = fc[1];                                   // two_sg
+            q[4 + h] = (float)(a_s * inv);                      // A
+            q[6 + h] = (float)((ct0 - (double)tnrd::kWindow) * inv);       // B0
+            q[8 + h] = (float)((ct0 + (double)tnrd::kCutT + 0.01) * inv);  // B1
+            q[10 + h] = fc[4];                                  // yrmax
+            int nbi = NB;                                       // NB as int bits
+            std::memcpy(&q[12], &nbi, 4);
+            for (int b = 0; b < NB; ++b)
+                for (int e = 0; e < 9; ++e)  // ct, c0..c7
+                    q[tnrd::kTcPairHdr + b * tnrd::kTcPairUnit + 2 * e + h] = units[b * tnrd::kHornerUnit + e];
+        }
+    }
 }
 
 }  // namespace

@@ -98,11 +98,7 @@ __device__ __forceinline__ float reaction_step(int kind, float u, float ut, floa
     return prox_poisson(ut, lam, f);
 }
 
-// Per-lane left cut of the Horner units: a lane with t < -kCutT
-// sees only block terms below 2^-30.25 of their weight, so G's exponent is pushed
-// below -126 there (an exact zero, decided per lane, so skipping stays warp-
-// independent); bitwise unchanged where the cut does not bind.
-constexpr float kCutT = 5.5f, kCutBig = 1048576.0f;
+
 
 }  // namespace
 }  // namespace tnrd

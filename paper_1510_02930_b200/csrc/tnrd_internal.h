@@ -52,6 +52,11 @@ constexpr int kHornerUnit = 12;
 constexpr int kDirectUnit = 4;
 constexpr int kFc = 8;                // floats of per-filter constants
 constexpr float kWindow = 11.25f;     // > sqrt(126): all nonzero G lie inside
+// Per-lane left cut of the Horner units: a lane with t < -kCutT
+// sees only block terms below 2^-30.25 of their weight, so G's exponent is pushed
+// below -126 there (an exact zero, decided per lane, so skipping stays warp-
+// independent); bitwise unchanged where the cut does not bind.
+constexpr float kCutT = 5.5f, kCutBig = 1048576.0f;
 
 
 __host__ __device__ constexpr int tap_pitch(int K) { return (K + 3) / 4 * 4; }
@@ -104,14 +109,21 @@ cudaError_t launch_copy_rows(const float *src, long long src_ld, float *dst, lon
 // Stage operand block (floats), built by the host (tnrd_api.cpp, pack_tc_stage):
 //   bf_hi, bf_lo [Nk x KTP]  k_i taps, UMMA K-major no-swizzle layout (tc_b_index)
 //   ba_hi, ba_lo [NZ x Nk]   the same taps transposed (tap-major rows)
-//   phi          [Nk][tc_phi_stride(M)]  {fc[8], NB Horner units, one zero unit}
+//   phi  [Nk/2][tc_pair_stride(M)]  Horner phi of filter pairs (2p, 2p+1), each
+//        value interleaved {filter 2p, filter 2p+1} so that every constant pair is
+//        one aligned 64-bit operand of fma.rn.f32x2:
+//          header {a_s, a_s', two_sg, two_sg'} {A, A', B0, B0'} {B1, B1', yrmax, yrmax'} {NB, 0, 0, 0}
+//            (unit range of a warp: u0 = ceil(A vmin + B0), u1 = floor(A vmax + B1))
+//          unit b {ct, ct', c0, c0'} {c1, c1', c2, c2'} {c3, c3', c4, c4'} {c5, c5', c6, c6'} {c7, c7', 0, 0}
+//        for b = 0..NB-1, then NB all-zero units (so u0 + j needs no bound check).
 // KTP = roundup(k*k, 8) (GEMM K of the forward bank), NZ = max(16, KTP).
-constexpr int kTcVW = 64;   // v-region columns per tile (an M = 128 block is two rows)
+constexpr int kTcVW = 64;       // v-region columns per tile (an M = 128 block is two rows)
+constexpr int kTcPairHdr = 16, kTcPairUnit = 20;
 __host__ __device__ constexpr int tc_ktp(int K) { return (K * K + 7) / 8 * 8; }
 __host__ __device__ constexpr int tc_nz(int K) { return tc_ktp(K) < 16 ? 16 : tc_ktp(K); }
-__host__ __device__ constexpr int tc_phi_stride(int M) { return kFc + ((M + 7) / 8 + 1) * kHornerUnit; }
+__host__ __device__ constexpr int tc_pair_stride(int M) { return kTcPairHdr + 2 * ((M + 7) / 8) * kTcPairUnit; }
 __host__ __device__ constexpr int tc_par_floats(int K, int Nk, int M) {
-    return 2 * Nk * tc_ktp(K) + 2 * tc_nz(K) * Nk + Nk * tc_phi_stride(M);
+    return 2 * Nk * tc_ktp(K) + 2 * tc_nz(K) * Nk + (Nk / 2) * tc_pair_stride(M);
 }
 // element (row n, column k) of a rows x kdim K-major operand (8-row x 4-float core matrices)
 __host__ __device__ constexpr int tc_b_index(int n, int k, int kdim) {

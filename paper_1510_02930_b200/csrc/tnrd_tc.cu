@@ -39,9 +39,13 @@
 namespace tnrd {
 namespace {
 
-constexpr int kNWG = 4;            // warpgroups per CTA; all share the 128 TMEM lanes
-constexpr int kNT = 128 * kNWG;    // 512 threads
-constexpr int kColStride = 128, kColV = 256, kColZ = 384, kTmemCols = 512;
+#ifndef TNRD_TC_PG
+#define TNRD_TC_PG 3
+#endif
+constexpr int kPG = TNRD_TC_PG;    // phi warp groups (4 warps each, one per TMEM lane quarter)
+constexpr int kNT = (4 * kPG + 5) * 32;  // phi warps, 4 build / gather warps, 1 MMA warp
+constexpr int kSlots = 3;          // M-blocks in flight (TMEM slots)
+constexpr int kTmemCols = 512;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -62,6 +66,9 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int N) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 __device__ __forceinline__ void mma_tf32(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+#ifdef TNRD_EXP_NOMMA
+    return;
+#endif
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                  "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
                  "r"(a), "l"(b), "r"(idesc), "r"(acc));
@@ -80,6 +87,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
                      : "memory");
     }
 }
+// floor / ceil of |x| < 2^22 as an int without the XU pipe (F2I): a directed-
+// rounding add of 1.5 * 2^23 leaves the integer in the low mantissa bits
+__device__ __forceinline__ int floor_i(float x) { return __float_as_int(__fadd_rd(x, 12582912.0f)) - 0x4B400000; }
+__device__ __forceinline__ int ceil_i(float x) { return __float_as_int(__fadd_ru(x, 12582912.0f)) - 0x4B400000; }
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -140,64 +152,72 @@ __device__ __forceinline__ void tmem_st(uint32_t addr, const uint32_t (&r)[N]) {
     if constexpr (N % 4 >= 2) tmem_st2(addr + c, r + c);
 }
 
-// phi_i on the pixel pair (block X, block Y) of this thread for NF consecutive
-// filters, in lockstep groups of GF filters.  Per filter: the FP32 engine's
-// blocked-Horner units (tnrd_internal.h) in ascending order over
-// the warp-uniform range (min / max over the warp's 64 pixels); a filter whose
-// range is shorter than its group's runs the extra iterations on its zero unit
-// (index NB, all coefficients 0), which adds exactly 0.  Every w is therefore
-// bitwise the FP32 engine's phi of the same v.  Warp-collective.
-template <int NF>
-__device__ __forceinline__ void phi_pairs(const float *__restrict__ s_phi, int pst, const f2 (&v)[NF],
-                                          f2 (&w)[NF]) {
-    constexpr int GF = (NF % 4 == 0) ? 4 : 2;
+// phi of NP filter pairs (2p, 2p+1) on this thread's pixel: v[2p], v[2p+1] are
+// the two responses, evaluated together in packed fp32x2 with the interleaved pair
+// constants (tnrd_internal.h), so every constant is an aligned 64-bit operand.  Per
+// filter: the FP32 engine's blocked-Horner units in ascending
+// order.  A pair runs the union of its two filters' warp-uniform unit ranges (min /
+// max over the warp's 32 pixels) and pairs run in lockstep groups of GP: a pair
+// runs units u0 + j for j < nmax, past its own range into real units outside it or
+// into the zero units NB..2NB-1.  A unit outside a filter's own range is exactly 0
+// for every lane (the FP32 engine skips it for that reason), so each w is bitwise
+// the FP32 engine's phi of the same v.  Warp-collective.
+template <int NP>
+__device__ __forceinline__ void phi_fpairs(const float *__restrict__ s_pp, int pps, const uint32_t (&vr)[2 * NP],
+                                           f2 (&w)[NP]) {
+#ifndef TNRD_TC_GP
+#define TNRD_TC_GP 2
+#endif
+    constexpr int GP = NP % TNRD_TC_GP == 0 ? TNRD_TC_GP : (NP % 2 == 0 ? 2 : 1);
 #pragma unroll
-    for (int g = 0; g < NF; g += GF) {
-        int u0[GF], nu[GF], zu[GF];
-        float as[GF], tsg[GF], yrm[GF];
-        const float *units[GF];
+    for (int g = 0; g < NP; g += GP) {
+        f2 vv[GP], as2[GP], tsg2[GP];
+        float yra[GP], yrb[GP];
+        const char *up[GP];
         int nmax = 0;
 #pragma unroll
-        for (int f = 0; f < GF; ++f) {
-            const float *fp = s_phi + (g + f) * pst;
-            const float4 fc = *reinterpret_cast<const float4 *>(fp);
-            const float4 fd = *reinterpret_cast<const float4 *>(fp + 4);
-            const int nb = __float2int_rn(fc.w);
-            as[f] = fc.x;
-            tsg[f] = fc.y;
-            yrm[f] = fd.x;
-            units[f] = fp + kFc;
-            const float cs0 = fp[kFc];
-            const float vmin = fminf(lo(v[g + f]), hi(v[g + f])), vmax = fmaxf(lo(v[g + f]), hi(v[g + f]));
-            const float ylo = warp_min(fmaf(fc.x, vmin, cs0)), yhi = warp_max(fmaf(fc.x, vmax, cs0));
-            u0[f] = max(0, __float2int_ru((ylo - kWindow) * fc.z));
-            const int u1 = min(nb - 1, __float2int_rd((yhi + kCutT + 0.01f) * fc.z));
-            nu[f] = u1 - u0[f] + 1;
-            zu[f] = nb;
-            nmax = max(nmax, nu[f]);
-            w[g + f] = 0ull;
+        for (int p = 0; p < GP; ++p) {
+            const float *hp = s_pp + (g + p) * pps;
+            const float4 h0 = *reinterpret_cast<const float4 *>(hp);       // a_s, two_sg
+            const ulonglong2 h1 = *reinterpret_cast<const ulonglong2 *>(hp + 4);  // {A}, {B0}
+            const float4 h2 = *reinterpret_cast<const float4 *>(hp + 8);   // B1, yrmax
+            const int nb = __float_as_int(hp[12]);
+            const float va = __uint_as_float(vr[2 * (g + p)]), vb = __uint_as_float(vr[2 * (g + p) + 1]);
+            vv[p] = pk(va, vb);
+            as2[p] = pk(h0.x, h0.y);
+            tsg2[p] = pk(h0.z, h0.w);
+            yra[p] = h2.z;
+            yrb[p] = h2.w;
+            const f2 lo2 = fma2(pk(warp_min(va), warp_min(vb)), h1.x, h1.y);
+            const f2 hi2 = fma2(pk(warp_max(va), warp_max(vb)), h1.x, pk(h2.x, h2.y));
+            const int u0 = max(0, min(ceil_i(lo(lo2)), ceil_i(hi(lo2))));
+            const int u1 = min(nb - 1, max(floor_i(lo(hi2)), floor_i(hi(hi2))));
+            up[p] = reinterpret_cast<const char *>(hp + kTcPairHdr) + u0 * (4 * kTcPairUnit);
+            nmax = max(nmax, u1 - u0 + 1);
+            w[g + p] = 0ull;
         }
         for (int j = 0; j < nmax; ++j) {
 #pragma unroll
-            for (int f = 0; f < GF; ++f) {
-                const int u = j < nu[f] ? u0[f] + j : zu[f];
-                const float4 *up = reinterpret_cast<const float4 *>(units[f] + u * kHornerUnit);
-                const float4 q0 = up[0], q1 = up[1], q2 = up[2];
-                // q0 = {ct, c0, c1, c2}, q1 = {c3, c4, c5, c6}, q2 = {c7, ...}
-                const f2 t = fma2(v[g + f], bc(as[f]), bc(q0.x));
+            for (int p = 0; p < GP; ++p) {
+                const ulonglong2 *qp = reinterpret_cast<const ulonglong2 *>(up[p]);
+                up[p] += 4 * kTcPairUnit;
+                const ulonglong2 q0 = qp[0], q1 = qp[1], q2 = qp[2], q3 = qp[3];
+                const unsigned long long c7 = reinterpret_cast<const unsigned long long *>(qp + 4)[0];
+                // q0 = {ct, c0}, q1 = {c1, c2}, q2 = {c3, c4}, q3 = {c5, c6}  (pairs)
+                const f2 t = fma2(vv[p], as2[p], q0.x);
                 const f2 q = fma2(t, bc(-kCutBig), bc(-kCutBig * kCutT));
                 const f2 sq = fma2(t, t, pk(fmaxf(lo(q), 0.0f), fmaxf(hi(q), 0.0f)));
                 const f2 G = pk(ex2_ftz(-lo(sq)), ex2_ftz(-hi(sq)));
-                const f2 yr = mul2(t, bc(tsg[f]));
-                const f2 Rr = pk(ex2_ftz(fminf(lo(yr), yrm[f])), ex2_ftz(fminf(hi(yr), yrm[f])));
-                f2 h = fma2(Rr, bc(q2.x), bc(q1.w));
-                h = fma2(h, Rr, bc(q1.z));
-                h = fma2(h, Rr, bc(q1.y));
-                h = fma2(h, Rr, bc(q1.x));
-                h = fma2(h, Rr, bc(q0.w));
-                h = fma2(h, Rr, bc(q0.z));
-                h = fma2(h, Rr, bc(q0.y));
-                w[g + f] = fma2(G, h, w[g + f]);
+                const f2 yr = mul2(t, tsg2[p]);
+                const f2 Rr = pk(ex2_ftz(fminf(lo(yr), yra[p])), ex2_ftz(fminf(hi(yr), yrb[p])));
+                f2 h = fma2(Rr, c7, q3.y);
+                h = fma2(h, Rr, q3.x);
+                h = fma2(h, Rr, q2.y);
+                h = fma2(h, Rr, q2.x);
+                h = fma2(h, Rr, q1.y);
+                h = fma2(h, Rr, q1.x);
+                h = fma2(h, Rr, q0.y);
+                w[g + p] = fma2(G, h, w[g + p]);
             }
         }
     }
@@ -209,48 +229,68 @@ struct TcGeo {
     static constexpr int KTP = tc_ktp(K), NZ = tc_nz(K);
     static constexpr int OW = kTcVW - 2 * R;   // output columns per tile
     static constexpr int UW = kTcVW + 2 * R;   // u tile columns
-    static constexpr int NFW = NK / kNWG;      // filters per warpgroup in phi
+    static constexpr int PG = (NK % (2 * kPG) == 0) ? kPG : 2;  // phi groups used
+    static constexpr int NFW = NK / PG;        // filters per phi warp
     static constexpr int NCH = KTP / 8;        // 8-column chunks of an im2col row
+    static constexpr int NZC = NZ / 8;         // 8-column chunks of a Z row
+    static constexpr int SLOT = 2 * (KTP > NK ? KTP : NK);   // A / W columns of a slot
     static_assert(NK % 8 == 0 && NK <= 64 && NFW % 2 == 0, "N_k: multiple of 8, at most 64");
-    static_assert(2 * KTP <= kColStride && 2 * NK <= kColStride && NK <= 64 && NZ <= 64, "TMEM column plan");
+    static_assert(kSlots * (SLOT + (NK > NZ ? NK : NZ)) <= kTmemCols, "TMEM column plan");
 };
 
 __host__ __device__ constexpr int round4(int x) { return (x + 3) / 4 * 4; }
 
-// Shared memory: operand block, u tile, Z of a super-block [KT][256], d [OH][OW],
-// mbarrier + TMEM address.
+// Shared memory: operand block, u tile, d [OH][OW], Z of one M-block [KT][128],
+// 4 x kSlots mbarriers + TMEM address.
 template <int K, int NK>
 __host__ __device__ constexpr int tc_smem_floats(int oh, int par_floats) {
     using G = TcGeo<K, NK>;
-    return par_floats + round4((oh + 4 * G::R) * G::UW) + G::KT * 256 + round4(oh * G::OW) + 4;
+    return par_floats + round4((oh + 4 * G::R) * G::UW) + round4(oh * G::OW) + G::KT * 128 + 8 * kSlots + 4;
 }
 
-// One CTA = one output tile of OW x OH.  The v region (64 x (OH + 2r)) is walked in
-// super-blocks of four rows = two M-blocks, X (rows j0, j0+1) and Y (j0+2, j0+3);
-// TMEM lane m is pixel (j0 + 2b + m/64, m%64) of block b.  Each thread owns lane m
-// of both blocks, so phi runs on pixel pairs {X_m, Y_m} in packed fp32x2 with the
-// coefficients as broadcast scalars (as in the FP32 engine).
-//   TMEM columns (512):  block b: A / W at 128 b (hi, then lo at +KTP or +NK),
-//                        V at 256 + 64 b, Z at 384 + 64 b.
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// One CTA = one output tile of OW x OH.  The v region (64 x (OH + 2r) pixels) is
+// cut into M-blocks of two rows (TMEM lane m = pixel (2i + m/64, m%64) of block i);
+// block i lives in TMEM slot i % 3 (A / W columns, then V / Z columns).  Warp roles,
+// handing blocks over through mbarriers (no CTA-wide barrier until the epilogue):
+//   4 PG phi warps: warp w serves lane quarter w % 4, filters [NFW (w/4), +NFW):
+//               wait V(i), tcgen05.ld, phi, W (hi, lo) -> TMEM, arrive W_full(i)
+//   4 build / gather warps (lane quarter w % 4): im2col A(i) -> TMEM, arrive
+//               A_full(i); wait Z(i), Z -> smem, A(i+3) into the freed slot, then
+//               d += the block's taps (blocks in order: d summed in v-row order)
+//   last warp   lane 0 issues the 3xTF32 MMAs: F(i) on A_full(i) -> V_full(i),
+//               Adj(i) on W_full(i) -> Z_full(i), in the order F(0..2), Adj(0),
+//               F(3), Adj(1), F(4), ...
 template <int K, int NK>
 __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant__ StageArgs a) {
     using G = TcGeo<K, NK>;
     constexpr int R = G::R, KT = G::KT, KTP = G::KTP, NZ = G::NZ, OW = G::OW, UW = G::UW, NFW = G::NFW;
-    constexpr int NCH = G::NCH;
+    constexpr int NCH = G::NCH, NZC = G::NZC, SLOT = G::SLOT, PG = G::PG;
+    constexpr int WBG = 4 * kPG, WMMA = WBG + 4;   // first build / gather warp, MMA warp
+    constexpr int VZ0 = kSlots * SLOT, VZW = NK > NZ ? NK : NZ;  // V / Z columns of slot s at VZ0 + VZW s
+    constexpr int BAR_BG = 1;
     extern __shared__ __align__(1024) float4 smem4[];
     float *s_par = reinterpret_cast<float *>(smem4);
     const float *s_bf = s_par;                       // hi [NK x KTP], lo after it
     const float *s_ba = s_par + 2 * NK * KTP;        // hi [NZ x NK], lo after it
-    const float *s_phi = s_ba + 2 * NZ * NK;         // [NK][pst]
+    const float *s_pp = s_ba + 2 * NZ * NK;          // [NK/2][pps] filter-pair phi
     const int OH = a.tc_oh, VH = OH + 2 * R, UH = OH + 4 * R;
     float *s_u = s_par + a.tc_par_floats;
-    float *s_z = s_u + round4(UH * UW);              // [KT][256]
-    float *s_d = s_z + KT * 256;                     // [OH][OW]
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(s_d + round4(OH * OW));
-    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(mbar + 1);
+    float *s_d = s_u + round4(UH * UW);              // [OH][OW]
+    float *s_z = s_d + round4(OH * OW);              // [KT][128]
+    uint64_t *bar_a = reinterpret_cast<uint64_t *>(s_z + KT * 128);   // A_full[kSlots]
+    uint64_t *bar_v = bar_a + kSlots, *bar_w = bar_v + kSlots, *bar_z = bar_w + kSlots;
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(bar_z + kSlots);
 
-    const int tid = threadIdx.x, warp = tid >> 5, wg = tid >> 7, m = tid & 127;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int quarter = warp & 3, m = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const int H = a.H, W = a.W;
 
     // ---- tile
@@ -281,7 +321,12 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+        for (int s = 0; s < kSlots; ++s) {
+            mbar_init(bar_a + s, 128);
+            mbar_init(bar_v + s, 1);
+            mbar_init(bar_w + s, 128 * PG);
+            mbar_init(bar_z + s, 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // operands visible to the MMA (async proxy)
@@ -289,160 +334,146 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *s_tmem;
-    const uint32_t bf_hi = smem_u32(s_bf), bf_lo = bf_hi + 4 * NK * KTP;
-    const uint32_t ba_hi = smem_u32(s_ba), ba_lo = ba_hi + 4 * NZ * NK;
-    constexpr uint32_t SBO_F = (KTP / 4) * 128, SBO_A = (NK / 4) * 128;
-    const int pst = a.pstride;
-    const uint32_t tl = tmem + lane_off;  // this warp's lanes
+    const uint32_t tl = tmem + lane_off;
+    const int nmb = VH / 2;
 
-    // MMA issue (thread 0) and completion: thread 0 waits on the mbarrier, the CTA
-    // on a hardware barrier (no spinning warps).
-    uint32_t phase = 0;
-    const auto mma_wait_all = [&]() {
-        if (tid == 0) mbar_wait(mbar, phase);
-        phase ^= 1;
-        __syncthreads();
-        tc_fence_after();
-    };
-
-    const int nsb = (VH + 3) / 4;
-    for (int sb = 0; sb < nsb; ++sb) {
-        const int j0 = 4 * sb;
-        // (1) im2col rows (hi, lo) of pixel m of blocks X and Y.  v-region pixel
-        // (j, c) uses its mirror in the image (R1), clamped into the tile for pixels
-        // no output needs.  Chunk task k = (block, 8-tap chunk) goes to warpgroup k % 4.
-        {
-            const float *up[2];
+    if (warp < 4 * PG) {
+        // ======================= phi warps
+        const int h = warp >> 2;
+        const int pps = a.pstride;
+        for (int i = 0; i < nmb; ++i) {
+            const int s = i % kSlots;
+            mbar_wait(bar_v + s, (i / kSlots) & 1);
+            tc_fence_after();
+            uint32_t vr[NFW];
+            tmem_ld_nowait<NFW>(tl + VZ0 + VZW * s + h * NFW, vr);
+            tmem_wait_ld(vr);
+            f2 w[NFW / 2];
+#ifdef TNRD_EXP_NOPHI
 #pragma unroll
-            for (int blk = 0; blk < 2; ++blk) {
-                const int j = j0 + 2 * blk + (m >> 6), c = m & 63;
-                const int gy = reflect(y0 - R + j, H), gx = reflect(x0 - R + c, W);
-                const int pj = min(max(gy - y0 + R, 0), VH - 1);
-                const int pc = min(max(gx - x0 + R, 0), kTcVW - 1);
-                up[blk] = s_u + (pj + 2 * R) * UW + pc + 2 * R;  // tap (ta, tb) reads up[-ta*UW - tb]
+            for (int e = 0; e < NFW / 2; ++e) w[e] = pk(__uint_as_float(vr[2 * e]), __uint_as_float(vr[2 * e + 1]));
+#else
+            phi_fpairs<NFW / 2>(s_pp + h * (NFW / 2) * pps, pps, vr, w);
+#endif
+            uint32_t wh[NFW], wl[NFW];
+#pragma unroll
+            for (int e = 0; e < NFW; ++e) {
+                const float x = (e & 1) ? hi(w[e / 2]) : lo(w[e / 2]);
+                const float xh = tf32_rn(x);
+                wh[e] = __float_as_uint(xh);
+                wl[e] = __float_as_uint(x - xh);
             }
+            tmem_st<NFW>(tl + SLOT * s + h * NFW, wh);
+            tmem_st<NFW>(tl + SLOT * s + NK + h * NFW, wl);
+            tc_wait_st();
+            tc_fence_before();
+            mbar_arrive(bar_w + s);
+        }
+    } else if (warp < WBG) {
+        // phi warps of an unused group (N_k not divisible): idle until the epilogue
+    } else if (warp < WMMA) {
+        // ======================= build / gather warps
+        const auto build = [&](int i) {
+            // im2col row (hi, lo) of pixel m of block i: v-region (j, c) uses its mirror
+            // in the image (R1), clamped into the tile for pixels no output needs
+            const int s = i % kSlots;
+            const int j = 2 * i + (m >> 6), c = m & 63;
+            const int gy = reflect(y0 - R + j, H), gx = reflect(x0 - R + c, W);
+            const int pj = min(max(gy - y0 + R, 0), VH - 1);
+            const int pc = min(max(gx - x0 + R, 0), kTcVW - 1);
+            const float *up = s_u + (pj + 2 * R) * UW + pc + 2 * R;  // tap (ta, tb) reads up[-ta*UW - tb]
 #pragma unroll
-            for (int k = 0; k < 2 * NCH; ++k) {
-                if (k % kNWG != wg) continue;
-                const int blk = k / NCH, ch = k % NCH;
-                uint32_t h[8], l[8];
+            for (int ch = 0; ch < NCH; ++ch) {
+                uint32_t hv[8], lv[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     const int t = ch * 8 + e;
                     float x = 0.0f;
-                    if (t < KT) x = up[blk][-(t / K) * UW - (t % K)];
+                    if (t < KT) x = up[-(t / K) * UW - (t % K)];
                     const float xh = tf32_rn(x);
-                    h[e] = __float_as_uint(xh);
-                    l[e] = __float_as_uint(x - xh);
+                    hv[e] = __float_as_uint(xh);
+                    lv[e] = __float_as_uint(x - xh);
                 }
-                tmem_st8(tl + kColStride * blk + ch * 8, h);
-                tmem_st8(tl + kColStride * blk + KTP + ch * 8, l);
+                tmem_st8(tl + SLOT * s + ch * 8, hv);
+                tmem_st8(tl + SLOT * s + KTP + ch * 8, lv);
             }
-        }
-        tc_wait_st();
-        tc_fence_before();
-        __syncthreads();
-        // (2) forward bank, both blocks: V = A_lo B_hi + A_hi B_lo + A_hi B_hi
-        if (tid == 0) {
+            tc_wait_st();
+            tc_fence_before();
+            mbar_arrive(bar_a + s);
+        };
+        for (int i = 0; i < kSlots && i < nmb; ++i) build(i);
+        const int gt = tid - 32 * WBG;  // 0..127
+        for (int i = 0; i < nmb; ++i) {
+            const int s = i % kSlots;
+            mbar_wait(bar_z + s, (i / kSlots) & 1);
             tc_fence_after();
-            constexpr uint32_t id = idesc_tf32(NK);
+            named_sync(BAR_BG, 128);  // every BG thread is done with gather(i - 1)
 #pragma unroll
-            for (int blk = 0; blk < 2; ++blk) {
-                const uint32_t tA = tmem + kColStride * blk, tV = tmem + kColV + 64 * blk;
+            for (int ch = 0; ch < NZC; ++ch) {
+                if (ch * 8 >= KT) continue;
+                uint32_t z[8];
+                tmem_ld_nowait<8>(tl + VZ0 + VZW * s + ch * 8, z);
+                tmem_wait_ld(z);
 #pragma unroll
-                for (int s = 0; s < KTP / 8; ++s) {
-                    mma_tf32(tV, tA + KTP + 8 * s, umma_desc(bf_hi + 256 * s, SBO_F), id, s > 0);
-                    mma_tf32(tV, tA + 8 * s, umma_desc(bf_lo + 256 * s, SBO_F), id, 1);
-                    mma_tf32(tV, tA + 8 * s, umma_desc(bf_hi + 256 * s, SBO_F), id, 1);
-                }
+                for (int e = 0; e < 8; ++e)
+                    if (ch * 8 + e < KT) s_z[(ch * 8 + e) * 128 + m] = __uint_as_float(z[e]);
             }
-            mma_commit(mbar);
-        }
-        mma_wait_all();
-        // (3) phi of this warpgroup's filters on the pixel pairs; w (hi, lo) of each
-        // block over its dead im2col columns
-        {
-            uint32_t vx[NFW], vy[NFW];
-            tmem_ld_nowait<NFW>(tl + kColV + wg * NFW, vx);
-            tmem_ld_nowait<NFW>(tl + kColV + 64 + wg * NFW, vy);
-            tmem_wait_ld(vx);
-            tmem_wait_ld(vy);
-            f2 v[NFW], w[NFW];
+            tc_fence_before();
+            if (i + kSlots < nmb) build(i + kSlots);  // slot s is free: W(i) consumed, Z(i) read
+            named_sync(BAR_BG, 128);
+            // d(y, x) += sum_b Z[(y + a, x + b)][a K + b] over rows 2i, 2i + 1 (v row y + a)
+            const int j0 = 2 * i;
+            for (int it = gt; it < (K + 1) * OW; it += 128) {
+                const int y = j0 - (K - 1) + it / OW, x = it % OW;
+                if (y < 0 || y >= OH) continue;
+                float d = s_d[y * OW + x];
 #pragma unroll
-            for (int e = 0; e < NFW; ++e) v[e] = pk(__uint_as_float(vx[e]), __uint_as_float(vy[e]));
-#ifdef TNRD_EXP_NOPHI
+                for (int jj = 0; jj < 2; ++jj) {
+                    const int ta = j0 + jj - y;
+                    if (ta < 0 || ta >= K) continue;
+                    const float *zp = s_z + (ta * K) * 128 + jj * 64 + x;
+                    float S = 0.0f;
 #pragma unroll
-            for (int e = 0; e < NFW; ++e) w[e] = v[e];
-#else
-            phi_pairs<NFW>(s_phi + wg * NFW * pst, pst, v, w);
-#endif
-#pragma unroll
-            for (int blk = 0; blk < 2; ++blk) {
-                uint32_t wh[NFW], wl[NFW];
-#pragma unroll
-                for (int e = 0; e < NFW; ++e) {
-                    const float x = blk ? hi(w[e]) : lo(w[e]);
-                    const float xh = tf32_rn(x);
-                    wh[e] = __float_as_uint(xh);
-                    wl[e] = __float_as_uint(x - xh);
+                    for (int tb = 0; tb < K; ++tb) S += zp[tb * 128 + tb];
+                    d += S;
                 }
-                tmem_st<NFW>(tl + kColStride * blk + wg * NFW, wh);
-                tmem_st<NFW>(tl + kColStride * blk + NK + wg * NFW, wl);
+                s_d[y * OW + x] = d;
             }
         }
-        tc_wait_st();
-        tc_fence_before();
-        __syncthreads();
-        // (4) adjoint bank, both blocks: Z = W_lo B_hi + W_hi B_lo + W_hi B_hi
-        if (tid == 0) {
+    } else if (lane == 0) {
+        // ======================= MMA issuer (one thread)
+        const uint32_t bf_hi = smem_u32(s_bf), bf_lo = bf_hi + 4 * NK * KTP;
+        const uint32_t ba_hi = smem_u32(s_ba), ba_lo = ba_hi + 4 * NZ * NK;
+        constexpr uint32_t SBO_F = (KTP / 4) * 128, SBO_A = (NK / 4) * 128;
+        constexpr uint32_t id_f = idesc_tf32(NK), id_a = idesc_tf32(NZ);
+        const auto fwd = [&](int i) {  // V = A_lo B_hi + A_hi B_lo + A_hi B_hi
+            const int s = i % kSlots;
+            mbar_wait(bar_a + s, (i / kSlots) & 1);
             tc_fence_after();
-            constexpr uint32_t id = idesc_tf32(NZ);
+            const uint32_t tA = tmem + SLOT * s, tV = tmem + VZ0 + VZW * s;
 #pragma unroll
-            for (int blk = 0; blk < 2; ++blk) {
-                const uint32_t tW = tmem + kColStride * blk, tZ = tmem + kColZ + 64 * blk;
-#pragma unroll
-                for (int s = 0; s < NK / 8; ++s) {
-                    mma_tf32(tZ, tW + NK + 8 * s, umma_desc(ba_hi + 256 * s, SBO_A), id, s > 0);
-                    mma_tf32(tZ, tW + 8 * s, umma_desc(ba_lo + 256 * s, SBO_A), id, 1);
-                    mma_tf32(tZ, tW + 8 * s, umma_desc(ba_hi + 256 * s, SBO_A), id, 1);
-                }
+            for (int k = 0; k < KTP / 8; ++k) {
+                mma_tf32(tV, tA + KTP + 8 * k, umma_desc(bf_hi + 256 * k, SBO_F), id_f, k > 0);
+                mma_tf32(tV, tA + 8 * k, umma_desc(bf_lo + 256 * k, SBO_F), id_f, 1);
+                mma_tf32(tV, tA + 8 * k, umma_desc(bf_hi + 256 * k, SBO_F), id_f, 1);
             }
-            mma_commit(mbar);
-        }
-        mma_wait_all();
-        // (5) Z -> smem [tap][pixel of the super-block], then for every output pixel
-        // d(y, x) += sum_b Z[(y + a, x + b)][a K + b] for the super-block's rows, a
-        // ascending (rows in order), b ascending
+            mma_commit(bar_v + s);
+        };
+        for (int i = 0; i < kSlots && i < nmb; ++i) fwd(i);
+        for (int i = 0; i < nmb; ++i) {  // Z = W_lo B_hi + W_hi B_lo + W_hi B_hi
+            const int s = i % kSlots;
+            mbar_wait(bar_w + s, (i / kSlots) & 1);
+            tc_fence_after();
+            const uint32_t tW = tmem + SLOT * s, tZ = tmem + VZ0 + VZW * s;
 #pragma unroll
-        for (int k = 0; k < 2 * (NZ / 8); ++k) {
-            if (k % kNWG != wg) continue;
-            const int blk = k / (NZ / 8), ch = k % (NZ / 8);
-            if (ch * 8 >= KT) continue;
-            uint32_t z[8];
-            tmem_ld_nowait<8>(tl + kColZ + 64 * blk + ch * 8, z);
-            tmem_wait_ld(z);
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-                if (ch * 8 + e < KT) s_z[(ch * 8 + e) * 256 + 128 * blk + m] = __uint_as_float(z[e]);
-        }
-        __syncthreads();
-        for (int it = tid; it < (K + 3) * OW; it += kNT) {
-            const int y = j0 - (K - 1) + it / OW, x = it % OW;
-            if (y < 0 || y >= OH) continue;
-            float d = s_d[y * OW + x];
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-                const int ta = j0 + jj - y;
-                if (ta < 0 || ta >= K) continue;
-                const float *zp = s_z + (ta * K) * 256 + jj * 64 + x;
-                float S = 0.0f;
-#pragma unroll
-                for (int tb = 0; tb < K; ++tb) S += zp[tb * 256 + tb];
-                d += S;
+            for (int k = 0; k < NK / 8; ++k) {
+                mma_tf32(tZ, tW + NK + 8 * k, umma_desc(ba_hi + 256 * k, SBO_A), id_a, k > 0);
+                mma_tf32(tZ, tW + 8 * k, umma_desc(ba_lo + 256 * k, SBO_A), id_a, 1);
+                mma_tf32(tZ, tW + 8 * k, umma_desc(ba_hi + 256 * k, SBO_A), id_a, 1);
             }
-            s_d[y * OW + x] = d;
+            mma_commit(bar_z + s);
+            if (i + kSlots < nmb) fwd(i + kSlots);
         }
-        // the next super-block writes s_z / s_d only after two more CTA barriers
     }
     __syncthreads();
 
@@ -472,7 +503,14 @@ cudaError_t launch_tc(StageArgs &a, int B, cudaStream_t s) {
     using G = TcGeo<K, NK>;
     auto kern = tc_stage_kernel<K, NK>;
     if (a.tc_oh <= 0 || a.tc_oh % 2 != 0) return cudaErrorInvalidValue;
-    const size_t smem = sizeof(float) * (size_t)tc_smem_floats<K, NK>(a.tc_oh, a.tc_par_floats);
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    size_t smem = sizeof(float) * (size_t)tc_smem_floats<K, NK>(a.tc_oh, a.tc_par_floats);
+    while (smem > (size_t)optin && a.tc_oh > 8) {  // fewer rows per tile until it fits
+        a.tc_oh -= 8;
+        smem = sizeof(float) * (size_t)tc_smem_floats<K, NK>(a.tc_oh, a.tc_par_floats);
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     a.tiles_x = (a.W + G::OW - 1) / G::OW;
