@@ -12,11 +12,14 @@
 //                 d(p)    = sum_t Z[p + tap(t)][t]  (col2im gather = kbar_i * w_i, P l.309-311)
 //   reaction      u+ = prox(u - d)                 (P Eq.12, l.318-322)
 //
-// 3xTF32: every fp32 operand x is split as x = hi + lo with hi = tf32(x) (round to
-// nearest) and the GEMM accumulates A_lo B_hi + A_hi B_lo + A_hi B_hi in fp32 TMEM,
-// dropping only A_lo B_lo (< 2^-22 relative).  Measured on B200 (tools/tc_probe.cu):
+// 3xTF32: every fp32 operand x is split as x = hi + lo (hi: TF32, x - hi exact in
+// fp32) and the GEMM accumulates A_lo B_hi + A_hi B_lo + A_hi B_hi in fp32 TMEM,
+// dropping A_lo B_lo.  Taps (B) are split on the host with round-to-nearest (|lo| <=
+// 2^-11 |x|), data (A: u, w) here by truncation (one LOP3; |lo| < 2^-10 |x|), so
+// each product is exact to < 2^-20 relative.  Measured on B200 (tools/tc_probe.cu):
 // 3e-7 of sum |products| against 3e-4 for plain TF32, which fails the 1e-4 peak
-// tolerance by 30x.
+// tolerance by 30x; an fp32 emulation of the whole pass with this split stays at
+// 0.04-0.06 of the tolerance on C4/C5 windows, as fp32 does.
 //
 // Data flow per tile (output OW x OH, v region 64 x (OH + 2r), u region + 2r):
 // the v region is cut into M-blocks of two 64-pixel rows.  TMEM lane m = pixel m
@@ -40,19 +43,19 @@ namespace tnrd {
 namespace {
 
 #ifndef TNRD_TC_PG
-#define TNRD_TC_PG 3
+#define TNRD_TC_PG 4
 #endif
 constexpr int kPG = TNRD_TC_PG;    // phi warp groups (4 warps each, one per TMEM lane quarter)
 constexpr int kNT = (4 * kPG + 5) * 32;  // phi warps, 4 build / gather warps, 1 MMA warp
 constexpr int kSlots = 3;          // M-blocks in flight (TMEM slots)
+constexpr int kZP = 132;           // Z row pitch in smem: a warp spanning two gather rows stays conflict-free
 constexpr int kTmemCols = 512;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-// tf32 round-to-nearest of x (the high 19 bits), as fp32
-__device__ __forceinline__ float tf32_rn(float x) {
-    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
-}
+// high part of the 3xTF32 split of a data operand: x truncated to its high 19 bits
+// (TF32); x - hi is exact in fp32 and |x - hi| < 2^-10 |x|
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 // UMMA shared-memory descriptor, K-major, no swizzle (sm_100 version 1): 8-row x
 // 16-byte core matrices, K-adjacent core matrices 128 B apart (LBO), 8-row groups
@@ -78,12 +81,14 @@ __device__ __forceinline__ void mma_commit(uint64_t *bar) {
                  : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    // try_wait with a suspend-time hint: the thread sleeps until the phase completes
+    // (or the hint expires) instead of spinning on issue slots
     uint32_t done = 0;
     while (!done) {
-        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
                      "selp.u32 %0, 1, 0, p;\n\t}"
                      : "=r"(done)
-                     : "r"(smem_u32(bar)), "r"(parity)
+                     : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
                      : "memory");
     }
 }
@@ -245,7 +250,7 @@ __host__ __device__ constexpr int round4(int x) { return (x + 3) / 4 * 4; }
 template <int K, int NK>
 __host__ __device__ constexpr int tc_smem_floats(int oh, int par_floats) {
     using G = TcGeo<K, NK>;
-    return par_floats + round4((oh + 4 * G::R) * G::UW) + round4(oh * G::OW) + G::KT * 128 + 8 * kSlots + 4;
+    return par_floats + round4((oh + 4 * G::R) * G::UW) + round4(oh * G::OW) + G::KT * kZP + 8 * kSlots + 4;
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
@@ -283,8 +288,8 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
     const int OH = a.tc_oh, VH = OH + 2 * R, UH = OH + 4 * R;
     float *s_u = s_par + a.tc_par_floats;
     float *s_d = s_u + round4(UH * UW);              // [OH][OW]
-    float *s_z = s_d + round4(OH * OW);              // [KT][128]
-    uint64_t *bar_a = reinterpret_cast<uint64_t *>(s_z + KT * 128);   // A_full[kSlots]
+    float *s_z = s_d + round4(OH * OW);              // [KT][kZP]
+    uint64_t *bar_a = reinterpret_cast<uint64_t *>(s_z + KT * kZP);   // A_full[kSlots]
     uint64_t *bar_v = bar_a + kSlots, *bar_w = bar_v + kSlots, *bar_z = bar_w + kSlots;
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(bar_z + kSlots);
 
@@ -359,7 +364,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
 #pragma unroll
             for (int e = 0; e < NFW; ++e) {
                 const float x = (e & 1) ? hi(w[e / 2]) : lo(w[e / 2]);
-                const float xh = tf32_rn(x);
+                const float xh = tf32_hi(x);
                 wh[e] = __float_as_uint(xh);
                 wl[e] = __float_as_uint(x - xh);
             }
@@ -390,7 +395,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
                     const int t = ch * 8 + e;
                     float x = 0.0f;
                     if (t < KT) x = up[-(t / K) * UW - (t % K)];
-                    const float xh = tf32_rn(x);
+                    const float xh = tf32_hi(x);
                     hv[e] = __float_as_uint(xh);
                     lv[e] = __float_as_uint(x - xh);
                 }
@@ -416,7 +421,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
                 tmem_wait_ld(z);
 #pragma unroll
                 for (int e = 0; e < 8; ++e)
-                    if (ch * 8 + e < KT) s_z[(ch * 8 + e) * 128 + m] = __uint_as_float(z[e]);
+                    if (ch * 8 + e < KT) s_z[(ch * 8 + e) * kZP + m] = __uint_as_float(z[e]);
             }
             tc_fence_before();
             if (i + kSlots < nmb) build(i + kSlots);  // slot s is free: W(i) consumed, Z(i) read
@@ -431,10 +436,10 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
                 for (int jj = 0; jj < 2; ++jj) {
                     const int ta = j0 + jj - y;
                     if (ta < 0 || ta >= K) continue;
-                    const float *zp = s_z + (ta * K) * 128 + jj * 64 + x;
+                    const float *zp = s_z + (ta * K) * kZP + jj * 64 + x;
                     float S = 0.0f;
 #pragma unroll
-                    for (int tb = 0; tb < K; ++tb) S += zp[tb * 128 + tb];
+                    for (int tb = 0; tb < K; ++tb) S += zp[tb * kZP + tb];
                     d += S;
                 }
                 s_d[y * OW + x] = d;
