@@ -234,6 +234,8 @@ def main():
                          "(tnrd_loss_grad, P Eq.14-20) on one image of --config (default C3), reported separately")
     ap.add_argument("--phi", default="exact", choices=["exact", "table"],
                     help="exact RBF sum (the headline) or the tabulated variant (reported separately)")
+    ap.add_argument("--engine", default="auto", choices=["auto", "fp32", "tensor"],
+                    help="stage engine (tnrd_set_engine): auto = tensor cores where they apply")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -256,7 +258,8 @@ def main():
     p = make_problem(args.config)
     model = p.model
     B, H, W = p.f.shape
-    eng = P.TNRD(model, device=local, phi_mode=P.PHI_TABLE if args.phi == "table" else P.PHI_EXACT)
+    eng = P.TNRD(model, device=local, phi_mode=P.PHI_TABLE if args.phi == "table" else P.PHI_EXACT,
+                 engine={"auto": P.ENGINE_AUTO, "fp32": P.ENGINE_FP32, "tensor": P.ENGINE_TENSOR}[args.engine])
     stream = torch.cuda.current_stream()
 
     if args.config == 5:
@@ -352,26 +355,57 @@ def main():
         n_sm = props.multi_processor_count
         max_mhz = (clocks or {}).get("sm_max_mhz") or 1965.0
         peak = fp32_peak_tflops(n_sm, max_mhz)
-        flop_launch = (F_TAB if args.phi == "table" else F_ALG)(model.Nk, model.k, model.M) * px_rank
-        achieved = flop_launch / (mean_launch_ms / 1e3) / 1e12 if mean_launch_ms > 0 else None
+        f_px = (F_TAB if args.phi == "table" else F_ALG)(model.Nk, model.k, model.M)
+        flop_launch = f_px * px_rank
+        tensor = eng.engine_for(B if args.config != 5 else 1, H if args.config != 5 else shard[1] - shard[0],
+                                W) == P.ENGINE_TENSOR
         traffic = None
         tf = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tf):
             try:
-                traffic = json.load(open(tf)).get(f"C{args.config}")
+                traffic = json.load(open(tf)).get(f"C{args.config}" + ("/tensor" if tensor else ""))
             except Exception:
                 traffic = None
+        secs = mean_launch_ms / 1e3 if mean_launch_ms > 0 else None
+        if not tensor:
+            achieved = flop_launch / secs / 1e12 if secs else None
+            roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                        "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                        "kernel": "stage_kernel (FP32 engine, one fused TNRD stage)",
+                        "flop_per_px_stage": f_px, "flop_per_launch": flop_launch, "mean_launch_ms": mean_launch_ms,
+                        "peak_source": f"derived: {n_sm} SM x 128 FP32 lanes x 2 x {max_mhz:.0f} MHz "
+                                       "(MEASURED_PEAKS.json has no FP32 figure)"}
+        else:
+            # tensor-core engine: the two filter banks run on the tensor
+            # pipe (3xTF32), everything else on the FP32 pipes.  The bound is the FP32
+            # side: its algorithmic work is F_alg minus the conv flops (the RBF MACs + prox).
+            f_conv = 4 * model.Nk * model.k * model.k
+            f_alu = f_px - f_conv
+            achieved = f_alu * px_rank / secs / 1e12 if secs else None
+            tf32_peak = None
+            mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+            if os.path.exists(mp):
+                tf32_peak = json.load(open(mp)).get("bf16_tflops")
+                tf32_peak = tf32_peak / 2 if tf32_peak else None
+            t_ach = f_conv * px_rank / secs / 1e12 if secs else None
+            roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                        "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                        "kernel": "tc_stage_kernel (tensor-core engine, one fused TNRD stage)",
+                        "flop_per_px_stage": f_alu, "flop_per_launch": f_alu * px_rank,
+                        "mean_launch_ms": mean_launch_ms,
+                        "peak_source": f"derived: {n_sm} SM x 128 FP32 lanes x 2 x {max_mhz:.0f} MHz "
+                                       "(MEASURED_PEAKS.json has no FP32 figure)",
+                        "fp32_equivalent_frac": (flop_launch / secs / 1e12 / peak) if secs else None,
+                        "tensor": {"flop_per_px_stage": f_conv, "executed_split": "3xTF32 (3 MMAs per product)",
+                                   "achieved": t_ach, "peak": tf32_peak,
+                                   "frac": (t_ach / tf32_peak) if (t_ach and tf32_peak) else None,
+                                   "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (TF32 = half the bf16 rate)"}}
         line = {
             "metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": workload_config(p, world, args),
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "stage_kernel (one fused TNRD stage)",
-                         "flop_per_launch": flop_launch, "mean_launch_ms": mean_launch_ms,
-                         "peak_source": f"derived: {n_sm} SM x 128 FP32 lanes x 2 x {max_mhz:.0f} MHz "
-                                        "(MEASURED_PEAKS.json has no FP32 figure)"},
+            "config": dict(workload_config(p, world, args), engine="tensor" if tensor else "fp32"),
+            "roofline": roofline,
             "gpu_launches": launches,
             "clocks": clocks,
             "e2e": e2e,
