@@ -195,8 +195,9 @@ __device__ __forceinline__ void phi_fpairs(const float *__restrict__ s_pp, int p
             yrb[p] = h2.w;
             const f2 lo2 = fma2(pk(warp_min(va), warp_min(vb)), h1.x, h1.y);
             const f2 hi2 = fma2(pk(warp_max(va), warp_max(vb)), h1.x, pk(h2.x, h2.y));
-            const int u0 = max(0, min(ceil_i(lo(lo2)), ceil_i(hi(lo2))));
-            const int u1 = min(nb - 1, max(floor_i(lo(hi2)), floor_i(hi(hi2))));
+            // ceil / floor are monotone: min / max first, one conversion each
+            const int u0 = max(0, ceil_i(fminf(lo(lo2), hi(lo2))));
+            const int u1 = min(nb - 1, floor_i(fmaxf(lo(hi2), hi(hi2))));
             up[p] = reinterpret_cast<const char *>(hp + kTcPairHdr) + u0 * (4 * kTcPairUnit);
             nmax = max(nmax, u1 - u0 + 1);
             w[g + p] = 0ull;
@@ -427,10 +428,10 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
             if (i + kSlots < nmb) build(i + kSlots);  // slot s is free: W(i) consumed, Z(i) read
             named_sync(BAR_BG, 128);
             // d(y, x) += sum_b Z[(y + a, x + b)][a K + b] over rows 2i, 2i + 1 (v row y + a)
-            const int j0 = 2 * i;
-            for (int it = gt; it < (K + 1) * OW; it += 128) {
-                const int y = j0 - (K - 1) + it / OW, x = it % OW;
-                if (y < 0 || y >= OH) continue;
+            const int j0 = 2 * i, x = gt & 63;
+            for (int r = gt >> 6; r < K + 1; r += 2) {  // output rows j0 - (K-1) .. j0 + 1
+                const int y = j0 - (K - 1) + r;
+                if (x >= OW || y < 0 || y >= OH) continue;
                 float d = s_d[y * OW + x];
 #pragma unroll
                 for (int jj = 0; jj < 2; ++jj) {
@@ -533,14 +534,22 @@ bool tc_supported(int ksize, int Nk) {
     return (ksize == 3 && Nk == 8) || (ksize == 5 && Nk == 24) || (ksize == 7 && Nk == 48);
 }
 
-// Output rows per tile: 128 (v region 64 x 134 at k = 7: 1.155 pixel-stages of
-// work per output pixel) when the launch has at least one tile per SM, else halved
-// until it has (or 16 rows).
+// Output rows per tile: the OH in {128, 96, 64, 48, 32, 24, 16} that minimises
+// waves x (M-blocks per tile + ~6 blocks of per-tile set-up and pipeline fill):
+// C4 / C5 take 128 (1.155 pixel-stages per output pixel), one 512^2 image 32
+// (144 tiles: one wave of 58 x 32 tiles).
 int tc_choose_rows(int ksize, int B, int H, int W, int num_sms) {
-    const int ow = kTcVW - 2 * (ksize / 2);
-    int oh = 128;
-    while (oh > 16 && (long long)B * ((W + ow - 1) / ow) * ((H + oh - 1) / oh) < num_sms) oh /= 2;
-    return oh;
+    const int R = ksize / 2, ow = kTcVW - 2 * R;
+    const int cand[] = {128, 96, 64, 48, 32, 24, 16};
+    int best = 128;
+    double best_cost = 1e300;
+    for (int oh : cand) {
+        const long long tiles = (long long)B * ((W + ow - 1) / ow) * ((H + oh - 1) / oh);
+        const long long waves = (tiles + num_sms - 1) / num_sms;
+        const double cost = (double)waves * ((oh + 2 * R) / 2 + 6);
+        if (cost < best_cost) { best_cost = cost; best = oh; }
+    }
+    return best;
 }
 
 cudaError_t launch_stage_tc(int ksize, StageArgs &a, int B, cudaStream_t s) {
