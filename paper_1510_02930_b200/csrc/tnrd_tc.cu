@@ -76,25 +76,6 @@ __device__ __forceinline__ void mma_tf32(uint32_t d, uint32_t a, uint64_t b, uin
                  "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
                  "r"(a), "l"(b), "r"(idesc), "r"(acc));
 }
-// Warp-collective forms: the whole (converged) warp runs the issue code, so the
-// operands stay in uniform registers, and one elected lane issues.  A single thread
-// issuing with per-thread operands reaches only one MMA per ~55 cycles (register ->
-// uniform moves), below the tensor pipe's 24-28 cycles at N = 48-56
-// (tools/tc_rate.cu, profiles/r01_tc_rate.json).
-__device__ __forceinline__ void mma_tf32_warp(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-#ifdef TNRD_EXP_NOMMA
-    return;
-#endif
-    asm volatile("{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                 "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-                 "r"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void mma_commit_warp(uint64_t *bar) {
-    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
-                     smem_u32(bar))
-                 : "memory");
-}
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -289,7 +270,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 //   4 build / gather warps (lane quarter w % 4): im2col A(i) -> TMEM, arrive
 //               A_full(i); wait Z(i), Z -> smem, A(i+3) into the freed slot, then
 //               d += the block's taps (blocks in order: d summed in v-row order)
-//   last warp   issues the 3xTF32 MMAs (one elected lane, warp converged): F(i) on A_full(i) -> V_full(i),
+//   last warp   lane 0 issues the 3xTF32 MMAs: F(i) on A_full(i) -> V_full(i),
 //               Adj(i) on W_full(i) -> Z_full(i), in the order F(0..2), Adj(0),
 //               F(3), Adj(1), F(4), ...
 template <int K, int NK>
@@ -448,9 +429,6 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
             named_sync(BAR_BG, 128);
             // d(y, x) += sum_b Z[(y + a, x + b)][a K + b] over rows 2i, 2i + 1 (v row y + a)
             const int j0 = 2 * i, x = gt & 63;
-#ifdef TNRD_EXP_NOGATHER
-            if (j0 >= 0) continue;
-#endif
             for (int r = gt >> 6; r < K + 1; r += 2) {  // output rows j0 - (K-1) .. j0 + 1
                 const int y = j0 - (K - 1) + r;
                 if (x >= OW || y < 0 || y >= OH) continue;
@@ -468,14 +446,12 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
                 s_d[y * OW + x] = d;
             }
         }
-    } else {
-        // ======================= MMA warp: runs the issue loop converged, one elected
-        // lane issues (operands in uniform registers); descriptors of K-step k are the
-        // base descriptor + 16 k (256 B further in shared memory)
+    } else if (lane == 0) {
+        // ======================= MMA issuer (one thread)
+        const uint32_t bf_hi = smem_u32(s_bf), bf_lo = bf_hi + 4 * NK * KTP;
+        const uint32_t ba_hi = smem_u32(s_ba), ba_lo = ba_hi + 4 * NZ * NK;
         constexpr uint32_t SBO_F = (KTP / 4) * 128, SBO_A = (NK / 4) * 128;
         constexpr uint32_t id_f = idesc_tf32(NK), id_a = idesc_tf32(NZ);
-        const uint64_t df_hi = umma_desc(smem_u32(s_bf), SBO_F), df_lo = umma_desc(smem_u32(s_bf) + 4 * NK * KTP, SBO_F);
-        const uint64_t da_hi = umma_desc(smem_u32(s_ba), SBO_A), da_lo = umma_desc(smem_u32(s_ba) + 4 * NZ * NK, SBO_A);
         const auto fwd = [&](int i) {  // V = A_lo B_hi + A_hi B_lo + A_hi B_hi
             const int s = i % kSlots;
             mbar_wait(bar_a + s, (i / kSlots) & 1);
@@ -483,11 +459,11 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
             const uint32_t tA = tmem + SLOT * s, tV = tmem + VZ0 + VZW * s;
 #pragma unroll
             for (int k = 0; k < KTP / 8; ++k) {
-                mma_tf32_warp(tV, tA + KTP + 8 * k, df_hi + 16 * k, id_f, k > 0);
-                mma_tf32_warp(tV, tA + 8 * k, df_lo + 16 * k, id_f, 1);
-                mma_tf32_warp(tV, tA + 8 * k, df_hi + 16 * k, id_f, 1);
+                mma_tf32(tV, tA + KTP + 8 * k, umma_desc(bf_hi + 256 * k, SBO_F), id_f, k > 0);
+                mma_tf32(tV, tA + 8 * k, umma_desc(bf_lo + 256 * k, SBO_F), id_f, 1);
+                mma_tf32(tV, tA + 8 * k, umma_desc(bf_hi + 256 * k, SBO_F), id_f, 1);
             }
-            mma_commit_warp(bar_v + s);
+            mma_commit(bar_v + s);
         };
         for (int i = 0; i < kSlots && i < nmb; ++i) fwd(i);
         for (int i = 0; i < nmb; ++i) {  // Z = W_lo B_hi + W_hi B_lo + W_hi B_hi
@@ -497,11 +473,11 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
             const uint32_t tW = tmem + SLOT * s, tZ = tmem + VZ0 + VZW * s;
 #pragma unroll
             for (int k = 0; k < NK / 8; ++k) {
-                mma_tf32_warp(tZ, tW + NK + 8 * k, da_hi + 16 * k, id_a, k > 0);
-                mma_tf32_warp(tZ, tW + 8 * k, da_lo + 16 * k, id_a, 1);
-                mma_tf32_warp(tZ, tW + 8 * k, da_hi + 16 * k, id_a, 1);
+                mma_tf32(tZ, tW + NK + 8 * k, umma_desc(ba_hi + 256 * k, SBO_A), id_a, k > 0);
+                mma_tf32(tZ, tW + 8 * k, umma_desc(ba_lo + 256 * k, SBO_A), id_a, 1);
+                mma_tf32(tZ, tW + 8 * k, umma_desc(ba_hi + 256 * k, SBO_A), id_a, 1);
             }
-            mma_commit_warp(bar_z + s);
+            mma_commit(bar_z + s);
             if (i + kSlots < nmb) fwd(i + kSlots);
         }
     }
