@@ -190,7 +190,8 @@ bool tc_ready(const tnrd_handle *h) {
 }
 
 // Engine: tnrd_set_engine (TNRD_ENGINE=fp32|tc in the environment overrides it
-// for tests); AUTO takes the tensor-core engine when it can run.  FP32 tile: "L"
+// for tests; TNRD_TC_ROWS=n forces the tensor engine's tile height); AUTO takes
+// the tensor-core engine when it can run.  FP32 tile: "L"
 // when there are enough tiles to fill the GPU, else "S"; TNRD_FORCE_TILE=L|S
 // overrides (tests run every code path on small, fully oracle-checkable images).
 // Results do not depend on the tile choice (per-pixel arithmetic is tiling-free).
@@ -202,6 +203,8 @@ Plan plan_for(const tnrd_handle *h, int B, int H, int W, bool allow_tc) {
     if (env_engine && env_engine[0] == 't') engine = TNRD_ENGINE_TENSOR;
     if (allow_tc && engine != TNRD_ENGINE_FP32 && tc_ready(h)) {
         p.tc_oh = tnrd::tc_choose_rows(h->d.ksize, B, H, W, h->num_sms);
+        static const char *rows = getenv("TNRD_TC_ROWS");  // tests: force the tile height
+        if (rows && atoi(rows) >= 2 && atoi(rows) % 2 == 0) p.tc_oh = atoi(rows);
         return p;
     }
     static const char *force = getenv("TNRD_FORCE_TILE");

@@ -123,6 +123,27 @@ def test_c4_full_batch_windows(torch_cuda, P):
             _assert_parity(u[b, y0:y1, x0:x1], ref, float(p.peaks[b]), what=f"C4 b={b} win=({y0},{x0})")
 
 
+def test_c4_c5_fp32_engine_windows_and_engine_agreement(torch_cuda, P):
+    """The FP32 engine at C4 / C5 scale (the default engine is the tensor one): oracle
+    windows, and the two engines agree to within the bar everywhere."""
+    p4 = make_problem(4)
+    sub = slice(0, 16)
+    u_fp = _gpu_denoise(P, torch_cuda, p4.model, p4.f[sub], engine=P.ENGINE_FP32)
+    u_tc = _gpu_denoise(P, torch_cuda, p4.model, p4.f[sub], engine=P.ENGINE_TENSOR)
+    for b in range(16):
+        assert np.max(np.abs(u_fp[b] - u_tc[b])) <= 2 * TOL * float(p4.peaks[b]), b
+    rng = np.random.default_rng(44)
+    for b in (0, 3):
+        for (y0, y1, x0, x1) in _windows(512, 512, 1, rng)[:3]:
+            ref = oracle.denoise_window(p4.f[b], p4.model, y0, y1, x0, x1)
+            _assert_parity(u_fp[b, y0:y1, x0:x1], ref, float(p4.peaks[b]), what=f"C4/fp32 b={b} win=({y0},{x0})")
+    p5 = make_problem(5)
+    u5 = _gpu_denoise(P, torch_cuda, p5.model, p5.f, engine=P.ENGINE_FP32)[0]
+    for (y0, y1, x0, x1) in [(0, 48, 0, 48), (4000, 4048, 5000, 5048), (8144, 8192, 8144, 8192)]:
+        ref = oracle.denoise_window(p5.f[0], p5.model, y0, y1, x0, x1)
+        _assert_parity(u5[y0:y1, x0:x1], ref, 0.1, what=f"C5/fp32 win=({y0},{x0})")
+
+
 def test_c5_full_image_windows(torch_cuda, P):
     p = make_problem(5)
     u = _gpu_denoise(P, torch_cuda, p.model, p.f)[0]
@@ -233,13 +254,14 @@ def test_bitwise_determinism_batch_and_tile_independence(torch_cuda, P):
     eng.close()
 
 
+@pytest.mark.parametrize("engine", ["auto", "fp32"])
 @pytest.mark.parametrize("nslabs", [2, 3, 8])
-def test_loopback_slabs_bitwise_equal_full(torch_cuda, P, nslabs):
+def test_loopback_slabs_bitwise_equal_full(torch_cuda, P, nslabs, engine):
     """The row-slab path (halo exchange emulated by device copies) reproduces the
-    single-image result bitwise (P15)."""
+    single-image result bitwise (P15), on the default (tensor) and the FP32 engine."""
     torch = torch_cuda
     p = make_problem(3)
-    eng = P.TNRD(p.model)
+    eng = P.TNRD(p.model, engine=P.ENGINE_FP32 if engine == "fp32" else P.ENGINE_AUTO)
     f = torch.from_numpy(p.f[0]).cuda()
     full = eng.denoise(f)
     u = torch.empty_like(f)
