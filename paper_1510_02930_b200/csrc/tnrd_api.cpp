@@ -421,7 +421,7 @@ float tf32_rn_host(float x) {
     return r;
 }
 
-void pack_tc_stage(const tnrd_desc &d, const float *filters, const float *phi_host, int ps, float *out) {
+void pack_tc_stage(const tnrd_desc &d, const float *filters, const float *phi_host, int ps, int mode, float *out) {
     const int K = d.ksize, Nk = d.n_filters, M = d.n_rbf, KT = K * K;
     const int KTP = tnrd::tc_ktp(K), NZ = tnrd::tc_nz(K), PPS = tnrd::tc_pair_stride(M), NB = (M + 7) / 8;
     std::memset(out, 0, sizeof(float) * tnrd::tc_par_floats(K, Nk, M));
@@ -437,6 +437,11 @@ void pack_tc_stage(const tnrd_desc &d, const float *filters, const float *phi_ho
             ba_hi[tnrd::tc_b_index(t, n, Nk)] = hi;
             ba_lo[tnrd::tc_b_index(t, n, Nk)] = lo;
         }
+    if (mode == tnrd::MODE_TABLE) {  // tabulated phi: {a_t, b_t, n_int, b_lo} per filter
+        for (int n = 0; n < Nk; ++n)
+            std::memcpy(phi + 4 * (size_t)n, phi_host + (size_t)n * ps + tnrd::tap_floats(K), sizeof(float) * 4);
+        return;
+    }
     // phi of filter pairs, interleaved (tnrd_internal.h); units NB..2NB-1 stay 0.
     // Warp unit range (FP32 engine, phi_x2): u0 = ceil((a_s vmin + ct0 - kWindow) / (8 sg)),
     // u1 = floor((a_s vmax + ct0 + kCutT + 0.01) / (8 sg)), folded into one fma each;
@@ -537,8 +542,7 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
         h->raw_gamma = h->raw_mu0;
     }
     h->tc_ok.assign(d->T, 0);
-    if (tnrd::tc_supported(d->ksize, d->n_filters) && d->boundary == TNRD_BC_SYMMETRIC_EXPLICIT &&
-        d->phi_mode == TNRD_PHI_EXACT) {
+    if (tnrd::tc_supported(d->ksize, d->n_filters) && d->boundary == TNRD_BC_SYMMETRIC_EXPLICIT) {
         h->tc_stride = tnrd::tc_par_floats(d->ksize, d->n_filters, d->n_rbf);
         e = cudaMalloc(&h->d_tc, sizeof(float) * (size_t)d->T * h->tc_stride);
         if (e != cudaSuccess) {
@@ -635,9 +639,9 @@ tnrd_status tnrd_set_stage_params(tnrd_handle *h, int t, const float *filters, c
     TNRD_CUDA(h, cudaMemcpy(h->d_params + (size_t)t * Nk * h->pstride_max, host.data(),
                             sizeof(float) * host.size(), cudaMemcpyHostToDevice));
     h->tc_ok[t] = 0;
-    if (h->d_tc && mode == tnrd::MODE_HORNER) {
+    if (h->d_tc && (mode == tnrd::MODE_HORNER || mode == tnrd::MODE_TABLE)) {
         std::vector<float> tc((size_t)h->tc_stride);
-        pack_tc_stage(h->d, filters, host.data(), ps, tc.data());
+        pack_tc_stage(h->d, filters, host.data(), ps, mode, tc.data());
         TNRD_CUDA(h, cudaMemcpy(h->d_tc + (size_t)t * h->tc_stride, tc.data(), sizeof(float) * tc.size(),
                                 cudaMemcpyHostToDevice));
         h->tc_ok[t] = 1;

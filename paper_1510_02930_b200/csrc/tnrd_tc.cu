@@ -359,7 +359,27 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
 #pragma unroll
             for (int e = 0; e < NFW / 2; ++e) w[e] = pk(__uint_as_float(vr[2 * e]), __uint_as_float(vr[2 * e + 1]));
 #else
-            phi_fpairs<NFW / 2>(s_pp + h * (NFW / 2) * pps, pps, vr, w);
+            if (a.mode == MODE_TABLE) {
+                // tabulated phi (TNRD_PHI_TABLE): per filter {a_t, b_t,
+                // n_int, b_lo} in the operand block, the cubic intervals in global
+                // memory; the FP32 engine's arithmetic (phi_table_x2), value by value
+#pragma unroll
+                for (int e = 0; e < NFW; ++e) {
+                    const int fi = h * NFW + e;
+                    const float4 fc = *reinterpret_cast<const float4 *>(s_pp + 4 * fi);
+                    const float vv = __uint_as_float(vr[e]);
+                    const float kf = floorf(fmaf(vv, fc.x, fc.y));
+                    const float fr = fmaf(vv, fc.x, fc.y - kf) + fc.w;
+                    const unsigned nint = (unsigned)__float2int_rn(fc.z);
+                    const int k = __float2int_rz(kf);
+                    const float4 c = __ldg(a.table + (size_t)fi * a.table_stride + ((unsigned)k < nint ? (unsigned)k : nint));
+                    const float r = fmaf(fmaf(fmaf(c.w, fr, c.z), fr, c.y), fr, c.x);
+                    if (e & 1) w[e / 2] = pk(lo(w[e / 2]), r);
+                    else w[e / 2] = pk(r, 0.0f);
+                }
+            } else {
+                phi_fpairs<NFW / 2>(s_pp + h * (NFW / 2) * pps, pps, vr, w);
+            }
 #endif
             uint32_t wh[NFW], wl[NFW];
 #pragma unroll

@@ -79,6 +79,8 @@ TC_CASES = [
     dict(k=7, Nk=48, bc=0, phi=0, reaction=0, B=2, H=77, W=131),
     dict(k=7, Nk=48, bc=0, phi=0, reaction=1, B=1, H=130, W=66),
     dict(k=7, Nk=48, bc=0, phi=0, reaction=0, B=1, H=21, W=200),
+    dict(k=7, Nk=48, bc=0, phi=1, reaction=0, B=2, H=40, W=90),
+    dict(k=5, Nk=24, bc=0, phi=1, reaction=0, B=1, H=66, W=70),
 ]
 
 
