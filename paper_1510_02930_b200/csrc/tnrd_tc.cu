@@ -76,6 +76,21 @@ __device__ __forceinline__ void mma_tf32(uint32_t d, uint32_t a, uint64_t b, uin
                  "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
                  "r"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// Warp-collective forms: the whole (converged) warp runs the issue code, so the
+// operands stay in uniform registers, and one elected lane issues: the tensor pipe
+// then runs at its rate (24 cycles per N = 48 MMA against ~55 for a lone thread,
+// tools/tc_rate.cu, profiles/r01_tc_rate.json).
+__device__ __forceinline__ void mma_tf32_warp(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile("{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+                 "r"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_warp(uint64_t *bar) {
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -273,7 +288,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 //   last warp   lane 0 issues the 3xTF32 MMAs: F(i) on A_full(i) -> V_full(i),
 //               Adj(i) on W_full(i) -> Z_full(i), in the order F(0..2), Adj(0),
 //               F(3), Adj(1), F(4), ...
-template <int K, int NK>
+template <int K, int NK, bool TABLE>
 __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant__ StageArgs a) {
     using G = TcGeo<K, NK>;
     constexpr int R = G::R, KT = G::KT, KTP = G::KTP, NZ = G::NZ, OW = G::OW, UW = G::UW, NFW = G::NFW;
@@ -359,7 +374,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
 #pragma unroll
             for (int e = 0; e < NFW / 2; ++e) w[e] = pk(__uint_as_float(vr[2 * e]), __uint_as_float(vr[2 * e + 1]));
 #else
-            if (a.mode == MODE_TABLE) {
+            if constexpr (TABLE) {
                 // tabulated phi (TNRD_PHI_TABLE): per filter {a_t, b_t,
                 // n_int, b_lo} in the operand block, the cubic intervals in global
                 // memory; the FP32 engine's arithmetic (phi_table_x2), value by value
@@ -466,24 +481,38 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
                 s_d[y * OW + x] = d;
             }
         }
-    } else if (lane == 0) {
-        // ======================= MMA issuer (one thread)
+    } else if (TABLE || lane == 0) {
+        // ======================= MMA issuer: one thread with the exact phi; the
+        // converged warp with an elected lane for the tabulated phi, whose shorter phi
+        // puts the MMA chain on the critical path
         const uint32_t bf_hi = smem_u32(s_bf), bf_lo = bf_hi + 4 * NK * KTP;
         const uint32_t ba_hi = smem_u32(s_ba), ba_lo = ba_hi + 4 * NZ * NK;
         constexpr uint32_t SBO_F = (KTP / 4) * 128, SBO_A = (NK / 4) * 128;
         constexpr uint32_t id_f = idesc_tf32(NK), id_a = idesc_tf32(NZ);
+        const uint64_t df_hi = umma_desc(bf_hi, SBO_F), df_lo = umma_desc(bf_lo, SBO_F);
+        const uint64_t da_hi = umma_desc(ba_hi, SBO_A), da_lo = umma_desc(ba_lo, SBO_A);
         const auto fwd = [&](int i) {  // V = A_lo B_hi + A_hi B_lo + A_hi B_hi
             const int s = i % kSlots;
             mbar_wait(bar_a + s, (i / kSlots) & 1);
             tc_fence_after();
             const uint32_t tA = tmem + SLOT * s, tV = tmem + VZ0 + VZW * s;
+            if constexpr (TABLE) {
 #pragma unroll
-            for (int k = 0; k < KTP / 8; ++k) {
-                mma_tf32(tV, tA + KTP + 8 * k, umma_desc(bf_hi + 256 * k, SBO_F), id_f, k > 0);
-                mma_tf32(tV, tA + 8 * k, umma_desc(bf_lo + 256 * k, SBO_F), id_f, 1);
-                mma_tf32(tV, tA + 8 * k, umma_desc(bf_hi + 256 * k, SBO_F), id_f, 1);
+                for (int k = 0; k < KTP / 8; ++k) {   // K-chunk k: descriptor + 16 k (256 B)
+                    mma_tf32_warp(tV, tA + KTP + 8 * k, df_hi + 16 * k, id_f, k > 0);
+                    mma_tf32_warp(tV, tA + 8 * k, df_lo + 16 * k, id_f, 1);
+                    mma_tf32_warp(tV, tA + 8 * k, df_hi + 16 * k, id_f, 1);
+                }
+                mma_commit_warp(bar_v + s);
+            } else {
+#pragma unroll
+                for (int k = 0; k < KTP / 8; ++k) {
+                    mma_tf32(tV, tA + KTP + 8 * k, umma_desc(bf_hi + 256 * k, SBO_F), id_f, k > 0);
+                    mma_tf32(tV, tA + 8 * k, umma_desc(bf_lo + 256 * k, SBO_F), id_f, 1);
+                    mma_tf32(tV, tA + 8 * k, umma_desc(bf_hi + 256 * k, SBO_F), id_f, 1);
+                }
+                mma_commit(bar_v + s);
             }
-            mma_commit(bar_v + s);
         };
         for (int i = 0; i < kSlots && i < nmb; ++i) fwd(i);
         for (int i = 0; i < nmb; ++i) {  // Z = W_lo B_hi + W_hi B_lo + W_hi B_hi
@@ -491,13 +520,23 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
             mbar_wait(bar_w + s, (i / kSlots) & 1);
             tc_fence_after();
             const uint32_t tW = tmem + SLOT * s, tZ = tmem + VZ0 + VZW * s;
+            if constexpr (TABLE) {
 #pragma unroll
-            for (int k = 0; k < NK / 8; ++k) {
-                mma_tf32(tZ, tW + NK + 8 * k, umma_desc(ba_hi + 256 * k, SBO_A), id_a, k > 0);
-                mma_tf32(tZ, tW + 8 * k, umma_desc(ba_lo + 256 * k, SBO_A), id_a, 1);
-                mma_tf32(tZ, tW + 8 * k, umma_desc(ba_hi + 256 * k, SBO_A), id_a, 1);
+                for (int k = 0; k < NK / 8; ++k) {
+                    mma_tf32_warp(tZ, tW + NK + 8 * k, da_hi + 16 * k, id_a, k > 0);
+                    mma_tf32_warp(tZ, tW + 8 * k, da_lo + 16 * k, id_a, 1);
+                    mma_tf32_warp(tZ, tW + 8 * k, da_hi + 16 * k, id_a, 1);
+                }
+                mma_commit_warp(bar_z + s);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NK / 8; ++k) {
+                    mma_tf32(tZ, tW + NK + 8 * k, umma_desc(ba_hi + 256 * k, SBO_A), id_a, k > 0);
+                    mma_tf32(tZ, tW + 8 * k, umma_desc(ba_lo + 256 * k, SBO_A), id_a, 1);
+                    mma_tf32(tZ, tW + 8 * k, umma_desc(ba_hi + 256 * k, SBO_A), id_a, 1);
+                }
+                mma_commit(bar_z + s);
             }
-            mma_commit(bar_z + s);
             if (i + kSlots < nmb) fwd(i + kSlots);
         }
     }
@@ -527,7 +566,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
 template <int K, int NK>
 cudaError_t launch_tc(StageArgs &a, int B, cudaStream_t s) {
     using G = TcGeo<K, NK>;
-    auto kern = tc_stage_kernel<K, NK>;
+    auto kern = a.mode == MODE_TABLE ? tc_stage_kernel<K, NK, true> : tc_stage_kernel<K, NK, false>;
     if (a.tc_oh <= 0 || a.tc_oh % 2 != 0) return cudaErrorInvalidValue;
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
