@@ -542,7 +542,11 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
         h->raw_gamma = h->raw_mu0;
     }
     h->tc_ok.assign(d->T, 0);
-    if (tnrd::tc_supported(d->ksize, d->n_filters) && d->boundary == TNRD_BC_SYMMETRIC_EXPLICIT) {
+    // tensor engine: a built (ksize, N_k), R1, and its operands fit in shared memory
+    // with the smallest tile (large M raises the phi constants: FP32 engine then)
+    if (tnrd::tc_supported(d->ksize, d->n_filters) && d->boundary == TNRD_BC_SYMMETRIC_EXPLICIT &&
+        (long long)tnrd::tc_min_smem_bytes(d->ksize, d->n_filters,
+                                           tnrd::tc_par_floats(d->ksize, d->n_filters, d->n_rbf)) <= smem_optin) {
         h->tc_stride = tnrd::tc_par_floats(d->ksize, d->n_filters, d->n_rbf);
         e = cudaMalloc(&h->d_tc, sizeof(float) * (size_t)d->T * h->tc_stride);
         if (e != cudaSuccess) {

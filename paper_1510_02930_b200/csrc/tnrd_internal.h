@@ -130,6 +130,7 @@ __host__ __device__ constexpr int tc_b_index(int n, int k, int kdim) {
     return ((n >> 3) * (kdim >> 2) + (k >> 2)) * 32 + (n & 7) * 4 + (k & 3);
 }
 bool tc_supported(int ksize, int Nk);
+size_t tc_min_smem_bytes(int ksize, int Nk, int par_floats);
 int tc_choose_rows(int ksize, int B, int H, int W, int num_sms);
 cudaError_t launch_stage_tc(int ksize, StageArgs &a, int B, cudaStream_t s);
 

@@ -593,6 +593,15 @@ bool tc_supported(int ksize, int Nk) {
     return (ksize == 3 && Nk == 8) || (ksize == 5 && Nk == 24) || (ksize == 7 && Nk == 48);
 }
 
+// Shared memory the tensor engine needs with its smallest tile (16 rows) for a model
+// whose stage operand block has `par_floats` floats (0 if (ksize, N_k) is not built).
+size_t tc_min_smem_bytes(int ksize, int Nk, int par_floats) {
+    if (ksize == 3 && Nk == 8) return sizeof(float) * (size_t)tc_smem_floats<3, 8>(16, par_floats);
+    if (ksize == 5 && Nk == 24) return sizeof(float) * (size_t)tc_smem_floats<5, 24>(16, par_floats);
+    if (ksize == 7 && Nk == 48) return sizeof(float) * (size_t)tc_smem_floats<7, 48>(16, par_floats);
+    return 0;
+}
+
 // Output rows per tile: the OH in {128, 96, 64, 48, 32, 24, 16} that minimises
 // waves x (M-blocks per tile + ~6 blocks of per-tile set-up and pipeline fill):
 // C4 / C5 take 128 (1.155 pixel-stages per output pixel), one 512^2 image 32

@@ -94,6 +94,20 @@ def test_engine_parity(torch_cuda, P, cfg, engine):
     _assert_parity(u, u_ref, float(p.peaks[0]), p.clean[0], f"C{cfg} engine={engine}")
 
 
+@pytest.mark.parametrize("M", [9, 31, 100])
+def test_tensor_engine_other_rbf_counts(torch_cuda, P, M):
+    """The tensor engine with M != 63 Gaussians (unit count and constant layout scale
+    with M) against the oracle, 48 x 7 x 7, T = 2."""
+    rng = np.random.default_rng(300 + M)
+    f = rng.poisson(rng.uniform(0, 4, (1, 90, 75))).astype(np.float32)
+    model = make_model(rng, 2, 48, 7, M, float(max(f.max(), 1.0)))
+    eng = P.TNRD(model)
+    assert eng.engine_for(1, 90, 75) == P.ENGINE_TENSOR
+    eng.close()
+    u = _gpu_denoise(P, torch_cuda, model, f)[0]
+    _assert_parity(u, oracle.denoise(f[0], model), 4.0, what=f"tensor M={M}")
+
+
 @pytest.mark.parametrize("cfg", [1, 2])
 def test_r2_boundary_parity(torch_cuda, P, cfg):
     p = make_problem(cfg)
