@@ -181,9 +181,9 @@ struct Plan {
 };
 
 // The tensor-core engine can run every stage of this handle: a built (ksize, N_k)
-// instantiation, boundary R1 and Horner-unit phi in every stage.
+// instantiation and Horner-unit or tabulated phi in every stage (R1 or R2).
 bool tc_ready(const tnrd_handle *h) {
-    if (!h->d_tc || h->d.boundary != TNRD_BC_SYMMETRIC_EXPLICIT) return false;
+    if (!h->d_tc) return false;
     for (int t = 0; t < h->d.T; ++t)
         if (!h->tc_ok[t]) return false;
     return true;
@@ -544,7 +544,7 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
     h->tc_ok.assign(d->T, 0);
     // tensor engine: a built (ksize, N_k), R1, and its operands fit in shared memory
     // with the smallest tile (large M raises the phi constants: FP32 engine then)
-    if (tnrd::tc_supported(d->ksize, d->n_filters) && d->boundary == TNRD_BC_SYMMETRIC_EXPLICIT &&
+    if (tnrd::tc_supported(d->ksize, d->n_filters) &&
         (long long)tnrd::tc_min_smem_bytes(d->ksize, d->n_filters,
                                            tnrd::tc_par_floats(d->ksize, d->n_filters, d->n_rbf)) <= smem_optin) {
         h->tc_stride = tnrd::tc_par_floats(d->ksize, d->n_filters, d->n_rbf);

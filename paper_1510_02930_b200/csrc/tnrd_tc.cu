@@ -288,7 +288,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 //   last warp   lane 0 issues the 3xTF32 MMAs: F(i) on A_full(i) -> V_full(i),
 //               Adj(i) on W_full(i) -> Z_full(i), in the order F(0..2), Adj(0),
 //               F(3), Adj(1), F(4), ...
-template <int K, int NK, bool TABLE>
+template <int K, int NK, bool TABLE, bool R2>
 __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant__ StageArgs a) {
     using G = TcGeo<K, NK>;
     constexpr int R = G::R, KT = G::KT, KTP = G::KTP, NZ = G::NZ, OW = G::OW, UW = G::UW, NFW = G::NFW;
@@ -396,10 +396,14 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
                 phi_fpairs<NFW / 2>(s_pp + h * (NFW / 2) * pps, pps, vr, w);
             }
 #endif
+            // R2 (exact K^T): w is zero outside the image (the gather adds the mirror
+            // images instead); R1 keeps the mirrored w of out-of-image pixels
+            const int gyp = y0 - R + 2 * i + (m >> 6), gxp = x0 - R + (m & 63);
+            const bool zero_w = R2 && ((unsigned)gyp >= (unsigned)H || (unsigned)gxp >= (unsigned)W);
             uint32_t wh[NFW], wl[NFW];
 #pragma unroll
             for (int e = 0; e < NFW; ++e) {
-                const float x = (e & 1) ? hi(w[e / 2]) : lo(w[e / 2]);
+                const float x = zero_w ? 0.0f : ((e & 1) ? hi(w[e / 2]) : lo(w[e / 2]));
                 const float xh = tf32_hi(x);
                 wh[e] = __float_as_uint(xh);
                 wl[e] = __float_as_uint(x - xh);
@@ -444,6 +448,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
         };
         for (int i = 0; i < kSlots && i < nmb; ++i) build(i);
         const int gt = tid - 32 * WBG;  // 0..127
+        const bool r2_edge = R2 && (y0 - R < 0 || y0 + OH + R > H || x0 - R < 0 || x0 + OW + R > W);
         for (int i = 0; i < nmb; ++i) {
             const int s = i % kSlots;
             mbar_wait(bar_z + s, (i / kSlots) & 1);
@@ -464,21 +469,64 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
             named_sync(BAR_BG, 128);
             // d(y, x) += sum_b Z[(y + a, x + b)][a K + b] over rows 2i, 2i + 1 (v row y + a)
             const int j0 = 2 * i, x = gt & 63;
-            for (int r = gt >> 6; r < K + 1; r += 2) {  // output rows j0 - (K-1) .. j0 + 1
-                const int y = j0 - (K - 1) + r;
-                if (x >= OW || y < 0 || y >= OH) continue;
-                float d = s_d[y * OW + x];
+            if (!R2 || !r2_edge) {
+                for (int r = gt >> 6; r < K + 1; r += 2) {  // output rows j0 - (K-1) .. j0 + 1
+                    const int y = j0 - (K - 1) + r;
+                    if (x >= OW || y < 0 || y >= OH) continue;
+                    float d = s_d[y * OW + x];
 #pragma unroll
-                for (int jj = 0; jj < 2; ++jj) {
-                    const int ta = j0 + jj - y;
-                    if (ta < 0 || ta >= K) continue;
-                    const float *zp = s_z + (ta * K) * kZP + jj * 64 + x;
+                    for (int jj = 0; jj < 2; ++jj) {
+                        const int ta = j0 + jj - y;
+                        if (ta < 0 || ta >= K) continue;
+                        const float *zp = s_z + (ta * K) * kZP + jj * 64 + x;
+                        float S = 0.0f;
+#pragma unroll
+                        for (int tb = 0; tb < K; ++tb) S += zp[tb * kZP + tb];
+                        d += S;
+                    }
+                    s_d[y * OW + x] = d;
+                }
+            } else if constexpr (R2) {
+                // R2 tile at an image edge: d(q) = sum_t sum_{x in M(q)} Z[x + a_t][t] over
+                // the mirror images M(q) of q (itself, across the nearest vertical and
+                // horizontal edges, both; Z = 0 outside the image).  Per source row, in order:
+                // row term of q then of its row mirror, each over q's and the column mirror's
+                // columns (S l.57-65, the exact transpose)
+                const auto S_cols = [&](int jj, int ta, int xc) {  // sum_b Z[(row jj, col xc + b)][ta K + b]
+                    const float *zp = s_z + (ta * K) * kZP + jj * 64;
                     float S = 0.0f;
 #pragma unroll
-                    for (int tb = 0; tb < K; ++tb) S += zp[tb * kZP + tb];
-                    d += S;
+                    for (int tb = 0; tb < K; ++tb) {
+                        const int c = xc + tb;
+                        if ((unsigned)c < 64u) S += zp[tb * kZP + c];
+                    }
+                    return S;
+                };
+                for (int r = gt >> 6; r < K + 1; r += 2) {
+                    const int y = j0 - (K - 1) + r;
+                    if (x >= OW || y < 0 || y >= OH) continue;
+                    const int gy = y0 + y, gx = x0 + x;
+                    const int gym = gy < R ? -1 - gy : (gy >= H - R ? 2 * H - 1 - gy : INT_MIN);
+                    const int gxm = gx < R ? -1 - gx : (gx >= W - R ? 2 * W - 1 - gx : INT_MIN);
+                    const int xm = gxm == INT_MIN ? 0 : gxm - x0;  // source col of tap b: xm + b
+                    float d = s_d[y * OW + x];
+#pragma unroll
+                    for (int jj = 0; jj < 2; ++jj) {
+                        const int ta = j0 + jj - y;
+                        if (ta >= 0 && ta < K) {
+                            d += S_cols(jj, ta, x);
+                            if (gxm != INT_MIN) d += S_cols(jj, ta, xm);
+                        }
+                        if (gym != INT_MIN) {
+                            const int ta2 = (y0 - R + j0 + jj) - gym + R;
+                            if (ta2 >= 0 && ta2 < K) {
+                                d += S_cols(jj, ta2, x);
+                                if (gxm != INT_MIN) d += S_cols(jj, ta2, xm);
+                            }
+                        }
+                    }
+                    s_d[y * OW + x] = d;
                 }
-                s_d[y * OW + x] = d;
             }
         }
     } else if (TABLE || lane == 0) {
@@ -566,7 +614,10 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
 template <int K, int NK>
 cudaError_t launch_tc(StageArgs &a, int B, cudaStream_t s) {
     using G = TcGeo<K, NK>;
-    auto kern = a.mode == MODE_TABLE ? tc_stage_kernel<K, NK, true> : tc_stage_kernel<K, NK, false>;
+    auto kern = a.boundary == 1 ? (a.mode == MODE_TABLE ? tc_stage_kernel<K, NK, true, true>
+                                                        : tc_stage_kernel<K, NK, false, true>)
+                                : (a.mode == MODE_TABLE ? tc_stage_kernel<K, NK, true, false>
+                                                        : tc_stage_kernel<K, NK, false, false>);
     if (a.tc_oh <= 0 || a.tc_oh % 2 != 0) return cudaErrorInvalidValue;
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);

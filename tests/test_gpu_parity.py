@@ -108,12 +108,18 @@ def test_tensor_engine_other_rbf_counts(torch_cuda, P, M):
     _assert_parity(u, oracle.denoise(f[0], model), 4.0, what=f"tensor M={M}")
 
 
-@pytest.mark.parametrize("cfg", [1, 2])
-def test_r2_boundary_parity(torch_cuda, P, cfg):
+@pytest.mark.parametrize("engine", ["fp32", "tensor"])
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_r2_boundary_parity(torch_cuda, P, cfg, engine):
+    """R2 (exact K^T) on both engines against the oracle, every pixel."""
     p = make_problem(cfg)
+    e = P.ENGINE_FP32 if engine == "fp32" else P.ENGINE_TENSOR
+    eng = P.TNRD(p.model, boundary=1, engine=e)
+    assert eng.engine_for(1, *p.f.shape[1:]) == e
+    eng.close()
     u_ref = oracle.denoise(p.f[0], p.model, boundary=oracle.BOUNDARY_ADJOINT)
-    u = _gpu_denoise(P, torch_cuda, p.model, p.f, boundary=1)[0]
-    _assert_parity(u, u_ref, float(p.peaks[0]), p.clean[0], f"C{cfg}/R2")
+    u = _gpu_denoise(P, torch_cuda, p.model, p.f, boundary=1, engine=e)[0]
+    _assert_parity(u, u_ref, float(p.peaks[0]), p.clean[0], f"C{cfg}/R2 engine={engine}")
 
 
 def _windows(H, W, n_rand, rng, size=64):

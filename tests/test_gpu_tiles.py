@@ -81,10 +81,14 @@ TC_CASES = [
     dict(k=7, Nk=48, bc=0, phi=0, reaction=0, B=1, H=21, W=200),
     dict(k=7, Nk=48, bc=0, phi=1, reaction=0, B=2, H=40, W=90),
     dict(k=5, Nk=24, bc=0, phi=1, reaction=0, B=1, H=66, W=70),
+    dict(k=7, Nk=48, bc=1, phi=0, reaction=0, B=2, H=77, W=131),
+    dict(k=7, Nk=48, bc=1, phi=0, reaction=0, B=1, H=7, W=7),
+    dict(k=5, Nk=24, bc=1, phi=1, reaction=0, B=1, H=66, W=70),
+    dict(k=3, Nk=8, bc=1, phi=0, reaction=0, B=2, H=3, W=40),
 ]
 
 
-@pytest.mark.parametrize("case", TC_CASES, ids=lambda c: "tc-k{k}-r{reaction}-{B}x{H}x{W}".format(**c))
+@pytest.mark.parametrize("case", TC_CASES, ids=lambda c: "tc-k{k}-bc{bc}-phi{phi}-r{reaction}-{B}x{H}x{W}".format(**c))
 def test_tensor_engine_tile_heights_match_oracle_and_each_other(tmp_path, case):
     """The tensor-core engine with 16- and 128-row tiles (different M-block and tile
     boundaries) is bitwise equal to itself and within the bar of the oracle."""
