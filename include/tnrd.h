@@ -92,7 +92,7 @@ typedef enum {
  *   FP32:   fp32 FMAs on the CUDA cores (tnrd_kernels.cu);
  *   TENSOR: tcgen05 tensor-core GEMMs in 3xTF32 (each operand split hi + lo, three
  *           TF32 products, fp32 accumulation; tnrd_tc.cu), for
- *           (ksize, N_k) in {(3, 8), (5, 24), (7, 48)} and boundary R1, with exact
+ *           (ksize, N_k) in {(3, 8), (5, 24), (7, 48)}, boundary R1 or R2, exact
  *           or tabulated phi (the exact path's direct-sum fallback runs on FP32);
  *   AUTO:   TENSOR where it applies, else FP32 (the default). */
 typedef enum {
