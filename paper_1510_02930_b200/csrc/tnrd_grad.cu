@@ -202,15 +202,28 @@ __global__ void __launch_bounds__(kGradThreads) phi_all_kernel(GradFilterArgs g,
     __syncthreads();
     const float mu0 = g.grid3[(g.fi0 + f) * 3], step = g.grid3[(g.fi0 + f) * 3 + 1], gam = g.grid3[(g.fi0 + f) * 3 + 2];
     const float inv2g2 = 1.0f / (2.0f * gam * gam), invg2 = 1.0f / (gam * gam);
+    // G_j = __expf(-d^2 inv2g2) is exactly 0 once d^2 inv2g2 > 104 (ex2 of < -150):
+    // centres farther than dmax from every value of the warp are skipped, which leaves
+    // every sum bitwise unchanged (each skipped term would add an exact 0)
+    const float dmax = sqrtf(104.5f / inv2g2) * 1.0001f + 1e-6f * (fabsf(mu0) + 64.0f * step);
     float acc[64];
 #pragma unroll
     for (int j = 0; j < 64; ++j) acc[j] = 0.0f;
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < g.n; p += (long long)gridDim.x * blockDim.x) {
-        const float x = xv[(long long)f * g.n + p], a = av[(long long)f * g.n + p];
+    for (long long p0 = (long long)blockIdx.x * blockDim.x; p0 < g.n; p0 += (long long)gridDim.x * blockDim.x) {
+        const long long p = p0 + threadIdx.x;
+        const bool valid = p < g.n;
+        const float x = valid ? xv[(long long)f * g.n + p] : mu0, a = valid ? av[(long long)f * g.n + p] : 0.0f;
+        float wmin = x, wmax = x;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            wmin = fminf(wmin, __shfl_xor_sync(0xffffffffu, wmin, o));
+            wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+        }
+        const int jlo = (int)floorf((wmin - dmax - mu0) / step), jhi = (int)ceilf((wmax + dmax - mu0) / step);
         float phi = 0.0f, dphi = 0.0f;
 #pragma unroll
         for (int j = 0; j < 64; ++j) {
-            if (j < M) {
+            if (j < M && j >= jlo && j <= jhi) {
                 const float d = x - fmaf((float)j, step, mu0);
                 const float G = __expf(-d * d * inv2g2);
                 phi = fmaf(sw[j], G, phi);
@@ -218,8 +231,10 @@ __global__ void __launch_bounds__(kGradThreads) phi_all_kernel(GradFilterArgs g,
                 acc[j] = fmaf(-a, G, acc[j]);
             }
         }
-        wo[(long long)f * g.n + p] = phi;
-        bo[(long long)f * g.n + p] = dphi * a;
+        if (valid) {
+            wo[(long long)f * g.n + p] = phi;
+            bo[(long long)f * g.n + p] = dphi * a;
+        }
     }
     block_sum<64>(acc, partial + ((long long)f * gridDim.x + blockIdx.x) * 64);
 }
