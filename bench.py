@@ -404,7 +404,11 @@ def main():
             "metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": dict(workload_config(p, world, args), engine="tensor" if tensor else "fp32"),
+            "config": dict(workload_config(p, world, args), engine="tensor" if tensor else "fp32",
+                           conv_arithmetic=("3xTF32 tcgen05: fp32 operands split hi + lo, three TF32 products "
+                                            "per term, fp32 accumulation (products exact to < 2^-20 relative); "
+                                            "parity margin equal to the FP32 engine's (DESIGN.md §5.11)")
+                           if tensor else "fp32 FFMA2"),
             "roofline": roofline,
             "gpu_launches": launches,
             "clocks": clocks,
