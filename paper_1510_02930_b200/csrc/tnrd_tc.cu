@@ -22,17 +22,20 @@
 // 0.04-0.06 of the tolerance on C4/C5 windows, as fp32 does.
 //
 // Data flow per tile (output OW x OH, v region 64 x (OH + 2r), u region + 2r):
-// the v region is cut into M-blocks of two 64-pixel rows.  TMEM lane m = pixel m
-// of the block.  For each block: (1) every thread writes its pixel's im2col row
-// (hi, lo) into TMEM with tcgen05.st (A from TMEM; for out-of-image pixels the row
-// of the mirrored pixel, so w is the half-sample mirror of the in-image w, R1);
-// (2) one thread issues the forward MMAs (B = taps in shared memory); (3) each
-// thread reads its pixel's responses back (tcgen05.ld), evaluates phi with the
-// FP32 engine's blocked-Horner units (bitwise the same phi), and writes w (hi, lo)
-// over the dead im2col columns; (4) one thread issues the adjoint MMAs into Z;
-// (5) Z goes to shared memory and every output pixel adds its K tap rows of this
-// block to d in a fixed order (a ascending, b ascending), so d is deterministic and
-// independent of tiling and batching.
+// the v region is cut into M-blocks of two 64-pixel rows; TMEM lane m = pixel m of
+// the block; up to three blocks are in flight in three TMEM slots.  Per block:
+// (1) build warps write each pixel's im2col row (hi, lo) into TMEM (tcgen05.st, A
+// from TMEM; out-of-image pixels take the row of their mirror pixel, so w there is
+// the half-sample mirror of the in-image w, R1); (2) the MMA thread issues the
+// forward bank (B = taps in shared memory); (3) phi warps read the responses back
+// (tcgen05.ld), evaluate phi with the FP32 engine's blocked-Horner units (bitwise
+// the same phi) and write w (hi, lo) over the dead im2col columns; (4) the MMA
+// thread issues the adjoint bank into Z; (5) gather warps move Z to shared memory
+// and add each output pixel's K tap rows of the block to d in a fixed order (a
+// ascending, b ascending), so d is deterministic and independent of tiling and
+// batching (R2: mirror-image terms at image edges, w = 0 outside the image).
+// Hand-offs are mbarriers; see tc_stage_kernel.  Macros TNRD_EXP_* and TNRD_TC_GP
+// are timing experiments / tuning knobs, never set in the product build.
 #include "tnrd_internal.h"
 #include "tnrd_device.cuh"
 
