@@ -274,14 +274,16 @@ def test_bitwise_determinism_batch_and_tile_independence(torch_cuda, P):
     eng.close()
 
 
+@pytest.mark.parametrize("boundary", [0, 1])
 @pytest.mark.parametrize("engine", ["auto", "fp32"])
 @pytest.mark.parametrize("nslabs", [2, 3, 8])
-def test_loopback_slabs_bitwise_equal_full(torch_cuda, P, nslabs, engine):
+def test_loopback_slabs_bitwise_equal_full(torch_cuda, P, nslabs, engine, boundary):
     """The row-slab path (halo exchange emulated by device copies) reproduces the
-    single-image result bitwise (P15), on the default (tensor) and the FP32 engine."""
+    single-image result bitwise (P15), on the default (tensor) and the FP32 engine,
+    R1 and R2 (the slab seams are interior rows, the global edges mirror)."""
     torch = torch_cuda
     p = make_problem(3)
-    eng = P.TNRD(p.model, engine=P.ENGINE_FP32 if engine == "fp32" else P.ENGINE_AUTO)
+    eng = P.TNRD(p.model, boundary=boundary, engine=P.ENGINE_FP32 if engine == "fp32" else P.ENGINE_AUTO)
     f = torch.from_numpy(p.f[0]).cuda()
     full = eng.denoise(f)
     u = torch.empty_like(f)
@@ -300,10 +302,11 @@ def test_host_entry_point_matches_device_path(torch_cuda, P):
     eng.close()
 
 
-def test_strided_rows(torch_cuda, P):
+@pytest.mark.parametrize("engine", ["tensor", "fp32"])
+def test_strided_rows(torch_cuda, P, engine):
     torch = torch_cuda
     p = make_problem(2)
-    eng = P.TNRD(p.model)
+    eng = P.TNRD(p.model, engine=P.ENGINE_TENSOR if engine == "tensor" else P.ENGINE_FP32)
     big = torch.zeros((1, 256, 300), device="cuda")
     big[:, :, :256] = torch.from_numpy(p.f).cuda()
     ub = torch.full_like(big, -7.0)
@@ -313,6 +316,20 @@ def test_strided_rows(torch_cuda, P):
     assert torch.equal(ub[:, :, :256], dense)
     assert torch.all(ub[:, :, 256:] == -7.0)  # padding untouched
     eng.close()
+
+
+@pytest.mark.parametrize("shape", [(1, 7, 300), (3, 200, 7), (2, 129, 59), (1, 58, 58), (1, 59, 117)])
+def test_tensor_engine_tile_edges(torch_cuda, P, shape):
+    """Tensor engine on shapes around its 58-column / 2-row-block tiling (one column,
+    one row, exact and ragged tile multiples) against the oracle, both boundaries."""
+    B, H, W = shape
+    rng = np.random.default_rng(H * 7 + W)
+    f = rng.poisson(rng.uniform(0, 4, shape)).astype(np.float32)
+    model = make_model(rng, 2, 48, 7, 63, float(max(f.max(), 1.0)))
+    for bc in (0, 1):
+        u = _gpu_denoise(P, torch_cuda, model, f, boundary=bc, engine=P.ENGINE_TENSOR)
+        for b in range(B):
+            _assert_parity(u[b], oracle.denoise(f[b], model, boundary=bc), 4.0, what=f"tc edges {shape} bc{bc} b{b}")
 
 
 # ------------------------------------------------------------------ phi / prox micro-parity
