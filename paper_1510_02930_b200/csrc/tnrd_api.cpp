@@ -507,6 +507,14 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
     DeviceGuard g(d->device);
     tnrd_handle *h = new tnrd_handle();
     h->d = *d;
+    // on a failed allocation: free what exists (cudaFree(nullptr) is a no-op)
+    const auto release = [](tnrd_handle *hh) {
+        cudaFree(hh->d_params);
+        cudaFree(hh->d_raw);
+        cudaFree(hh->d_tc);
+        cudaFree(hh->d_table);
+        delete hh;
+    };
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, d->device);
     h->pstride_max = std::max(pstride_for(*d, tnrd::MODE_HORNER), pstride_for(*d, tnrd::MODE_DIRECT));
     h->pstride.assign(d->T, 0);
@@ -518,23 +526,21 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, d->device);
     const size_t need_s = tnrd::stage_smem_bytes(d->ksize, 1, d->n_filters, h->pstride_max);
     if ((long long)need_s > smem_optin) {
-        delete h;
+        release(h);
         return fail(nullptr, TNRD_EUNSUPPORTED, "model needs %zu B shared memory (> %d)", need_s, smem_optin);
     }
     h->allow_large_tile = (long long)tnrd::stage_smem_bytes(d->ksize, 0, d->n_filters, h->pstride_max) <= smem_optin;
     const size_t bytes = sizeof(float) * (size_t)d->T * d->n_filters * h->pstride_max;
     e = cudaMalloc(&h->d_params, bytes);
     if (e != cudaSuccess) {
-        delete h;
+        release(h);
         return fail(nullptr, TNRD_ENOMEM, "cudaMalloc params: %s", cudaGetErrorString(e));
     }
     {
         const size_t mm = (size_t)d->ksize * d->ksize;
         e = cudaMalloc(&h->d_raw, sizeof(float) * (size_t)d->T * d->n_filters * (2 * mm + d->n_rbf + 3));
         if (e != cudaSuccess) {
-            cudaFree(h->d_params);
-        cudaFree(h->d_tc);
-            delete h;
+            release(h);
             return fail(nullptr, TNRD_ENOMEM, "cudaMalloc raw params: %s", cudaGetErrorString(e));
         }
         h->raw_mu0.assign((size_t)d->T * d->n_filters, 0.f);
@@ -542,17 +548,15 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
         h->raw_gamma = h->raw_mu0;
     }
     h->tc_ok.assign(d->T, 0);
-    // tensor engine: a built (ksize, N_k), R1, and its operands fit in shared memory
-    // with the smallest tile (large M raises the phi constants: FP32 engine then)
+    // tensor engine: a built (ksize, N_k) whose operands fit in shared memory with the
+    // smallest tile (large M raises the phi constants: FP32 engine then)
     if (tnrd::tc_supported(d->ksize, d->n_filters) &&
         (long long)tnrd::tc_min_smem_bytes(d->ksize, d->n_filters,
                                            tnrd::tc_par_floats(d->ksize, d->n_filters, d->n_rbf)) <= smem_optin) {
         h->tc_stride = tnrd::tc_par_floats(d->ksize, d->n_filters, d->n_rbf);
         e = cudaMalloc(&h->d_tc, sizeof(float) * (size_t)d->T * h->tc_stride);
         if (e != cudaSuccess) {
-            cudaFree(h->d_params);
-        cudaFree(h->d_tc);
-            delete h;
+            release(h);
             return fail(nullptr, TNRD_ENOMEM, "cudaMalloc tensor-core operands: %s", cudaGetErrorString(e));
         }
     }
@@ -560,9 +564,7 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
         h->table_stride = table_intervals(d->n_rbf) + 1;
         e = cudaMalloc(&h->d_table, sizeof(float4) * (size_t)d->T * d->n_filters * h->table_stride);
         if (e != cudaSuccess) {
-            cudaFree(h->d_params);
-        cudaFree(h->d_tc);
-            delete h;
+            release(h);
             return fail(nullptr, TNRD_ENOMEM, "cudaMalloc phi tables: %s", cudaGetErrorString(e));
         }
     }
