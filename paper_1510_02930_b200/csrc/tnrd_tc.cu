@@ -622,9 +622,14 @@ cudaError_t launch_tc(StageArgs &a, int B, cudaStream_t s) {
                                 : (a.mode == MODE_TABLE ? tc_stage_kernel<K, NK, true, false>
                                                         : tc_stage_kernel<K, NK, false, false>);
     if (a.tc_oh <= 0 || a.tc_oh % 2 != 0) return cudaErrorInvalidValue;
-    int dev = 0, optin = 0;
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    static int optin_cache[64] = {0};  // per device, filled on first use
+    int optin = dev < 64 ? optin_cache[dev] : 0;
+    if (optin == 0) {
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (dev < 64) optin_cache[dev] = optin;
+    }
     size_t smem = sizeof(float) * (size_t)tc_smem_floats<K, NK>(a.tc_oh, a.tc_par_floats);
     while (smem > (size_t)optin && a.tc_oh > 8) {  // fewer rows per tile until it fits
         a.tc_oh -= 8;
