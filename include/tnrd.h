@@ -137,8 +137,8 @@ TNRD_API tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out);
  * EINVAL on non-finite values, step/gamma <= 0, lambda <= 0, t out of range.
  * Derived fp32 evaluation constants are computed on the host in double.
  * Synchronous (uploads with a blocking copy). */
-/* Select the engine (tnrd_engine) for later tnrd_denoise* calls on h; the
- * training tape (tnrd_loss_grad) always uses FP32.  EINVAL: bad value.  Host-only. */
+/* Select the engine (tnrd_engine) for later tnrd_denoise* and tnrd_loss_grad
+ * (forward tape) calls on h.  EINVAL: bad value.  Host-only. */
 TNRD_API tnrd_status tnrd_set_engine(tnrd_handle *h, int engine);
 
 /* The engine (TNRD_ENGINE_FP32 or TNRD_ENGINE_TENSOR) tnrd_denoise would use for

@@ -888,7 +888,7 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
     // ---- forward with tape (the fused stage kernel also writes ut)
     TNRD_K(cudaMemcpy2DAsync(tape_u, sizeof(float) * W, f, sizeof(float) * ld, sizeof(float) * W, (size_t)B * H,
                              cudaMemcpyDeviceToDevice, s));
-    const Plan plan = plan_for(h, B, H, W, false);  // the tape comes from the FP32 engine
+    const Plan plan = plan_for(h, B, H, W, true);   // the tape: the same engine as tnrd_denoise
     for (int t = 0; t < T; ++t) {
         StageArgs a{};
         a.u_in = {tape_u + (size_t)t * n, W, (long long)H * W, 0};
