@@ -915,6 +915,11 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
             c.u = tape_u + (size_t)t * n; c.e = e;
             c.gn = gn; c.x = cx; c.a = ca; c.b = cb; c.w = cw; c.t = ct; c.partial = part;
             c.red = red_f + (size_t)(t * Nk + i0) * per_f; c.red_stride = (int)per_f;
+            static const char *adj_env = getenv("TNRD_GRAD_ADJ");  // tests: "fp32" keeps the CUDA-core adjoint
+            if (plan.tc_oh > 0 && F == Nk && !(adj_env && adj_env[0] == 'f')) {
+                c.tc_ba = h->d_tc + (size_t)t * h->tc_stride + 2 * (size_t)Nk * tnrd::tc_ktp(K);
+                c.tc_oh = plan.tc_oh;
+            }
             TNRD_K(tnrd::grad_chunk(c, s));
         }
         std::swap(gb, gn);

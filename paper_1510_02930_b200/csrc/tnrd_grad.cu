@@ -382,8 +382,13 @@ cudaError_t grad_chunk(const GradChunk &c, cudaStream_t s) {
     TNRD_M(fwd_pair_kernel, g, c.u, c.e, c.boundary, c.x, c.a)
     phi_all_kernel<<<grid, kGradThreads, 0, s>>>(g, c.x, c.a, c.w, c.b, c.partial);
     reduce_f_kernel<<<dim3(c.M, c.F), kGradThreads, 0, s>>>(c.partial, c.gx, 64, c.red, c.red_stride, 2 * mm);
-    TNRD_M(adj_b_kernel, g, c.b, c.t)
-    sub_sum_kernel<<<c.gx * c.F, kGradThreads, 0, s>>>(c.t, c.F, g.n, c.gn);
+    if (c.tc_ba) {  // gn -= sum_f K_f^T b_f on the tensor cores (all N_k filters in this chunk)
+        const cudaError_t e = launch_tc_adjoint(c.m, c.F, c.b, c.tc_ba, c.gn, c.B, c.H, c.W, c.tc_oh, s);
+        if (e != cudaSuccess) return e;
+    } else {
+        TNRD_M(adj_b_kernel, g, c.b, c.t)
+        sub_sum_kernel<<<c.gx * c.F, kGradThreads, 0, s>>>(c.t, c.F, g.n, c.gn);
+    }
     TNRD_M(kgrad_pair_kernel, g, c.u, c.e, c.boundary, c.b, c.w, c.partial)
     reduce_f_kernel<<<dim3(2 * mm, c.F), kGradThreads, 0, s>>>(c.partial, c.gx, 2 * mm, c.red, c.red_stride, 0);
 #undef TNRD_M

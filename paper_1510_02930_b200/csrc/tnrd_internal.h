@@ -150,7 +150,13 @@ struct GradChunk {
     float *gn, *x, *a, *b, *w, *t, *partial;
     double *red;
     int red_stride;
+    const float *tc_ba;   // stage's tensor-engine adjoint operands (ba_hi, ba_lo) or null
+    int tc_oh;            // tile rows for the tensor adjoint bank
 };
+// gn -= sum_f K_f^T b_f over all N_k filters of a stage on the tensor cores (tnrd_tc.cu):
+// b [N_k][B*H*W] dense, ba = the stage's adjoint operand block (tc_par layout).
+cudaError_t launch_tc_adjoint(int ksize, int Nk, const float *b, const float *ba, float *gn, int B, int H, int W,
+                              int oh, cudaStream_t s);
 int grad_chunk_grid(long long n, int F, int num_sms);
 cudaError_t grad_chunk(const GradChunk &c, cudaStream_t s);
 cudaError_t grad_reduce(const float *partial, int nblk, int stride, int np, double *out, cudaStream_t s);

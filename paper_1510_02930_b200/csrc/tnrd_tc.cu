@@ -646,6 +646,180 @@ cudaError_t launch_tc(StageArgs &a, int B, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------
+// Tensor-core adjoint bank for the training gradient (tnrd_grad.cu, P Eq.15):
+// gn -= sum_f K_f^T b_f, K_f the symmetric-boundary convolution of the forward
+// bank, as one GEMM per M-block (Z[q][t] = sum_f b_f(q) k_f[t], 3xTF32) and the
+// exact-transpose gather of the stage kernel's R2 path (b = 0 outside the image,
+// mirror-image terms at image edges).  Simple serial form: one M-block at a time,
+// 512 threads (lane m of each warpgroup loads and splits NK/4 of the maps).
+struct TcAdjArgs {
+    const float *b;    // [NK][B*H*W]
+    const float *ba;   // ba_hi [NZ x NK], then ba_lo
+    float *gn;         // [B][H][W], updated in place
+    int B, H, W, oh, tiles_x, tiles_y;
+};
+
+template <int K, int NK>
+__global__ void __launch_bounds__(512, 1) tc_adjoint_kernel(const __grid_constant__ TcAdjArgs a) {
+    constexpr int R = K / 2, KT = K * K, NZ = tc_nz(K), OW = kTcVW - 2 * R, NFQ = NK / 4;
+    extern __shared__ __align__(1024) float4 smem4[];
+    float *s_ba = reinterpret_cast<float *>(smem4);          // [2][NZ x NK]
+    const int OH = a.oh, VH = OH + 2 * R;
+    float *s_z = s_ba + 2 * NZ * NK;                          // [KT][kZP]
+    float *s_d = s_z + KT * kZP;                              // [OH][OW]
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(s_d + round4(OH * OW));
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(mbar + 1);
+    const int tid = threadIdx.x, warp = tid >> 5, wg = tid >> 7, m = tid & 127;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const int H = a.H, W = a.W;
+    const long long n = (long long)a.B * H * W;
+    const int per_img = a.tiles_x * a.tiles_y;
+    const int bi = blockIdx.x / per_img, rem = blockIdx.x - bi * per_img;
+    const int ty = rem / a.tiles_x, x0 = (rem - ty * a.tiles_x) * OW, y0 = ty * OH;
+    for (int j = tid; j < (2 * NZ * NK) / 4; j += 512) smem4[j] = __ldg(reinterpret_cast<const float4 *>(a.ba) + j);
+    for (int j = tid; j < OH * OW; j += 512) s_d[j] = 0.0f;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(s_tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *s_tmem, tl = tmem + lane_off, tZ = tmem + 128;
+    const uint32_t ba_hi = smem_u32(s_ba), ba_lo = ba_hi + 4 * NZ * NK;
+    constexpr uint32_t SBO_A = (NK / 4) * 128;
+    constexpr uint32_t id_a = idesc_tf32(NZ);
+    const float *bb = a.b + (long long)bi * H * W;
+    uint32_t phase = 0;
+    const int nmb = VH / 2;
+    for (int i = 0; i < nmb; ++i) {
+        {   // W (hi, lo) of pixel m: the b maps, 0 outside the image
+            const int gy = y0 - R + 2 * i + (m >> 6), gx = x0 - R + (m & 63);
+            const bool in = (unsigned)gy < (unsigned)H && (unsigned)gx < (unsigned)W;
+            const long long off = (long long)gy * W + gx;
+            uint32_t wh[NFQ], wl[NFQ];
+#pragma unroll
+            for (int e = 0; e < NFQ; ++e) {
+                const float x = in ? __ldg(bb + (long long)(wg * NFQ + e) * n + off) : 0.0f;
+                const float xh = tf32_hi(x);
+                wh[e] = __float_as_uint(xh);
+                wl[e] = __float_as_uint(x - xh);
+            }
+            tmem_st<NFQ>(tl + wg * NFQ, wh);
+            tmem_st<NFQ>(tl + NK + wg * NFQ, wl);
+        }
+        tc_wait_st();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < NK / 8; ++k) {
+                mma_tf32(tZ, tmem + NK + 8 * k, umma_desc(ba_hi + 256 * k, SBO_A), id_a, k > 0);
+                mma_tf32(tZ, tmem + 8 * k, umma_desc(ba_lo + 256 * k, SBO_A), id_a, 1);
+                mma_tf32(tZ, tmem + 8 * k, umma_desc(ba_hi + 256 * k, SBO_A), id_a, 1);
+            }
+            mma_commit(mbar);
+            mbar_wait(mbar, phase);
+        }
+        phase ^= 1;
+        __syncthreads();
+        tc_fence_after();
+#pragma unroll
+        for (int ch = 0; ch < NZ / 8; ++ch) {
+            if (ch % 4 != wg || ch * 8 >= KT) continue;
+            uint32_t z[8];
+            tmem_ld_nowait<8>(tl + 128 + ch * 8, z);
+            tmem_wait_ld(z);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (ch * 8 + e < KT) s_z[(ch * 8 + e) * kZP + m] = __uint_as_float(z[e]);
+        }
+        tc_fence_before();
+        __syncthreads();
+        // d(q) += sum_t sum_{x in M(q)} Z[x + a_t][t] over this block's rows (mirror
+        // images M(q): q, across the nearest vertical / horizontal edge, both)
+        const int j0 = 2 * i;
+        const auto S_cols = [&](int jj, int ta, int xc) {
+            const float *zp = s_z + (ta * K) * kZP + jj * 64;
+            float S = 0.0f;
+#pragma unroll
+            for (int tb = 0; tb < K; ++tb) {
+                const int c = xc + tb;
+                if ((unsigned)c < 64u) S += zp[tb * kZP + c];
+            }
+            return S;
+        };
+        for (int it = tid; it < (K + 1) * 64; it += 512) {
+            const int y = j0 - (K - 1) + it / 64, x = it & 63;
+            if (x >= OW || y < 0 || y >= OH) continue;
+            const int gy = y0 + y, gx = x0 + x;
+            const int gym = gy < R ? -1 - gy : (gy >= H - R ? 2 * H - 1 - gy : INT_MIN);
+            const int gxm = gx < R ? -1 - gx : (gx >= W - R ? 2 * W - 1 - gx : INT_MIN);
+            const int xm = gxm == INT_MIN ? 0 : gxm - x0;
+            float d = s_d[y * OW + x];
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+                const int ta = j0 + jj - y;
+                if (ta >= 0 && ta < K) {
+                    d += S_cols(jj, ta, x);
+                    if (gxm != INT_MIN) d += S_cols(jj, ta, xm);
+                }
+                if (gym != INT_MIN) {
+                    const int ta2 = (y0 - R + j0 + jj) - gym + R;
+                    if (ta2 >= 0 && ta2 < K) {
+                        d += S_cols(jj, ta2, x);
+                        if (gxm != INT_MIN) d += S_cols(jj, ta2, xm);
+                    }
+                }
+            }
+            s_d[y * OW + x] = d;
+        }
+        // the next block writes s_z only after two more CTA barriers
+    }
+    __syncthreads();
+    float *gb = a.gn + (long long)bi * H * W;
+    for (int it = tid; it < OH * OW; it += 512) {
+        const int y = it / OW, x = it - y * OW;
+        if (y0 + y < H && x0 + x < W) gb[(long long)(y0 + y) * W + x0 + x] -= s_d[it];
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+template <int K, int NK>
+cudaError_t launch_tc_adj(const float *b, const float *ba, float *gn, int B, int H, int W, int oh, cudaStream_t s) {
+    constexpr int R = K / 2, OW = kTcVW - 2 * R;
+    TcAdjArgs a{b, ba, gn, B, H, W, oh, (W + OW - 1) / OW, (H + oh - 1) / oh};
+    const size_t smem = sizeof(float) * (2 * (size_t)tc_nz(K) * NK + (size_t)K * K * kZP + round4(oh * OW) + 4);
+    cudaError_t e = cudaFuncSetAttribute(tc_adjoint_kernel<K, NK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const long long nt = (long long)B * a.tiles_x * a.tiles_y;
+    if (nt > INT_MAX) return cudaErrorInvalidValue;
+    if (nt > 0) tc_adjoint_kernel<K, NK><<<(unsigned)nt, 512, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_tc_adjoint(int ksize, int Nk, const float *b, const float *ba, float *gn, int B, int H, int W,
+                              int oh, cudaStream_t s) {
+    if (oh <= 0 || oh % 2) return cudaErrorInvalidValue;
+    if (ksize == 3 && Nk == 8) return launch_tc_adj<3, 8>(b, ba, gn, B, H, W, oh, s);
+    if (ksize == 5 && Nk == 24) return launch_tc_adj<5, 24>(b, ba, gn, B, H, W, oh, s);
+    if (ksize == 7 && Nk == 48) return launch_tc_adj<7, 48>(b, ba, gn, B, H, W, oh, s);
+    return cudaErrorInvalidValue;
+}
+
+namespace {
 }  // namespace
 
 bool tc_supported(int ksize, int Nk) {
