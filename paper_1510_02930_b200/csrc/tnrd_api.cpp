@@ -918,6 +918,7 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
             static const char *adj_env = getenv("TNRD_GRAD_ADJ");  // tests: "fp32" keeps the CUDA-core adjoint
             if (plan.tc_oh > 0 && F == Nk && !(adj_env && adj_env[0] == 'f')) {
                 c.tc_ba = h->d_tc + (size_t)t * h->tc_stride + 2 * (size_t)Nk * tnrd::tc_ktp(K);
+                c.tc_bf = h->d_tc + (size_t)t * h->tc_stride;
                 c.tc_oh = plan.tc_oh;
             }
             TNRD_K(tnrd::grad_chunk(c, s));

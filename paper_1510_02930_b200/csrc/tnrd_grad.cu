@@ -191,6 +191,31 @@ __global__ void __launch_bounds__(kGradThreads) fwd_pair_kernel(GradFilterArgs g
     }
 }
 
+// a_f = Kbar_f^T e on the pixels within r of an image edge (R1), where the exact
+// transpose differs from the mirrored convolution the tensor forward bank computed.
+template <int m>
+__global__ void __launch_bounds__(kGradThreads) adj_border_kernel(GradFilterArgs g, const float *__restrict__ e,
+                                                                  float *__restrict__ ao) {
+    constexpr int r = m / 2;
+    __shared__ float sk[m * m];
+    const int f = blockIdx.y;
+    for (int j = threadIdx.x; j < m * m; j += blockDim.x) sk[j] = g.kbar[(long long)(g.fi0 + f) * m * m + j];
+    __syncthreads();
+    const int H = g.H, W = g.W;
+    const long long top = (long long)r * W, mid = (long long)2 * r * (H - 2 * r > 0 ? H - 2 * r : 0);
+    const long long nb = 2 * top + mid;  // border pixels per image
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (long long)g.B * nb;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long b = idx / nb, k = idx - b * nb;
+        int y, x;
+        if (k < top) { y = (int)(k / W); x = (int)(k - (long long)y * W); }
+        else if (k < 2 * top) { const long long q = k - top; y = H - r + (int)(q / W); x = (int)(q % W); }
+        else { const long long q = k - 2 * top; y = r + (int)(q / (2 * r)); const int c = (int)(q % (2 * r)); x = c < r ? c : W - 2 * r + c; }
+        if (y < 0 || y >= H) continue;
+        ao[(long long)f * g.n + b * H * W + (long long)y * W + x] = adj_at<m>(e + b * H * W, sk, y, x, H, W, false);
+    }
+}
+
 // w_f = phi(x_f), b_f = phi'(x_f) a_f (Lambda, P l.369-371), partial sums of
 // -a_f G_j(x_f) (d l / d w_j) for j < M <= 64: every Gaussian evaluated once.
 __global__ void __launch_bounds__(kGradThreads) phi_all_kernel(GradFilterArgs g, const float *__restrict__ xv,
@@ -379,7 +404,24 @@ cudaError_t grad_chunk(const GradChunk &c, cudaStream_t s) {
         default: return cudaErrorInvalidValue;                                    \
     }
     if (c.M > 64) return cudaErrorInvalidValue;
-    TNRD_M(fwd_pair_kernel, g, c.u, c.e, c.boundary, c.x, c.a)
+    if (c.tc_bf) {  // both forward banks on the tensor cores (all N_k filters in this chunk)
+        cudaError_t e = launch_tc_fwdbank(c.m, c.F, c.u, c.tc_bf, c.x, c.B, c.H, c.W, s);
+        if (e == cudaSuccess) e = launch_tc_fwdbank(c.m, c.F, c.e, c.tc_bf, c.a, c.B, c.H, c.W, s);
+        if (e != cudaSuccess) return e;
+        if (c.boundary == 0) {  // R1: Kbar^T e differs from k * E(e) only within r of an edge
+            const int r = c.m / 2;
+            const long long nb = (long long)c.B * (2LL * r * c.W + 2LL * r * std::max(c.H - 2 * r, 0));
+            const dim3 bgrid((unsigned)std::max<long long>(1, std::min<long long>((nb + kGradThreads - 1) / kGradThreads, 1024)), c.F);
+            switch (c.m) {
+                case 3: adj_border_kernel<3><<<bgrid, kGradThreads, 0, s>>>(g, c.e, c.a); break;
+                case 5: adj_border_kernel<5><<<bgrid, kGradThreads, 0, s>>>(g, c.e, c.a); break;
+                case 7: adj_border_kernel<7><<<bgrid, kGradThreads, 0, s>>>(g, c.e, c.a); break;
+                default: return cudaErrorInvalidValue;
+            }
+        }
+    } else {
+        TNRD_M(fwd_pair_kernel, g, c.u, c.e, c.boundary, c.x, c.a)
+    }
     phi_all_kernel<<<grid, kGradThreads, 0, s>>>(g, c.x, c.a, c.w, c.b, c.partial);
     reduce_f_kernel<<<dim3(c.M, c.F), kGradThreads, 0, s>>>(c.partial, c.gx, 64, c.red, c.red_stride, 2 * mm);
     if (c.tc_ba) {  // gn -= sum_f K_f^T b_f on the tensor cores (all N_k filters in this chunk)

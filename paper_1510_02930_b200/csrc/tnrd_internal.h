@@ -151,12 +151,18 @@ struct GradChunk {
     double *red;
     int red_stride;
     const float *tc_ba;   // stage's tensor-engine adjoint operands (ba_hi, ba_lo) or null
+    const float *tc_bf;   // stage's tensor-engine forward operands (bf_hi, bf_lo) or null
     int tc_oh;            // tile rows for the tensor adjoint bank
 };
 // gn -= sum_f K_f^T b_f over all N_k filters of a stage on the tensor cores (tnrd_tc.cu):
 // b [N_k][B*H*W] dense, ba = the stage's adjoint operand block (tc_par layout).
 cudaError_t launch_tc_adjoint(int ksize, int Nk, const float *b, const float *ba, float *gn, int B, int H, int W,
                               int oh, cudaStream_t s);
+// out[f][p] = (k_f * E(in))(p), the forward bank with the symmetric extension, for all
+// N_k filters on the tensor cores (tnrd_tc.cu): in [B][H][W] dense, out [N_k][B*H*W],
+// bf = the stage's forward operand block (bf_hi, bf_lo).
+cudaError_t launch_tc_fwdbank(int ksize, int Nk, const float *in, const float *bf, float *out, int B, int H, int W,
+                              cudaStream_t s);
 int grad_chunk_grid(long long n, int F, int num_sms);
 cudaError_t grad_chunk(const GradChunk &c, cudaStream_t s);
 cudaError_t grad_reduce(const float *partial, int nblk, int stride, int np, double *out, cudaStream_t s);

@@ -820,6 +820,140 @@ cudaError_t launch_tc_adjoint(int ksize, int Nk, const float *b, const float *ba
 }
 
 namespace {
+
+// ---------------------------------------------------------------------------
+// Tensor-core forward bank for the training gradient (tnrd_grad.cu): out[f][p] =
+// (k_f * E(in))(p) for all filters, the stage kernel's 3xTF32 implicit GEMM on
+// output pixels (M-block = two 64-pixel output rows; no halo), written to HBM in
+// filter-major maps.  Simple serial form, 512 threads.
+struct TcFwdArgs {
+    const float *in;   // [B][H][W]
+    const float *bf;   // bf_hi [NK x KTP], then bf_lo
+    float *out;        // [NK][B*H*W]
+    int B, H, W, tiles_x, tiles_y;
+};
+
+constexpr int kFwdOH = 32;   // output rows per tile of the gradient's forward bank
+
+template <int K, int NK>
+__global__ void __launch_bounds__(512, 1) tc_fwdbank_kernel(const __grid_constant__ TcFwdArgs a) {
+    constexpr int R = K / 2, KT = K * K, KTP = tc_ktp(K), UW = kTcVW + 2 * R, UH = kFwdOH + 2 * R, NFQ = NK / 4;
+    extern __shared__ __align__(1024) float4 smem4[];
+    float *s_bf = reinterpret_cast<float *>(smem4);           // [2][NK x KTP]
+    float *s_u = s_bf + 2 * NK * KTP;                         // [UH][UW]
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(s_u + round4(UH * UW));
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(mbar + 1);
+    const int tid = threadIdx.x, warp = tid >> 5, wg = tid >> 7, m = tid & 127;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const int H = a.H, W = a.W;
+    const long long n = (long long)a.B * H * W;
+    const int per_img = a.tiles_x * a.tiles_y;
+    const int bi = blockIdx.x / per_img, rem = blockIdx.x - bi * per_img;
+    const int ty = rem / a.tiles_x, x0 = (rem - ty * a.tiles_x) * kTcVW, y0 = ty * kFwdOH;
+    for (int j = tid; j < (2 * NK * KTP) / 4; j += 512) smem4[j] = __ldg(reinterpret_cast<const float4 *>(a.bf) + j);
+    const float *ib = a.in + (long long)bi * H * W;
+    for (int j = tid; j < UH * UW; j += 512) {
+        const int r = j / UW, c = j - r * UW;
+        s_u[j] = __ldg(ib + (long long)reflect(y0 - R + r, H) * W + reflect(x0 - R + c, W));
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(s_tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *s_tmem, tl = tmem + lane_off, tV = tmem + 128;
+    const uint32_t bf_hi = smem_u32(s_bf), bf_lo = bf_hi + 4 * NK * KTP;
+    constexpr uint32_t SBO_F = (KTP / 4) * 128;
+    constexpr uint32_t id_f = idesc_tf32(NK);
+    uint32_t phase = 0;
+    for (int i = 0; i < kFwdOH / 2; ++i) {
+        const int y = 2 * i + (m >> 6), x = m & 63;     // output pixel of lane m (tile coordinates)
+        {   // im2col row (hi, lo): tap (ta, tb) reads u(y + R - ta, x + R - tb), tile offset R
+            const float *up = s_u + (y + 2 * R) * UW + x + 2 * R;
+#pragma unroll
+            for (int ch = 0; ch < KTP / 8; ++ch) {
+                if (ch % 4 != wg) continue;
+                uint32_t hv[8], lv[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int t = ch * 8 + e;
+                    float v = 0.0f;
+                    if (t < KT) v = up[-(t / K) * UW - (t % K)];
+                    const float vh = tf32_hi(v);
+                    hv[e] = __float_as_uint(vh);
+                    lv[e] = __float_as_uint(v - vh);
+                }
+                tmem_st8(tl + ch * 8, hv);
+                tmem_st8(tl + KTP + ch * 8, lv);
+            }
+        }
+        tc_wait_st();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < KTP / 8; ++k) {
+                mma_tf32(tV, tmem + KTP + 8 * k, umma_desc(bf_hi + 256 * k, SBO_F), id_f, k > 0);
+                mma_tf32(tV, tmem + 8 * k, umma_desc(bf_lo + 256 * k, SBO_F), id_f, 1);
+                mma_tf32(tV, tmem + 8 * k, umma_desc(bf_hi + 256 * k, SBO_F), id_f, 1);
+            }
+            mma_commit(mbar);
+            mbar_wait(mbar, phase);
+        }
+        phase ^= 1;
+        __syncthreads();
+        tc_fence_after();
+        {   // V -> out maps (this warpgroup's filters), lanes = consecutive pixels
+            uint32_t vr[NFQ];
+            tmem_ld_nowait<NFQ>(tl + 128 + wg * NFQ, vr);
+            tmem_wait_ld(vr);
+            const int gy = y0 + y, gx = x0 + x;
+            if (gy < H && gx < W) {
+                float *op = a.out + (long long)bi * H * W + (long long)gy * W + gx;
+#pragma unroll
+                for (int e = 0; e < NFQ; ++e) op[(long long)(wg * NFQ + e) * n] = __uint_as_float(vr[e]);
+            }
+        }
+        tc_fence_before();
+        __syncthreads();   // TMEM A / V columns are rewritten by the next block
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+template <int K, int NK>
+cudaError_t launch_tc_fwd(const float *in, const float *bf, float *out, int B, int H, int W, cudaStream_t s) {
+    constexpr int R = K / 2;
+    TcFwdArgs a{in, bf, out, B, H, W, (W + kTcVW - 1) / kTcVW, (H + kFwdOH - 1) / kFwdOH};
+    const size_t smem = sizeof(float) * (2 * (size_t)NK * tc_ktp(K) + round4((kFwdOH + 2 * R) * (kTcVW + 2 * R)) + 4);
+    cudaError_t e = cudaFuncSetAttribute(tc_fwdbank_kernel<K, NK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const long long nt = (long long)B * a.tiles_x * a.tiles_y;
+    if (nt > INT_MAX) return cudaErrorInvalidValue;
+    if (nt > 0) tc_fwdbank_kernel<K, NK><<<(unsigned)nt, 512, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_tc_fwdbank(int ksize, int Nk, const float *in, const float *bf, float *out, int B, int H, int W,
+                              cudaStream_t s) {
+    if (ksize == 3 && Nk == 8) return launch_tc_fwd<3, 8>(in, bf, out, B, H, W, s);
+    if (ksize == 5 && Nk == 24) return launch_tc_fwd<5, 24>(in, bf, out, B, H, W, s);
+    if (ksize == 7 && Nk == 48) return launch_tc_fwd<7, 48>(in, bf, out, B, H, W, s);
+    return cudaErrorInvalidValue;
+}
+
+namespace {
 }  // namespace
 
 bool tc_supported(int ksize, int Nk) {

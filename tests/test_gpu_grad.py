@@ -42,7 +42,10 @@ def _check(got, ref, what):
 
 @pytest.mark.parametrize("boundary", [0, 1])
 @pytest.mark.parametrize("B,H,W,T,Nk,k,M", [(2, 24, 20, 2, 4, 3, 15), (1, 33, 40, 3, 6, 5, 31),
-                                           (1, 40, 36, 2, 8, 7, 63), (1, 96, 80, 8, 48, 7, 63)])
+                                           (1, 40, 36, 2, 8, 7, 63), (1, 96, 80, 8, 48, 7, 63),
+                                           # tensor-core banks: (k, N_k) = (3, 8), (5, 24), (7, 48)
+                                           (2, 37, 70, 2, 8, 3, 63), (1, 45, 131, 2, 24, 5, 63),
+                                           (2, 70, 67, 3, 48, 7, 63)])
 def test_loss_grad_parity(torch_cuda, B, H, W, T, Nk, k, M, boundary):
     import paper_1510_02930_b200 as P
     torch = torch_cuda
@@ -58,11 +61,13 @@ def test_loss_grad_parity(torch_cuda, B, H, W, T, Nk, k, M, boundary):
     _check(gl, rlam, "d lambda")
 
 
-def test_loss_grad_is_deterministic_and_batch_additive(torch_cuda):
-    """Bitwise reproducible, and the batch gradient is the sum over images."""
+@pytest.mark.parametrize("Nk,k", [(4, 3), (48, 7)])
+def test_loss_grad_is_deterministic_and_batch_additive(torch_cuda, Nk, k):
+    """Bitwise reproducible, and the batch gradient is the sum over images (CUDA-core
+    and tensor-core banks)."""
     import paper_1510_02930_b200 as P
     torch = torch_cuda
-    f, gt, m = _case(9, 3, 20, 24, 2, 4, 3, 15)
+    f, gt, m = _case(9, 3, 20, 24, 2, Nk, k, 15)
     eng = P.TNRD(m)
     a = eng.loss_grad(torch.from_numpy(f).cuda(), torch.from_numpy(gt).cuda())
     b = eng.loss_grad(torch.from_numpy(f).cuda(), torch.from_numpy(gt).cuda())
