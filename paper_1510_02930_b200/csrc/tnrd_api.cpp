@@ -864,7 +864,8 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
     if (st != TNRD_OK) return st;
     const int grid = tnrd::grad_grid((long long)n, h->num_sms);
     const int gx = tnrd::grad_chunk_grid((long long)n, F, h->num_sms);
-    const size_t part_floats = std::max((size_t)grid, (size_t)F * gx * std::max<size_t>(64, 2 * mm));
+    const int kg_nblk = tnrd::tc_kgrad_blocks(B, H, W, h->num_sms);
+    const size_t part_floats = std::max((size_t)grid, (size_t)F * std::max(gx, kg_nblk) * std::max<size_t>(64, 2 * mm));
     st = grow(h, &h->g_partial, &h->g_partial_bytes, sizeof(float) * part_floats, "partials");
     if (st != TNRD_OK) return st;
     const size_t per_f = 2 * mm + M, nred = TN * per_f + T + 1;
@@ -911,7 +912,7 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
             tnrd::GradChunk c{};
             c.k = raw_k; c.kbar = raw_kbar; c.rw = raw_w; c.grid3 = raw_g3;
             c.fi0 = t * Nk + i0; c.F = std::min(F, Nk - i0);
-            c.m = K; c.M = M; c.B = B; c.H = H; c.W = W; c.boundary = h->d.boundary; c.gx = gx;
+            c.m = K; c.M = M; c.B = B; c.H = H; c.W = W; c.boundary = h->d.boundary; c.gx = gx; c.num_sms = h->num_sms;
             c.u = tape_u + (size_t)t * n; c.e = e;
             c.gn = gn; c.x = cx; c.a = ca; c.b = cb; c.w = cw; c.t = ct; c.partial = part;
             c.red = red_f + (size_t)(t * Nk + i0) * per_f; c.red_stride = (int)per_f;
@@ -920,6 +921,8 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
                 c.tc_ba = h->d_tc + (size_t)t * h->tc_stride + 2 * (size_t)Nk * tnrd::tc_ktp(K);
                 c.tc_bf = h->d_tc + (size_t)t * h->tc_stride;
                 c.tc_oh = plan.tc_oh;
+                static const char *kg_env = getenv("TNRD_GRAD_KG");  // tests: "fp32" keeps the CUDA-core k-gradient
+                if (!(kg_env && kg_env[0] == 'f')) c.tc_kg_nblk = kg_nblk;
             }
             TNRD_K(tnrd::grad_chunk(c, s));
         }

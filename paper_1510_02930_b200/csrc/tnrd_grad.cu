@@ -218,50 +218,88 @@ __global__ void __launch_bounds__(kGradThreads) adj_border_kernel(GradFilterArgs
 
 // w_f = phi(x_f), b_f = phi'(x_f) a_f (Lambda, P l.369-371), partial sums of
 // -a_f G_j(x_f) (d l / d w_j) for j < M <= 64: every Gaussian evaluated once.
-__global__ void __launch_bounds__(kGradThreads) phi_all_kernel(GradFilterArgs g, const float *__restrict__ xv,
-                                                               const float *__restrict__ av, float *__restrict__ wo,
-                                                               float *__restrict__ bo, float *__restrict__ partial) {
-    __shared__ float sw[64];
-    const int f = blockIdx.y, M = g.M;
-    for (int j = threadIdx.x; j < 64; j += blockDim.x) sw[j] = j < M ? g.rw[(long long)(g.fi0 + f) * M + j] : 0.0f;
-    __syncthreads();
+// Two threads per pixel (lanes l and l ^ 16 of a warp: 16 pixels per warp), half h
+// owning the centres j = 2i + h, i < 32 (its weights and 32 accumulators in
+// registers); phi and phi' are the two halves' sums added in a fixed order (half 0 +
+// half 1).  Centres run in groups of 4 per half behind warp-uniform branches: a group
+// is skipped when it lies entirely outside [jlo, jhi], the centres within dmax of
+// some value of the warp; beyond dmax every G_j is exactly 0 (ex2 of < -126
+// flushes), so skipping leaves every sum unchanged.
+constexpr int kPhiThreads = 256;
+
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__global__ void __launch_bounds__(kPhiThreads, 3) phi_all_kernel(GradFilterArgs g, const float *__restrict__ xv,
+                                                                 const float *__restrict__ av, float *__restrict__ wo,
+                                                                 float *__restrict__ bo, float *__restrict__ partial) {
+    __shared__ float red[kPhiThreads / 32][64];
+    const int f = blockIdx.y, M = g.M, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, h = lane >> 4;
     const float mu0 = g.grid3[(g.fi0 + f) * 3], step = g.grid3[(g.fi0 + f) * 3 + 1], gam = g.grid3[(g.fi0 + f) * 3 + 2];
-    const float inv2g2 = 1.0f / (2.0f * gam * gam), invg2 = 1.0f / (gam * gam);
-    // G_j = __expf(-d^2 inv2g2) is exactly 0 once d^2 inv2g2 > 104 (ex2 of < -150):
-    // centres farther than dmax from every value of the warp are skipped, which leaves
-    // every sum bitwise unchanged (each skipped term would add an exact 0)
-    const float dmax = sqrtf(104.5f / inv2g2) * 1.0001f + 1e-6f * (fabsf(mu0) + 64.0f * step);
-    float acc[64];
+    const float c2 = -1.4426950408889634f / (2.0f * gam * gam), invg2 = 1.0f / (gam * gam);
+    const float dmax = sqrtf(104.5f * 2.0f * gam * gam) * 1.0001f + 1e-6f * (fabsf(mu0) + 64.0f * step);
+    float wj[32], acc[32];
 #pragma unroll
-    for (int j = 0; j < 64; ++j) acc[j] = 0.0f;
-    for (long long p0 = (long long)blockIdx.x * blockDim.x; p0 < g.n; p0 += (long long)gridDim.x * blockDim.x) {
-        const long long p = p0 + threadIdx.x;
-        const bool valid = p < g.n;
-        const float x = valid ? xv[(long long)f * g.n + p] : mu0, a = valid ? av[(long long)f * g.n + p] : 0.0f;
-        float wmin = x, wmax = x;
+    for (int i = 0; i < 32; ++i) {
+        wj[i] = 2 * i + h < M ? g.rw[(long long)(g.fi0 + f) * M + 2 * i + h] : 0.0f;
+        acc[i] = 0.0f;
+    }
+    const long long n = g.n;
+    const float *xf = xv + (long long)f * n, *af = av + (long long)f * n;
+    for (long long p0 = ((long long)blockIdx.x * (kPhiThreads / 32) + warp) * 16; p0 < n;
+         p0 += (long long)gridDim.x * (kPhiThreads / 32) * 16) {
+        const long long p = p0 + (lane & 15);
+        const bool valid = p < n;
+        const float x = valid ? xf[p] : 0.0f, na = valid ? -af[p] : 0.0f;
+        float wmin = valid ? x : 3.0e38f, wmax = valid ? x : -3.0e38f;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+        for (int o = 8; o > 0; o >>= 1) {
             wmin = fminf(wmin, __shfl_xor_sync(0xffffffffu, wmin, o));
             wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
         }
-        const int jlo = (int)floorf((wmin - dmax - mu0) / step), jhi = (int)ceilf((wmax + dmax - mu0) / step);
+        // the warp's centre range (the union over its 16 pixels), as local indices
+        // i = j >> 1 covering both halves: warp-uniform
+        const int ilo = max((int)floorf((wmin - dmax - mu0) / step), -2) >> 1;
+        const int ihi = min((int)ceilf((wmax + dmax - mu0) / step), 64) >> 1;
         float phi = 0.0f, dphi = 0.0f;
 #pragma unroll
-        for (int j = 0; j < 64; ++j) {
-            if (j < M && j >= jlo && j <= jhi) {
-                const float d = x - fmaf((float)j, step, mu0);
-                const float G = __expf(-d * d * inv2g2);
-                phi = fmaf(sw[j], G, phi);
-                dphi = fmaf(-sw[j] * d * invg2, G, dphi);
-                acc[j] = fmaf(-a, G, acc[j]);
+        for (int g4 = 0; g4 < 8; ++g4) {
+            if (4 * g4 + 3 >= ilo && 4 * g4 <= ihi) {
+#pragma unroll
+                for (int i = 4 * g4; i < 4 * g4 + 4; ++i) {
+                    const float d = x - fmaf((float)(2 * i + h), step, mu0);
+                    const float G = ex2_ftz(c2 * (d * d));
+                    phi = fmaf(wj[i], G, phi);
+                    dphi = fmaf(wj[i] * d, G, dphi);
+                    acc[i] = fmaf(na, G, acc[i]);
+                }
             }
         }
-        if (valid) {
-            wo[(long long)f * g.n + p] = phi;
-            bo[(long long)f * g.n + p] = dphi * a;
+        // phi = half 0 + half 1 on both lanes of the pair, in that order
+        const float phi_o = __shfl_xor_sync(0xffffffffu, phi, 16), dphi_o = __shfl_xor_sync(0xffffffffu, dphi, 16);
+        const float phi_t = h ? phi_o + phi : phi + phi_o, dphi_t = h ? dphi_o + dphi : dphi + dphi_o;
+        if (valid && h == 0) {
+            wo[(long long)f * n + p] = phi_t;
+            bo[(long long)f * n + p] = -dphi_t * invg2 * -na;
         }
     }
-    block_sum<64>(acc, partial + ((long long)f * gridDim.x + blockIdx.x) * 64);
+    // block sum of acc: lanes of a half, then warps, in fixed orders
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        float v = acc[i];
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((lane & 15) == 0) red[warp][2 * i + h] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 64) {
+        float s = 0.0f;
+        for (int w = 0; w < kPhiThreads / 32; ++w) s += red[w][threadIdx.x];
+        partial[((long long)f * gridDim.x + blockIdx.x) * 64 + threadIdx.x] = s;
+    }
 }
 
 // t_f = K_f^T b_f.
@@ -422,8 +460,14 @@ cudaError_t grad_chunk(const GradChunk &c, cudaStream_t s) {
     } else {
         TNRD_M(fwd_pair_kernel, g, c.u, c.e, c.boundary, c.x, c.a)
     }
-    phi_all_kernel<<<grid, kGradThreads, 0, s>>>(g, c.x, c.a, c.w, c.b, c.partial);
-    reduce_f_kernel<<<dim3(c.M, c.F), kGradThreads, 0, s>>>(c.partial, c.gx, 64, c.red, c.red_stride, 2 * mm);
+    {   // phi_all: one full wave of resident blocks (its grid-stride loop then balances)
+        static int occ = 0;
+        if (occ == 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, phi_all_kernel, kPhiThreads, 0) != cudaSuccess)
+            occ = 1;
+        const int gphi = std::max(1, std::min(c.gx, std::max(1, c.num_sms * std::max(occ, 1) / c.F)));
+        phi_all_kernel<<<dim3(gphi, c.F), kPhiThreads, 0, s>>>(g, c.x, c.a, c.w, c.b, c.partial);
+        reduce_f_kernel<<<dim3(c.M, c.F), kGradThreads, 0, s>>>(c.partial, gphi, 64, c.red, c.red_stride, 2 * mm);
+    }
     if (c.tc_ba) {  // gn -= sum_f K_f^T b_f on the tensor cores (all N_k filters in this chunk)
         const cudaError_t e = launch_tc_adjoint(c.m, c.F, c.b, c.tc_ba, c.gn, c.B, c.H, c.W, c.tc_oh, s);
         if (e != cudaSuccess) return e;
@@ -431,8 +475,16 @@ cudaError_t grad_chunk(const GradChunk &c, cudaStream_t s) {
         TNRD_M(adj_b_kernel, g, c.b, c.t)
         sub_sum_kernel<<<c.gx * c.F, kGradThreads, 0, s>>>(c.t, c.F, g.n, c.gn);
     }
-    TNRD_M(kgrad_pair_kernel, g, c.u, c.e, c.boundary, c.b, c.w, c.partial)
-    reduce_f_kernel<<<dim3(2 * mm, c.F), kGradThreads, 0, s>>>(c.partial, c.gx, 2 * mm, c.red, c.red_stride, 0);
+    if (c.tc_kg_nblk > 0) {  // filter gradient as one GEMM over pixels on the tensor cores
+        const cudaError_t e = launch_tc_kgrad(c.m, c.F, c.u, c.e, c.b, c.w, c.boundary, c.B, c.H, c.W, c.partial,
+                                              c.tc_kg_nblk, s);
+        if (e != cudaSuccess) return e;
+        reduce_f_kernel<<<dim3(2 * mm, c.F), kGradThreads, 0, s>>>(c.partial, c.tc_kg_nblk, 2 * mm, c.red,
+                                                                     c.red_stride, 0);
+    } else {
+        TNRD_M(kgrad_pair_kernel, g, c.u, c.e, c.boundary, c.b, c.w, c.partial)
+        reduce_f_kernel<<<dim3(2 * mm, c.F), kGradThreads, 0, s>>>(c.partial, c.gx, 2 * mm, c.red, c.red_stride, 0);
+    }
 #undef TNRD_M
     return cudaGetLastError();
 }

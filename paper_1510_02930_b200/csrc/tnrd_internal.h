@@ -153,6 +153,8 @@ struct GradChunk {
     const float *tc_ba;   // stage's tensor-engine adjoint operands (ba_hi, ba_lo) or null
     const float *tc_bf;   // stage's tensor-engine forward operands (bf_hi, bf_lo) or null
     int tc_oh;            // tile rows for the tensor adjoint bank
+    int tc_kg_nblk;       // > 0: the filter gradient on the tensor cores with this many CTAs
+    int num_sms;          // of the device (grid sizing)
 };
 // gn -= sum_f K_f^T b_f over all N_k filters of a stage on the tensor cores (tnrd_tc.cu):
 // b [N_k][B*H*W] dense, ba = the stage's adjoint operand block (tc_par layout).
@@ -163,6 +165,12 @@ cudaError_t launch_tc_adjoint(int ksize, int Nk, const float *b, const float *ba
 // bf = the stage's forward operand block (bf_hi, bf_lo).
 cudaError_t launch_tc_fwdbank(int ksize, int Nk, const float *in, const float *bf, float *out, int B, int H, int W,
                               cudaStream_t s);
+// The filter-gradient sums (kgrad_pair_kernel's inner / outer) for all N_k filters
+// as a 3xTF32 GEMM over pixels (tnrd_tc.cu): partial[(f*nblk + blk)*2k^2 + j],
+// nblk = tc_kgrad_blocks(...) CTAs, summed by reduce_f_kernel.
+int tc_kgrad_blocks(int B, int H, int W, int num_sms);
+cudaError_t launch_tc_kgrad(int ksize, int Nk, const float *u, const float *e, const float *b, const float *w,
+                            int boundary, int B, int H, int W, float *partial, int nblk, cudaStream_t s);
 int grad_chunk_grid(long long n, int F, int num_sms);
 cudaError_t grad_chunk(const GradChunk &c, cudaStream_t s);
 cudaError_t grad_reduce(const float *partial, int nblk, int stride, int np, double *out, cudaStream_t s);

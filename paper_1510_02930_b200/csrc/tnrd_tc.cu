@@ -943,6 +943,241 @@ cudaError_t launch_tc_fwd(const float *in, const float *bf, float *out, int B, i
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core filter gradient (P Eq.18-20, the k-part of dL/dθ): for every tap t =
+// (ta, tb) of the k x k support, displacement d_t = (ta - r, tb - r), and filter f
+//   inner[f][t] = sum_p b_f(p) E(u)(p - d_t)
+//   outer[f][t] = sum_p e(p) w_f(mirror(p - d_t))                                    (R1)
+//               = sum_q w_f(q) Ẽ_t(q),  Ẽ_t(q) = sum_{p in Ω: mirror(p - d_t) = q} e(p)
+//   outer[f][t] = sum_p w_f(p) E(e)(p - d_t)                                         (R2)
+// — the sums kgrad_pair_kernel (tnrd_grad.cu) forms pixel by pixel — as one GEMM
+// over pixels: D[t][f] = sum_p A[t][p] Bm[f][p], M = 128 rows = taps (rows >= k^2
+// zero), N = N_k filters, K = pixels.  A (the tap-shifted images, one per tap) is
+// written into TMEM by the thread owning lane t; Bm (the b and w maps) is staged in
+// shared memory in the K-major core-matrix layout; 3xTF32 as in the stage kernel.
+// Two accumulators (inner, outer) stay in TMEM for the CTA's whole pixel range;
+// each CTA writes its D once to `partial` in the layout reduce_f_kernel sums.
+// Work: 32-pixel chunks (half a tile row of a 64 x kKgTH tile), double-buffered in
+// TMEM and shared memory; one CTA per SM, tiles grid-strided over the CTAs.
+struct TcKgArgs {
+    const float *u, *e;       // [B][H][W]
+    const float *b, *w;       // [NK][B*H*W]
+    float *partial;           // [NK][nblk][2 k^2]
+    int boundary, B, H, W, tiles_x, tiles_y;
+};
+
+constexpr int kKgTH = 8;     // tile rows
+
+template <int K, int NK>
+__global__ void __launch_bounds__(512, 1) tc_kgrad_kernel(const __grid_constant__ TcKgArgs a) {
+    constexpr int R = K / 2, KT = K * K, UW = kTcVW + 2 * R + 1, UH = kKgTH + 2 * R;
+    constexpr int QA = (KT + 31) / 32;          // TMEM lane quarters holding taps
+    constexpr int BMF = NK * 32;                // floats of one (map, hi|lo) Bm block
+    constexpr uint32_t SBO = (32 / 4) * 128;    // 8-filter groups, 32 pixels of K
+    constexpr uint32_t id = idesc_tf32(NK);
+    constexpr uint32_t kDin = 256, kDout = 256 + 64;   // TMEM columns of the accumulators
+    static_assert(NK % 8 == 0 && NK <= 64, "N_k");
+    extern __shared__ __align__(1024) float4 smem4[];
+    float *s_bm = reinterpret_cast<float *>(smem4);   // [2 buffers][b_hi, b_lo, w_hi, w_lo][BMF]
+    float *s_u = s_bm + 8 * BMF;                      // [UH][UW], E(u)
+    float *s_e = s_u + round4(UH * UW);               // [UH][UW], E(e) (R1: raw e where used)
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(s_e + round4(UH * UW));   // [2]
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(mbar + 2);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = warp & 3;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const int H = a.H, W = a.W;
+    const long long n = (long long)a.B * H * W;
+    const int per_img = a.tiles_x * a.tiles_y, ntiles = a.B * per_img;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + 1)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *s_tmem, tl = tmem + lane_off;
+    // A rows >= QA*32 (lane quarters without taps) stay zero: write them once
+    if (q >= QA) {
+        const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int c = (warp >> 2) * 8; c < 256; c += 32) tmem_st8(tl + c, z);
+    }
+    const int t = q * 32 + lane;                     // this thread's tap (A builders)
+    const int ta = t / K, tb = t - (t / K) * K;
+    const int sub = warp >> 2;                       // A builders: pixels 8 sub .. 8 sub + 7 of a chunk
+    int chunk = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int bi = tile / per_img, rem = tile - bi * per_img;
+        const int ty = rem / a.tiles_x, x0 = (rem - ty * a.tiles_x) * kTcVW, y0 = ty * kKgTH;
+        const float *ub = a.u + (long long)bi * H * W, *eb = a.e + (long long)bi * H * W;
+        __syncthreads();   // the previous tile's A builds are done with s_u / s_e
+        for (int j = tid; j < UH * (UW - 1); j += 512) {
+            const int r = j / (UW - 1), c = j - r * (UW - 1);
+            const long long o = (long long)reflect(y0 - R + r, H) * W + reflect(x0 - R + c, W);
+            s_u[r * UW + c] = __ldg(ub + o);
+            s_e[r * UW + c] = __ldg(eb + o);
+        }
+        __syncthreads();
+        for (int ch = 0; ch < 2 * kKgTH; ++ch, ++chunk) {
+            const int bb = chunk & 1, yr = ch >> 1, xc0 = (ch & 1) * 32;
+            if (chunk >= 2) mbar_wait(mbar + bb, ((chunk - 2) >> 1) & 1);   // MMAs of chunk - 2 done
+            tc_fence_after();
+            const int gy = y0 + yr;
+            if (q < QA) {   // A: lane t = tap t, 8 pixels per thread
+                uint32_t ih[8], il[8], oh[8], ol[8];
+                const int xc = xc0 + 8 * sub;
+                const float *pu = s_u + (yr + 2 * R - ta) * UW + xc + 2 * R - tb;
+                const bool r1edge = a.boundary == 0 &&
+                                    (gy < R || gy >= H - R || x0 + xc < R || x0 + xc + 7 >= W - R);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    float vi = 0.0f, vo = 0.0f;
+                    if (t < KT) {
+                        vi = pu[i];
+                        if (a.boundary == 1) {
+                            vo = s_e[(yr + 2 * R - ta) * UW + xc + i + 2 * R - tb];
+                        } else if (!r1edge) {
+                            vo = s_e[(yr + ta) * UW + xc + i + tb];
+                        }
+                    }
+                    const float hi_i = tf32_hi(vi), hi_o = tf32_hi(vo);
+                    ih[i] = __float_as_uint(hi_i); il[i] = __float_as_uint(vi - hi_i);
+                    oh[i] = __float_as_uint(hi_o); ol[i] = __float_as_uint(vo - hi_o);
+                }
+                if (r1edge && t < KT) {   // Ẽ_t(q): every in-image preimage p of q (warp-uniform branch)
+                    const int dy = ta - R, dx = tb - R;
+                    for (int i = 0; i < 8; ++i) {
+                        const int qy = gy, qx = x0 + xc + i;
+                        float s = 0.0f;
+                        if (qy < H && qx < W) {
+                            const int cy[3] = {qy + dy, dy - 1 - qy, 2 * H - 1 - qy + dy};
+                            const int cx[3] = {qx + dx, dx - 1 - qx, 2 * W - 1 - qx + dx};
+#pragma unroll
+                            for (int iy = 0; iy < 3; ++iy) {
+                                const int py = cy[iy];
+                                if (py < 0 || py >= H || reflect(py - dy, H) != qy) continue;
+#pragma unroll
+                                for (int ix = 0; ix < 3; ++ix) {
+                                    const int px = cx[ix];
+                                    if (px < 0 || px >= W || reflect(px - dx, W) != qx) continue;
+                                    s += __ldg(eb + (long long)py * W + px);
+                                }
+                            }
+                        }
+                        const float hs = tf32_hi(s);
+                        oh[i] = __float_as_uint(hs); ol[i] = __float_as_uint(s - hs);
+                    }
+                }
+                const uint32_t base = tl + bb * 128 + 8 * sub;
+                tmem_st8(base, ih);
+                tmem_st8(base + 32, il);
+                tmem_st8(base + 64, oh);
+                tmem_st8(base + 96, ol);
+            } else {        // Bm: b and w of this chunk's 32 pixels, float4 per (map, filter, 4 pixels)
+                const int nbt = 512 - QA * 128;                          // builder threads (lane quarters >= QA)
+                const int bt = ((warp >> 2) * (4 - QA) + (q - QA)) * 32 + lane;   // this one's index
+                float *sb = s_bm + bb * 4 * BMF;
+                const bool rowin = gy < H;
+                const long long pbase = (long long)bi * H * W + (long long)gy * W + x0 + xc0;
+                for (int j = bt; j < 2 * NK * 8; j += nbt) {
+                    const int fl = j & 7, kq = (j >> 3) & 7, fg = (j >> 6) % (NK / 8), map = j / (8 * NK);
+                    const int f = fg * 8 + fl, gx = x0 + xc0 + 4 * kq;
+                    const float *src = (map ? a.w : a.b) + (long long)f * n + pbase + 4 * kq;
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (rowin) {
+                        if (gx + 3 < W && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+                            v = __ldg(reinterpret_cast<const float4 *>(src));
+                        } else {
+                            if (gx < W) v.x = __ldg(src);
+                            if (gx + 1 < W) v.y = __ldg(src + 1);
+                            if (gx + 2 < W) v.z = __ldg(src + 2);
+                            if (gx + 3 < W) v.w = __ldg(src + 3);
+                        }
+                    }
+                    const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+                    const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+                    const int o = (fg * 8 + kq) * 32 + fl * 4;
+                    *reinterpret_cast<float4 *>(sb + (2 * map) * BMF + o) = h;
+                    *reinterpret_cast<float4 *>(sb + (2 * map + 1) * BMF + o) = l;
+                }
+            }
+            tc_wait_st();
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tc_fence_before();
+            __syncthreads();
+            if (warp == 0) {
+                tc_fence_after();
+                const uint32_t ab = tmem + bb * 128, sb = smem_u32(s_bm + bb * 4 * BMF);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t ko = 256 * k;
+                    mma_tf32_warp(tmem + kDin, ab + 32 + 8 * k, umma_desc(sb + ko, SBO), id, chunk > 0 || k > 0);
+                    mma_tf32_warp(tmem + kDin, ab + 8 * k, umma_desc(sb + 4 * BMF + ko, SBO), id, 1);
+                    mma_tf32_warp(tmem + kDin, ab + 8 * k, umma_desc(sb + ko, SBO), id, 1);
+                    mma_tf32_warp(tmem + kDout, ab + 96 + 8 * k, umma_desc(sb + 8 * BMF + ko, SBO), id, chunk > 0 || k > 0);
+                    mma_tf32_warp(tmem + kDout, ab + 64 + 8 * k, umma_desc(sb + 12 * BMF + ko, SBO), id, 1);
+                    mma_tf32_warp(tmem + kDout, ab + 64 + 8 * k, umma_desc(sb + 8 * BMF + ko, SBO), id, 1);
+                }
+                mma_commit_warp(mbar + bb);
+            }
+        }
+    }
+    // the last chunk's commit covers every MMA of this CTA
+    if (chunk > 0) mbar_wait(mbar + ((chunk - 1) & 1), ((chunk - 1) >> 1) & 1);
+    tc_fence_after();
+    if (warp < QA) {   // D lanes = taps: write inner / outer for this CTA
+        uint32_t di[NK], dout[NK];
+        tmem_ld_nowait<NK>(tl + kDin, di);
+        tmem_ld_nowait<NK>(tl + kDout, dout);
+        tmem_wait_ld(di);
+        tmem_wait_ld(dout);
+        if (t < KT) {
+#pragma unroll
+            for (int f = 0; f < NK; ++f) {
+                float *pp = a.partial + ((long long)f * gridDim.x + blockIdx.x) * 2 * KT;
+                pp[t] = chunk > 0 ? __uint_as_float(di[f]) : 0.0f;
+                pp[KT + t] = chunk > 0 ? __uint_as_float(dout[f]) : 0.0f;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+template <int K, int NK>
+cudaError_t launch_tc_kg(const float *u, const float *e, const float *b, const float *w, int boundary, int B, int H,
+                         int W, float *partial, int nblk, cudaStream_t s) {
+    constexpr int R = K / 2, UW = kTcVW + 2 * R + 1, UH = kKgTH + 2 * R;
+    TcKgArgs a{u, e, b, w, partial, boundary, B, H, W, (W + kTcVW - 1) / kTcVW, (H + kKgTH - 1) / kKgTH};
+    const size_t smem = sizeof(float) * (8 * (size_t)NK * 32 + 2 * (size_t)round4(UH * UW) + 8);
+    cudaError_t err = cudaFuncSetAttribute(tc_kgrad_kernel<K, NK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    if (nblk > 0) tc_kgrad_kernel<K, NK><<<(unsigned)nblk, 512, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+int tc_kgrad_blocks(int B, int H, int W, int num_sms) {
+    const long long nt = (long long)B * ((W + kTcVW - 1) / kTcVW) * ((H + kKgTH - 1) / kKgTH);
+    return (int)std::max<long long>(1, std::min<long long>(nt, num_sms));
+}
+
+cudaError_t launch_tc_kgrad(int ksize, int Nk, const float *u, const float *e, const float *b, const float *w,
+                            int boundary, int B, int H, int W, float *partial, int nblk, cudaStream_t s) {
+    if (ksize == 3 && Nk == 8) return launch_tc_kg<3, 8>(u, e, b, w, boundary, B, H, W, partial, nblk, s);
+    if (ksize == 5 && Nk == 24) return launch_tc_kg<5, 24>(u, e, b, w, boundary, B, H, W, partial, nblk, s);
+    if (ksize == 7 && Nk == 48) return launch_tc_kg<7, 48>(u, e, b, w, boundary, B, H, W, partial, nblk, s);
+    return cudaErrorInvalidValue;
+}
+
+namespace {
+
 }  // namespace
 
 cudaError_t launch_tc_fwdbank(int ksize, int Nk, const float *in, const float *bf, float *out, int B, int H, int W,
