@@ -19,6 +19,7 @@
 // correct, simple form of the backward (one HBM pass per operation); the fused
 // forward stage kernel (tnrd_kernels.cu) is the optimised hot path.
 #include "tnrd_internal.h"
+#include "tnrd_device.cuh"
 
 #include <algorithm>
 
@@ -219,80 +220,91 @@ __global__ void __launch_bounds__(kGradThreads) adj_border_kernel(GradFilterArgs
 // w_f = phi(x_f), b_f = phi'(x_f) a_f (Lambda, P l.369-371), partial sums of
 // -a_f G_j(x_f) (d l / d w_j) for j < M <= 64: every Gaussian evaluated once.
 // Two threads per pixel (lanes l and l ^ 16 of a warp: 16 pixels per warp), half h
-// owning the centres j = 2i + h, i < 32 (its weights and 32 accumulators in
-// registers); phi and phi' are the two halves' sums added in a fixed order (half 0 +
-// half 1).  Centres run in groups of 4 per half behind warp-uniform branches: a group
-// is skipped when it lies entirely outside [jlo, jhi], the centres within dmax of
-// some value of the warp; beyond dmax every G_j is exactly 0 (ex2 of < -126
-// flushes), so skipping leaves every sum unchanged.
+// owning the centres j = 2i + h, i < 32, as 16 pairs (i, i + 1) in packed fp32x2
+// (weights and accumulators in registers).  With sc = sqrt(log2 e / 2) / gamma and
+// d'_j = (x - mu_j) sc, G_j = 2^(-d'_j^2); phi' uses sum_j w_j d'_j G_j / sc.
+// phi and phi' are the two halves' sums, each half's pair lanes added low + high,
+// then half 0 + half 1 (fixed order).  Centres run in groups of two pairs behind
+// warp-uniform branches: a group is skipped when it lies entirely outside
+// [jlo, jhi], the centres within dmax of some value of the warp; beyond dmax every
+// G_j is exactly 0 (ex2.approx.ftz of < -126 flushes), so skipping changes no sum.
 constexpr int kPhiThreads = 256;
 
-__device__ __forceinline__ float ex2_ftz(float x) {
-    float r;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-
-__global__ void __launch_bounds__(kPhiThreads, 3) phi_all_kernel(GradFilterArgs g, const float *__restrict__ xv,
+#ifndef TNRD_PHI_MINB
+#define TNRD_PHI_MINB 2
+#endif
+__global__ void __launch_bounds__(kPhiThreads, TNRD_PHI_MINB) phi_all_kernel(GradFilterArgs g, const float *__restrict__ xv,
                                                                  const float *__restrict__ av, float *__restrict__ wo,
                                                                  float *__restrict__ bo, float *__restrict__ partial) {
     __shared__ float red[kPhiThreads / 32][64];
     const int f = blockIdx.y, M = g.M, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, h = lane >> 4;
     const float mu0 = g.grid3[(g.fi0 + f) * 3], step = g.grid3[(g.fi0 + f) * 3 + 1], gam = g.grid3[(g.fi0 + f) * 3 + 2];
-    const float c2 = -1.4426950408889634f / (2.0f * gam * gam), invg2 = 1.0f / (gam * gam);
-    const float dmax = sqrtf(104.5f * 2.0f * gam * gam) * 1.0001f + 1e-6f * (fabsf(mu0) + 64.0f * step);
-    float wj[32], acc[32];
+    const float sc = sqrtf(0.72134752044448170f) / gam;             // sqrt(log2(e) / 2) / gamma
+    const float s2 = 2.0f * step * sc, base = fmaf((float)h, step, mu0), invg2 = 1.0f / (gam * gam);
+    // 2^(-t) is exactly 0 for t > 126, t = d^2 log2(e) / (2 gamma^2): |d| > dmax
+    const float dmax = sqrtf(126.0f / 0.72134752044448170f) * gam * 1.0001f + 1e-6f * (fabsf(mu0) + 64.0f * step);
+    const float rstep = 1.0f / step;
+    f2 w2[16], acc2[16];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        wj[i] = 2 * i + h < M ? g.rw[(long long)(g.fi0 + f) * M + 2 * i + h] : 0.0f;
-        acc[i] = 0.0f;
+    for (int ip = 0; ip < 16; ++ip) {
+        const int j0 = 4 * ip + h, j1 = 4 * ip + 2 + h;    // centres of local i = 2ip, 2ip + 1
+        const float *rw = g.rw + (long long)(g.fi0 + f) * M;
+        w2[ip] = pk(j0 < M ? rw[j0] : 0.0f, j1 < M ? rw[j1] : 0.0f);
+        acc2[ip] = 0ull;
     }
     const long long n = g.n;
     const float *xf = xv + (long long)f * n, *af = av + (long long)f * n;
-    for (long long p0 = ((long long)blockIdx.x * (kPhiThreads / 32) + warp) * 16; p0 < n;
-         p0 += (long long)gridDim.x * (kPhiThreads / 32) * 16) {
-        const long long p = p0 + (lane & 15);
+    const long long pstep = (long long)gridDim.x * (kPhiThreads / 32) * 16;
+    long long p = ((long long)blockIdx.x * (kPhiThreads / 32) + warp) * 16 + (lane & 15);
+    float xn = p < n ? xf[p] : 0.0f, an = p < n ? af[p] : 0.0f;
+    for (; p - (lane & 15) < n; p += pstep) {
         const bool valid = p < n;
-        const float x = valid ? xf[p] : 0.0f, na = valid ? -af[p] : 0.0f;
-        float wmin = valid ? x : 3.0e38f, wmax = valid ? x : -3.0e38f;
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) {
-            wmin = fminf(wmin, __shfl_xor_sync(0xffffffffu, wmin, o));
-            wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
-        }
-        // the warp's centre range (the union over its 16 pixels), as local indices
-        // i = j >> 1 covering both halves: warp-uniform
-        const int ilo = max((int)floorf((wmin - dmax - mu0) / step), -2) >> 1;
-        const int ihi = min((int)ceilf((wmax + dmax - mu0) / step), 64) >> 1;
-        float phi = 0.0f, dphi = 0.0f;
+        const float x = xn, na = valid ? -an : 0.0f;
+        if (p + pstep < n) { xn = xf[p + pstep]; an = af[p + pstep]; }   // next pixel's loads in flight
+        const float wmin = warp_min(valid ? x : 3.0e38f), wmax = warp_max(valid ? x : -3.0e38f);
+        // the warp's centre range (its 16 pixels), as local indices i = j >> 1 of
+        // both halves: warp-uniform
+        const int ilo = max((int)floorf((wmin - dmax - mu0) * rstep), -2) >> 1;
+        const int ihi = min((int)ceilf((wmax + dmax - mu0) * rstep), 64) >> 1;
+        const float xs = (x - base) * sc;
+        const f2 na2 = bc(na);
+        f2 phi2 = 0ull, dphi2 = 0ull;
 #pragma unroll
         for (int g4 = 0; g4 < 8; ++g4) {
             if (4 * g4 + 3 >= ilo && 4 * g4 <= ihi) {
 #pragma unroll
-                for (int i = 4 * g4; i < 4 * g4 + 4; ++i) {
-                    const float d = x - fmaf((float)(2 * i + h), step, mu0);
-                    const float G = ex2_ftz(c2 * (d * d));
-                    phi = fmaf(wj[i], G, phi);
-                    dphi = fmaf(wj[i] * d, G, dphi);
-                    acc[i] = fmaf(na, G, acc[i]);
+                for (int ip = 2 * g4; ip < 2 * g4 + 2; ++ip) {
+                    const f2 d2 = fma2(pk(-(float)(2 * ip), -(float)(2 * ip + 1)), bc(s2), bc(xs));
+                    const f2 t2 = mul2(d2, d2);
+                    const f2 G2 = pk(ex2_ftz(-lo(t2)), ex2_ftz(-hi(t2)));
+                    phi2 = fma2(w2[ip], G2, phi2);
+                    dphi2 = fma2(mul2(w2[ip], d2), G2, dphi2);
+                    acc2[ip] = fma2(na2, G2, acc2[ip]);
                 }
             }
         }
+        const float phi = lo(phi2) + hi(phi2), dphi = lo(dphi2) + hi(dphi2);
         // phi = half 0 + half 1 on both lanes of the pair, in that order
         const float phi_o = __shfl_xor_sync(0xffffffffu, phi, 16), dphi_o = __shfl_xor_sync(0xffffffffu, dphi, 16);
         const float phi_t = h ? phi_o + phi : phi + phi_o, dphi_t = h ? dphi_o + dphi : dphi + dphi_o;
         if (valid && h == 0) {
             wo[(long long)f * n + p] = phi_t;
-            bo[(long long)f * n + p] = -dphi_t * invg2 * -na;
+            bo[(long long)f * n + p] = (dphi_t / sc) * invg2 * na;   // -(sum w d G / gamma^2) a
         }
     }
     // block sum of acc: lanes of a half, then warps, in fixed orders
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        float v = acc[i];
+    for (int ip = 0; ip < 16; ++ip) {
+        float v0 = lo(acc2[ip]), v1 = hi(acc2[ip]);
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if ((lane & 15) == 0) red[warp][2 * i + h] = v;
+        for (int o = 8; o > 0; o >>= 1) {
+            v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+            v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+        }
+        if ((lane & 15) == 0) {
+            red[warp][4 * ip + h] = v0;
+            red[warp][4 * ip + 2 + h] = v1;
+        }
     }
     __syncthreads();
     if (threadIdx.x < 64) {

@@ -967,6 +967,17 @@ struct TcKgArgs {
 };
 
 constexpr int kKgTH = 8;     // tile rows
+constexpr int kKgS = 4;      // Bm prefetch depth (chunks in flight, cp.async)
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void *src, int bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int K, int NK>
 __global__ void __launch_bounds__(512, 1) tc_kgrad_kernel(const __grid_constant__ TcKgArgs a) {
@@ -981,7 +992,8 @@ __global__ void __launch_bounds__(512, 1) tc_kgrad_kernel(const __grid_constant_
     float *s_bm = reinterpret_cast<float *>(smem4);   // [2 buffers][b_hi, b_lo, w_hi, w_lo][BMF]
     float *s_u = s_bm + 8 * BMF;                      // [UH][UW], E(u)
     float *s_e = s_u + round4(UH * UW);               // [UH][UW], E(e) (R1: raw e where used)
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(s_e + round4(UH * UW));   // [2]
+    float *s_st = s_e + round4(UH * UW);              // [kKgS][2 maps][NK][32] raw b, w (prefetch ring)
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(s_st + kKgS * 2 * BMF);   // [2]
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(mbar + 2);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = warp & 3;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
@@ -1009,6 +1021,39 @@ __global__ void __launch_bounds__(512, 1) tc_kgrad_kernel(const __grid_constant_
     const int t = q * 32 + lane;                     // this thread's tap (A builders)
     const int ta = t / K, tb = t - (t / K) * K;
     const int sub = warp >> 2;                       // A builders: pixels 8 sub .. 8 sub + 7 of a chunk
+    // Bm builders (lane quarters >= QA): float4 slots j = bt, bt + nbt, ... of a
+    // chunk's 2 x NK x 32 values, prefetched kKgS - 1 chunks ahead into their own
+    // ring slots with cp.async (zero-filled outside the image)
+    const int nbt = 512 - QA * 128;
+    const int bt = ((warp >> 2) * (4 - QA) + (q - QA)) * 32 + lane;
+    const int nch = 2 * kKgTH * ((ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1);   // this CTA's chunks
+    auto prefetch = [&](int cc) {
+        if (cc < nch) {
+            const int tile = blockIdx.x + (cc / (2 * kKgTH)) * gridDim.x, chh = cc % (2 * kKgTH);
+            const int bi = tile / per_img, rem = tile - bi * per_img;
+            const int ty = rem / a.tiles_x, x0 = (rem - ty * a.tiles_x) * kTcVW;
+            const int gy = ty * kKgTH + (chh >> 1), xb = x0 + (chh & 1) * 32;
+            const uint32_t st = smem_u32(s_st + (cc % kKgS) * 2 * BMF);
+            for (int j = bt; j < 2 * NK * 8; j += nbt) {
+                const int fl = j & 7, kq = (j >> 3) & 7, fg = (j >> 6) % (NK / 8), map = j / (8 * NK);
+                const int gx = xb + 4 * kq;
+                const int valid = gy < H ? min(max(W - gx, 0), 4) : 0;
+                const float *mb = map ? a.w : a.b;
+                const float *src = valid > 0 ? mb + (long long)(fg * 8 + fl) * n + (long long)bi * H * W +
+                                                   (long long)gy * W + gx
+                                             : mb;
+                if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+                    cp_async16(st + 16 * j, src, 4 * valid);
+                } else {
+#pragma unroll
+                    for (int e4 = 0; e4 < 4; ++e4) cp_async4(st + 16 * j + 4 * e4, e4 < valid ? src + e4 : mb, e4 < valid ? 4 : 0);
+                }
+            }
+        }
+        cp_async_commit();
+    };
+    if (q >= QA)
+        for (int cc = 0; cc < kKgS - 1; ++cc) prefetch(cc);
     int chunk = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int bi = tile / per_img, rem = tile - bi * per_img;
@@ -1078,26 +1123,13 @@ __global__ void __launch_bounds__(512, 1) tc_kgrad_kernel(const __grid_constant_
                 tmem_st8(base + 64, oh);
                 tmem_st8(base + 96, ol);
             } else {        // Bm: b and w of this chunk's 32 pixels, float4 per (map, filter, 4 pixels)
-                const int nbt = 512 - QA * 128;                          // builder threads (lane quarters >= QA)
-                const int bt = ((warp >> 2) * (4 - QA) + (q - QA)) * 32 + lane;   // this one's index
+                prefetch(chunk + kKgS - 1);
+                cp_async_wait<kKgS - 1>();   // this thread's copies of this chunk have landed
                 float *sb = s_bm + bb * 4 * BMF;
-                const bool rowin = gy < H;
-                const long long pbase = (long long)bi * H * W + (long long)gy * W + x0 + xc0;
+                const float *st = s_st + (chunk % kKgS) * 2 * BMF;
                 for (int j = bt; j < 2 * NK * 8; j += nbt) {
                     const int fl = j & 7, kq = (j >> 3) & 7, fg = (j >> 6) % (NK / 8), map = j / (8 * NK);
-                    const int f = fg * 8 + fl, gx = x0 + xc0 + 4 * kq;
-                    const float *src = (map ? a.w : a.b) + (long long)f * n + pbase + 4 * kq;
-                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (rowin) {
-                        if (gx + 3 < W && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-                            v = __ldg(reinterpret_cast<const float4 *>(src));
-                        } else {
-                            if (gx < W) v.x = __ldg(src);
-                            if (gx + 1 < W) v.y = __ldg(src + 1);
-                            if (gx + 2 < W) v.z = __ldg(src + 2);
-                            if (gx + 3 < W) v.w = __ldg(src + 3);
-                        }
-                    }
+                    const float4 v = *reinterpret_cast<const float4 *>(st + 4 * j);
                     const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
                     const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
                     const int o = (fg * 8 + kq) * 32 + fl * 4;
@@ -1126,6 +1158,7 @@ __global__ void __launch_bounds__(512, 1) tc_kgrad_kernel(const __grid_constant_
             }
         }
     }
+    cp_async_wait<0>();
     // the last chunk's commit covers every MMA of this CTA
     if (chunk > 0) mbar_wait(mbar + ((chunk - 1) & 1), ((chunk - 1) >> 1) & 1);
     tc_fence_after();
@@ -1154,7 +1187,7 @@ cudaError_t launch_tc_kg(const float *u, const float *e, const float *b, const f
                          int W, float *partial, int nblk, cudaStream_t s) {
     constexpr int R = K / 2, UW = kTcVW + 2 * R + 1, UH = kKgTH + 2 * R;
     TcKgArgs a{u, e, b, w, partial, boundary, B, H, W, (W + kTcVW - 1) / kTcVW, (H + kKgTH - 1) / kKgTH};
-    const size_t smem = sizeof(float) * (8 * (size_t)NK * 32 + 2 * (size_t)round4(UH * UW) + 8);
+    const size_t smem = sizeof(float) * ((8 + 2 * kKgS) * (size_t)NK * 32 + 2 * (size_t)round4(UH * UW) + 8);
     cudaError_t err = cudaFuncSetAttribute(tc_kgrad_kernel<K, NK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     if (nblk > 0) tc_kgrad_kernel<K, NK><<<(unsigned)nblk, 512, smem, s>>>(a);
