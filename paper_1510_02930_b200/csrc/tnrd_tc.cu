@@ -957,8 +957,10 @@ cudaError_t launch_tc_fwd(const float *in, const float *bf, float *out, int B, i
 // shared memory in the K-major core-matrix layout; 3xTF32 as in the stage kernel.
 // Two accumulators (inner, outer) stay in TMEM for the CTA's whole pixel range;
 // each CTA writes its D once to `partial` in the layout reduce_f_kernel sums.
-// Work: 32-pixel chunks (half a tile row of a 64 x kKgTH tile), double-buffered in
-// TMEM and shared memory; one CTA per SM, tiles grid-strided over the CTAs.
+// Work: 32-pixel chunks (half a tile row of a 64 x kKgTH tile), kKgBuf chunks in
+// flight in TMEM and shared memory between 16 builder warps and one MMA warp
+// (mbarriers full / empty); b and w arrive through a cp.async ring kKgS - 1 chunks
+// ahead; one CTA per SM, tiles grid-strided over the CTAs.
 struct TcKgArgs {
     const float *u, *e;       // [B][H][W]
     const float *b, *w;       // [NK][B*H*W]
@@ -968,6 +970,9 @@ struct TcKgArgs {
 
 constexpr int kKgTH = 8;     // tile rows
 constexpr int kKgS = 4;      // Bm prefetch depth (chunks in flight, cp.async)
+constexpr int kKgBuf = 3;    // chunks in TMEM / shared memory between the builders and the MMA warp
+constexpr int kKgBuilders = 512;              // 16 builder warps
+constexpr int kKgThreads = kKgBuilders + 32;  // + the MMA warp
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, int bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
@@ -980,189 +985,204 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int K, int NK>
-__global__ void __launch_bounds__(512, 1) tc_kgrad_kernel(const __grid_constant__ TcKgArgs a) {
-    constexpr int R = K / 2, KT = K * K, UW = kTcVW + 2 * R + 1, UH = kKgTH + 2 * R;
+__global__ void __launch_bounds__(kKgThreads, 1) tc_kgrad_kernel(const __grid_constant__ TcKgArgs a) {
+    constexpr int R = K / 2, KT = K * K, UW = kTcVW + 2 * R + 1, UH = kKgTH + 2 * R, UT = round4(UH * UW);
     constexpr int QA = (KT + 31) / 32;          // TMEM lane quarters holding taps
     constexpr int BMF = NK * 32;                // floats of one (map, hi|lo) Bm block
     constexpr uint32_t SBO = (32 / 4) * 128;    // 8-filter groups, 32 pixels of K
     constexpr uint32_t id = idesc_tf32(NK);
-    constexpr uint32_t kDin = 256, kDout = 256 + 64;   // TMEM columns of the accumulators
-    static_assert(NK % 8 == 0 && NK <= 64, "N_k");
+    constexpr uint32_t kDin = kKgBuf * 128, kDout = kDin + 64;   // TMEM columns of the accumulators
+    static_assert(NK % 8 == 0 && NK <= 64 && kDout + NK <= 512, "N_k");
     extern __shared__ __align__(1024) float4 smem4[];
-    float *s_bm = reinterpret_cast<float *>(smem4);   // [2 buffers][b_hi, b_lo, w_hi, w_lo][BMF]
-    float *s_u = s_bm + 8 * BMF;                      // [UH][UW], E(u)
-    float *s_e = s_u + round4(UH * UW);               // [UH][UW], E(e) (R1: raw e where used)
-    float *s_st = s_e + round4(UH * UW);              // [kKgS][2 maps][NK][32] raw b, w (prefetch ring)
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(s_st + kKgS * 2 * BMF);   // [2]
-    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(mbar + 2);
+    float *s_bm = reinterpret_cast<float *>(smem4);   // [kKgBuf][b_hi, b_lo, w_hi, w_lo][BMF]
+    float *s_u = s_bm + kKgBuf * 4 * BMF;             // [2 tiles][UH][UW], E(u)
+    float *s_e = s_u + 2 * UT;                        // [2 tiles][UH][UW], E(e) (R1: raw e where used)
+    float *s_st = s_e + 2 * UT;                       // [kKgS][2 maps][NK][32] raw b, w (prefetch ring)
+    uint64_t *full = reinterpret_cast<uint64_t *>(s_st + kKgS * 2 * BMF);   // [kKgBuf] builders -> MMA
+    uint64_t *empty = full + kKgBuf;                                        // [kKgBuf] MMA -> builders
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(empty + kKgBuf);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = warp & 3;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const int H = a.H, W = a.W;
     const long long n = (long long)a.B * H * W;
     const int per_img = a.tiles_x * a.tiles_y, ntiles = a.B * per_img;
+    const int nch = 2 * kKgTH * ((ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1);   // this CTA's chunks
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_tmem)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + 1)));
+        for (int i = 0; i < kKgBuf; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(full + i)), "r"(kKgBuilders / 32));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(empty + i)));
+        }
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *s_tmem, tl = tmem + lane_off;
-    // A rows >= QA*32 (lane quarters without taps) stay zero: write them once
-    if (q >= QA) {
-        const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int c = (warp >> 2) * 8; c < 256; c += 32) tmem_st8(tl + c, z);
-    }
-    const int t = q * 32 + lane;                     // this thread's tap (A builders)
-    const int ta = t / K, tb = t - (t / K) * K;
-    const int sub = warp >> 2;                       // A builders: pixels 8 sub .. 8 sub + 7 of a chunk
-    // Bm builders (lane quarters >= QA): float4 slots j = bt, bt + nbt, ... of a
-    // chunk's 2 x NK x 32 values, prefetched kKgS - 1 chunks ahead into their own
-    // ring slots with cp.async (zero-filled outside the image)
-    const int nbt = 512 - QA * 128;
-    const int bt = ((warp >> 2) * (4 - QA) + (q - QA)) * 32 + lane;
-    const int nch = 2 * kKgTH * ((ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1);   // this CTA's chunks
-    auto prefetch = [&](int cc) {
-        if (cc < nch) {
-            const int tile = blockIdx.x + (cc / (2 * kKgTH)) * gridDim.x, chh = cc % (2 * kKgTH);
-            const int bi = tile / per_img, rem = tile - bi * per_img;
-            const int ty = rem / a.tiles_x, x0 = (rem - ty * a.tiles_x) * kTcVW;
-            const int gy = ty * kKgTH + (chh >> 1), xb = x0 + (chh & 1) * 32;
-            const uint32_t st = smem_u32(s_st + (cc % kKgS) * 2 * BMF);
-            for (int j = bt; j < 2 * NK * 8; j += nbt) {
-                const int fl = j & 7, kq = (j >> 3) & 7, fg = (j >> 6) % (NK / 8), map = j / (8 * NK);
-                const int gx = xb + 4 * kq;
-                const int valid = gy < H ? min(max(W - gx, 0), 4) : 0;
-                const float *mb = map ? a.w : a.b;
-                const float *src = valid > 0 ? mb + (long long)(fg * 8 + fl) * n + (long long)bi * H * W +
-                                                   (long long)gy * W + gx
-                                             : mb;
-                if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-                    cp_async16(st + 16 * j, src, 4 * valid);
-                } else {
-#pragma unroll
-                    for (int e4 = 0; e4 < 4; ++e4) cp_async4(st + 16 * j + 4 * e4, e4 < valid ? src + e4 : mb, e4 < valid ? 4 : 0);
-                }
-            }
-        }
-        cp_async_commit();
-    };
-    if (q >= QA)
-        for (int cc = 0; cc < kKgS - 1; ++cc) prefetch(cc);
-    int chunk = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int bi = tile / per_img, rem = tile - bi * per_img;
-        const int ty = rem / a.tiles_x, x0 = (rem - ty * a.tiles_x) * kTcVW, y0 = ty * kKgTH;
-        const float *ub = a.u + (long long)bi * H * W, *eb = a.e + (long long)bi * H * W;
-        __syncthreads();   // the previous tile's A builds are done with s_u / s_e
-        for (int j = tid; j < UH * (UW - 1); j += 512) {
-            const int r = j / (UW - 1), c = j - r * (UW - 1);
-            const long long o = (long long)reflect(y0 - R + r, H) * W + reflect(x0 - R + c, W);
-            s_u[r * UW + c] = __ldg(ub + o);
-            s_e[r * UW + c] = __ldg(eb + o);
-        }
-        __syncthreads();
-        for (int ch = 0; ch < 2 * kKgTH; ++ch, ++chunk) {
-            const int bb = chunk & 1, yr = ch >> 1, xc0 = (ch & 1) * 32;
-            if (chunk >= 2) mbar_wait(mbar + bb, ((chunk - 2) >> 1) & 1);   // MMAs of chunk - 2 done
+    if (warp == kKgBuilders / 32) {
+        // MMA warp: chunk c in buffer c % kKgBuf once its 16 builder warps arrived
+        for (int c = 0; c < nch; ++c) {
+            const int bb = c % kKgBuf;
+            mbar_wait(full + bb, (c / kKgBuf) & 1);
             tc_fence_after();
-            const int gy = y0 + yr;
-            if (q < QA) {   // A: lane t = tap t, 8 pixels per thread
-                uint32_t ih[8], il[8], oh[8], ol[8];
-                const int xc = xc0 + 8 * sub;
-                const float *pu = s_u + (yr + 2 * R - ta) * UW + xc + 2 * R - tb;
-                const bool r1edge = a.boundary == 0 &&
-                                    (gy < R || gy >= H - R || x0 + xc < R || x0 + xc + 7 >= W - R);
+            const uint32_t ab = tmem + bb * 128, sb = smem_u32(s_bm + bb * 4 * BMF);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    float vi = 0.0f, vo = 0.0f;
-                    if (t < KT) {
-                        vi = pu[i];
-                        if (a.boundary == 1) {
-                            vo = s_e[(yr + 2 * R - ta) * UW + xc + i + 2 * R - tb];
-                        } else if (!r1edge) {
-                            vo = s_e[(yr + ta) * UW + xc + i + tb];
-                        }
-                    }
-                    const float hi_i = tf32_hi(vi), hi_o = tf32_hi(vo);
-                    ih[i] = __float_as_uint(hi_i); il[i] = __float_as_uint(vi - hi_i);
-                    oh[i] = __float_as_uint(hi_o); ol[i] = __float_as_uint(vo - hi_o);
-                }
-                if (r1edge && t < KT) {   // Ẽ_t(q): every in-image preimage p of q (warp-uniform branch)
-                    const int dy = ta - R, dx = tb - R;
-                    for (int i = 0; i < 8; ++i) {
-                        const int qy = gy, qx = x0 + xc + i;
-                        float s = 0.0f;
-                        if (qy < H && qx < W) {
-                            const int cy[3] = {qy + dy, dy - 1 - qy, 2 * H - 1 - qy + dy};
-                            const int cx[3] = {qx + dx, dx - 1 - qx, 2 * W - 1 - qx + dx};
-#pragma unroll
-                            for (int iy = 0; iy < 3; ++iy) {
-                                const int py = cy[iy];
-                                if (py < 0 || py >= H || reflect(py - dy, H) != qy) continue;
-#pragma unroll
-                                for (int ix = 0; ix < 3; ++ix) {
-                                    const int px = cx[ix];
-                                    if (px < 0 || px >= W || reflect(px - dx, W) != qx) continue;
-                                    s += __ldg(eb + (long long)py * W + px);
-                                }
-                            }
-                        }
-                        const float hs = tf32_hi(s);
-                        oh[i] = __float_as_uint(hs); ol[i] = __float_as_uint(s - hs);
-                    }
-                }
-                const uint32_t base = tl + bb * 128 + 8 * sub;
-                tmem_st8(base, ih);
-                tmem_st8(base + 32, il);
-                tmem_st8(base + 64, oh);
-                tmem_st8(base + 96, ol);
-            } else {        // Bm: b and w of this chunk's 32 pixels, float4 per (map, filter, 4 pixels)
-                prefetch(chunk + kKgS - 1);
-                cp_async_wait<kKgS - 1>();   // this thread's copies of this chunk have landed
-                float *sb = s_bm + bb * 4 * BMF;
-                const float *st = s_st + (chunk % kKgS) * 2 * BMF;
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t ko = 256 * k;
+                mma_tf32_warp(tmem + kDin, ab + 32 + 8 * k, umma_desc(sb + ko, SBO), id, c > 0 || k > 0);
+                mma_tf32_warp(tmem + kDin, ab + 8 * k, umma_desc(sb + 4 * BMF + ko, SBO), id, 1);
+                mma_tf32_warp(tmem + kDin, ab + 8 * k, umma_desc(sb + ko, SBO), id, 1);
+                mma_tf32_warp(tmem + kDout, ab + 96 + 8 * k, umma_desc(sb + 8 * BMF + ko, SBO), id, c > 0 || k > 0);
+                mma_tf32_warp(tmem + kDout, ab + 64 + 8 * k, umma_desc(sb + 12 * BMF + ko, SBO), id, 1);
+                mma_tf32_warp(tmem + kDout, ab + 64 + 8 * k, umma_desc(sb + 8 * BMF + ko, SBO), id, 1);
+            }
+            mma_commit_warp(empty + bb);
+        }
+    } else {
+        // A rows >= QA*32 (lane quarters without taps) stay zero: write them once
+        if (q >= QA) {
+            const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int c = (warp >> 2) * 8; c < kKgBuf * 128; c += 32) tmem_st8(tl + c, z);
+            tc_wait_st();
+        }
+        const int t = q * 32 + lane;                     // this thread's tap (A builders)
+        const int ta = t / K, tb = t - (t / K) * K;
+        const int sub = warp >> 2;                       // A builders: pixels 8 sub .. 8 sub + 7 of a chunk
+        // Bm builders (lane quarters >= QA): float4 slots j = bt, bt + nbt, ... of a
+        // chunk's 2 x NK x 32 values, prefetched kKgS - 1 chunks ahead into their own
+        // ring slots with cp.async (zero-filled outside the image)
+        const int nbt = kKgBuilders - QA * 128;
+        const int bt = ((warp >> 2) * (4 - QA) + (q - QA)) * 32 + lane;
+        auto prefetch = [&](int cc) {
+            if (cc < nch) {
+                const int tile = blockIdx.x + (cc / (2 * kKgTH)) * gridDim.x, chh = cc % (2 * kKgTH);
+                const int bi = tile / per_img, rem = tile - bi * per_img;
+                const int ty = rem / a.tiles_x, x0 = (rem - ty * a.tiles_x) * kTcVW;
+                const int gy = ty * kKgTH + (chh >> 1), xb = x0 + (chh & 1) * 32;
+                const uint32_t st = smem_u32(s_st + (cc % kKgS) * 2 * BMF);
                 for (int j = bt; j < 2 * NK * 8; j += nbt) {
                     const int fl = j & 7, kq = (j >> 3) & 7, fg = (j >> 6) % (NK / 8), map = j / (8 * NK);
-                    const float4 v = *reinterpret_cast<const float4 *>(st + 4 * j);
-                    const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-                    const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-                    const int o = (fg * 8 + kq) * 32 + fl * 4;
-                    *reinterpret_cast<float4 *>(sb + (2 * map) * BMF + o) = h;
-                    *reinterpret_cast<float4 *>(sb + (2 * map + 1) * BMF + o) = l;
+                    const int gx = xb + 4 * kq;
+                    const int valid = gy < H ? min(max(W - gx, 0), 4) : 0;
+                    const float *mb = map ? a.w : a.b;
+                    const float *src = valid > 0 ? mb + (long long)(fg * 8 + fl) * n + (long long)bi * H * W +
+                                                       (long long)gy * W + gx
+                                                 : mb;
+                    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+                        cp_async16(st + 16 * j, src, 4 * valid);
+                    } else {
+#pragma unroll
+                        for (int e4 = 0; e4 < 4; ++e4)
+                            cp_async4(st + 16 * j + 4 * e4, e4 < valid ? src + e4 : mb, e4 < valid ? 4 : 0);
+                    }
                 }
             }
-            tc_wait_st();
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            tc_fence_before();
-            __syncthreads();
-            if (warp == 0) {
+            cp_async_commit();
+        };
+        if (q >= QA)
+            for (int cc = 0; cc < kKgS - 1; ++cc) prefetch(cc);
+        int chunk = 0, it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int bi = tile / per_img, rem = tile - bi * per_img;
+            const int ty = rem / a.tiles_x, x0 = (rem - ty * a.tiles_x) * kTcVW, y0 = ty * kKgTH;
+            const float *ub = a.u + (long long)bi * H * W, *eb = a.e + (long long)bi * H * W;
+            // tiles alternate between two u / e buffers: the one written here was last
+            // read in tile it - 2, which every builder finished before the barrier of it - 1
+            float *tu = s_u + (it & 1) * UT, *te = s_e + (it & 1) * UT;
+            for (int j = tid; j < UH * (UW - 1); j += kKgBuilders) {
+                const int r = j / (UW - 1), c = j - r * (UW - 1);
+                const long long o = (long long)reflect(y0 - R + r, H) * W + reflect(x0 - R + c, W);
+                tu[r * UW + c] = __ldg(ub + o);
+                te[r * UW + c] = __ldg(eb + o);
+            }
+            named_sync(1, kKgBuilders);
+            for (int ch = 0; ch < 2 * kKgTH; ++ch, ++chunk) {
+                const int bb = chunk % kKgBuf, yr = ch >> 1, xc0 = (ch & 1) * 32;
+                if (chunk >= kKgBuf) mbar_wait(empty + bb, (chunk / kKgBuf - 1) & 1);   // MMAs of chunk - kKgBuf done
                 tc_fence_after();
-                const uint32_t ab = tmem + bb * 128, sb = smem_u32(s_bm + bb * 4 * BMF);
+                const int gy = y0 + yr;
+                if (q < QA) {   // A: lane t = tap t, 8 pixels per thread
+                    uint32_t ih[8], il[8], oh[8], ol[8];
+                    const int xc = xc0 + 8 * sub;
+                    const float *pu = tu + (yr + 2 * R - ta) * UW + xc + 2 * R - tb;
+                    const bool r1edge = a.boundary == 0 &&
+                                        (gy < R || gy >= H - R || x0 + xc < R || x0 + xc + 7 >= W - R);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t ko = 256 * k;
-                    mma_tf32_warp(tmem + kDin, ab + 32 + 8 * k, umma_desc(sb + ko, SBO), id, chunk > 0 || k > 0);
-                    mma_tf32_warp(tmem + kDin, ab + 8 * k, umma_desc(sb + 4 * BMF + ko, SBO), id, 1);
-                    mma_tf32_warp(tmem + kDin, ab + 8 * k, umma_desc(sb + ko, SBO), id, 1);
-                    mma_tf32_warp(tmem + kDout, ab + 96 + 8 * k, umma_desc(sb + 8 * BMF + ko, SBO), id, chunk > 0 || k > 0);
-                    mma_tf32_warp(tmem + kDout, ab + 64 + 8 * k, umma_desc(sb + 12 * BMF + ko, SBO), id, 1);
-                    mma_tf32_warp(tmem + kDout, ab + 64 + 8 * k, umma_desc(sb + 8 * BMF + ko, SBO), id, 1);
+                    for (int i = 0; i < 8; ++i) {
+                        float vi = 0.0f, vo = 0.0f;
+                        if (t < KT) {
+                            vi = pu[i];
+                            if (a.boundary == 1) {
+                                vo = te[(yr + 2 * R - ta) * UW + xc + i + 2 * R - tb];
+                            } else if (!r1edge) {
+                                vo = te[(yr + ta) * UW + xc + i + tb];
+                            }
+                        }
+                        const float hi_i = tf32_hi(vi), hi_o = tf32_hi(vo);
+                        ih[i] = __float_as_uint(hi_i); il[i] = __float_as_uint(vi - hi_i);
+                        oh[i] = __float_as_uint(hi_o); ol[i] = __float_as_uint(vo - hi_o);
+                    }
+                    if (r1edge && t < KT) {   // Ẽ_t(q): every in-image preimage p of q (warp-uniform branch)
+                        const int dy = ta - R, dx = tb - R;
+                        for (int i = 0; i < 8; ++i) {
+                            const int qy = gy, qx = x0 + xc + i;
+                            float sum = 0.0f;
+                            if (qy < H && qx < W) {
+                                const int cy[3] = {qy + dy, dy - 1 - qy, 2 * H - 1 - qy + dy};
+                                const int cx[3] = {qx + dx, dx - 1 - qx, 2 * W - 1 - qx + dx};
+#pragma unroll
+                                for (int iy = 0; iy < 3; ++iy) {
+                                    const int py = cy[iy];
+                                    if (py < 0 || py >= H || reflect(py - dy, H) != qy) continue;
+#pragma unroll
+                                    for (int ix = 0; ix < 3; ++ix) {
+                                        const int px = cx[ix];
+                                        if (px < 0 || px >= W || reflect(px - dx, W) != qx) continue;
+                                        sum += __ldg(eb + (long long)py * W + px);
+                                    }
+                                }
+                            }
+                            const float hs = tf32_hi(sum);
+                            oh[i] = __float_as_uint(hs); ol[i] = __float_as_uint(sum - hs);
+                        }
+                    }
+                    const uint32_t base = tl + bb * 128 + 8 * sub;
+                    tmem_st8(base, ih);
+                    tmem_st8(base + 32, il);
+                    tmem_st8(base + 64, oh);
+                    tmem_st8(base + 96, ol);
+                    tc_wait_st();
+                    tc_fence_before();
+                } else {        // Bm: b and w of this chunk's 32 pixels, float4 per (map, filter, 4 pixels)
+                    prefetch(chunk + kKgS - 1);
+                    cp_async_wait<kKgS - 1>();   // this thread's copies of this chunk have landed
+                    float *sbm = s_bm + bb * 4 * BMF;
+                    const float *st = s_st + (chunk % kKgS) * 2 * BMF;
+                    for (int j = bt; j < 2 * NK * 8; j += nbt) {
+                        const int fl = j & 7, kq = (j >> 3) & 7, fg = (j >> 6) % (NK / 8), map = j / (8 * NK);
+                        const float4 v = *reinterpret_cast<const float4 *>(st + 4 * j);
+                        const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+                        const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+                        const int o = (fg * 8 + kq) * 32 + fl * 4;
+                        *reinterpret_cast<float4 *>(sbm + (2 * map) * BMF + o) = h;
+                        *reinterpret_cast<float4 *>(sbm + (2 * map + 1) * BMF + o) = l;
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
-                mma_commit_warp(mbar + bb);
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(full + bb)) : "memory");
             }
         }
+        cp_async_wait<0>();
     }
-    cp_async_wait<0>();
     // the last chunk's commit covers every MMA of this CTA
-    if (chunk > 0) mbar_wait(mbar + ((chunk - 1) & 1), ((chunk - 1) >> 1) & 1);
+    if (nch > 0) mbar_wait(empty + (nch - 1) % kKgBuf, ((nch - 1) / kKgBuf) & 1);
     tc_fence_after();
     if (warp < QA) {   // D lanes = taps: write inner / outer for this CTA
+        const int t = q * 32 + lane;
         uint32_t di[NK], dout[NK];
         tmem_ld_nowait<NK>(tl + kDin, di);
         tmem_ld_nowait<NK>(tl + kDout, dout);
@@ -1172,8 +1192,8 @@ __global__ void __launch_bounds__(512, 1) tc_kgrad_kernel(const __grid_constant_
 #pragma unroll
             for (int f = 0; f < NK; ++f) {
                 float *pp = a.partial + ((long long)f * gridDim.x + blockIdx.x) * 2 * KT;
-                pp[t] = chunk > 0 ? __uint_as_float(di[f]) : 0.0f;
-                pp[KT + t] = chunk > 0 ? __uint_as_float(dout[f]) : 0.0f;
+                pp[t] = nch > 0 ? __uint_as_float(di[f]) : 0.0f;
+                pp[KT + t] = nch > 0 ? __uint_as_float(dout[f]) : 0.0f;
             }
         }
     }
@@ -1187,10 +1207,10 @@ cudaError_t launch_tc_kg(const float *u, const float *e, const float *b, const f
                          int W, float *partial, int nblk, cudaStream_t s) {
     constexpr int R = K / 2, UW = kTcVW + 2 * R + 1, UH = kKgTH + 2 * R;
     TcKgArgs a{u, e, b, w, partial, boundary, B, H, W, (W + kTcVW - 1) / kTcVW, (H + kKgTH - 1) / kKgTH};
-    const size_t smem = sizeof(float) * ((8 + 2 * kKgS) * (size_t)NK * 32 + 2 * (size_t)round4(UH * UW) + 8);
+    const size_t smem = sizeof(float) * ((4 * kKgBuf + 2 * kKgS) * (size_t)NK * 32 + 4 * (size_t)round4(UH * UW) + 16);
     cudaError_t err = cudaFuncSetAttribute(tc_kgrad_kernel<K, NK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
-    if (nblk > 0) tc_kgrad_kernel<K, NK><<<(unsigned)nblk, 512, smem, s>>>(a);
+    if (nblk > 0) tc_kgrad_kernel<K, NK><<<(unsigned)nblk, kKgThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
