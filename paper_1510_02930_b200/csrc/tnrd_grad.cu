@@ -224,11 +224,19 @@ __global__ void __launch_bounds__(kGradThreads) adj_border_kernel(GradFilterArgs
 // (weights and accumulators in registers).  With sc = sqrt(log2 e / 2) / gamma and
 // d'_j = (x - mu_j) sc, G_j = 2^(-d'_j^2); phi' uses sum_j w_j d'_j G_j / sc.
 // phi and phi' are the two halves' sums, each half's pair lanes added low + high,
-// then half 0 + half 1 (fixed order).  Centres run in groups of two pairs behind
-// warp-uniform branches: a group is skipped when it lies entirely outside
+// then half 0 + half 1 (fixed order).  Pairs run in groups of TNRD_PHI_GP behind
+// warp-uniform branches: a group is skipped when all its centres lie outside
 // [jlo, jhi], the centres within dmax of some value of the warp; beyond dmax every
-// G_j is exactly 0 (ex2.approx.ftz of < -126 flushes), so skipping changes no sum.
+// G_j is exactly 0 (ex2.approx.ftz of < -126 flushes, kPhiCut = 126), so skipping
+// changes no sum.  (A cut at 2^-40 instead measured no faster: DESIGN.md §5.9.)
 constexpr int kPhiThreads = 256;
+#ifndef TNRD_PHI_CUT
+#define TNRD_PHI_CUT 126.0f
+#endif
+#ifndef TNRD_PHI_GP
+#define TNRD_PHI_GP 4
+#endif
+constexpr float kPhiCut = TNRD_PHI_CUT;   // 2^(-t) for t > kPhiCut is not evaluated (exactly 0 at 126)
 
 #ifndef TNRD_PHI_MINB
 #define TNRD_PHI_MINB 2
@@ -241,8 +249,8 @@ __global__ void __launch_bounds__(kPhiThreads, TNRD_PHI_MINB) phi_all_kernel(Gra
     const float mu0 = g.grid3[(g.fi0 + f) * 3], step = g.grid3[(g.fi0 + f) * 3 + 1], gam = g.grid3[(g.fi0 + f) * 3 + 2];
     const float sc = sqrtf(0.72134752044448170f) / gam;             // sqrt(log2(e) / 2) / gamma
     const float s2 = 2.0f * step * sc, base = fmaf((float)h, step, mu0), invg2 = 1.0f / (gam * gam);
-    // 2^(-t) is exactly 0 for t > 126, t = d^2 log2(e) / (2 gamma^2): |d| > dmax
-    const float dmax = sqrtf(126.0f / 0.72134752044448170f) * gam * 1.0001f + 1e-6f * (fabsf(mu0) + 64.0f * step);
+    // 2^(-t) = 0 (flushed) for t = d^2 log2(e) / (2 gamma^2) > kPhiCut = 126: |d| > dmax
+    const float dmax = sqrtf(kPhiCut / 0.72134752044448170f) * gam * 1.0001f + 1e-6f * (fabsf(mu0) + 64.0f * step);
     const float rstep = 1.0f / step;
     f2 w2[16], acc2[16];
 #pragma unroll
@@ -270,10 +278,10 @@ __global__ void __launch_bounds__(kPhiThreads, TNRD_PHI_MINB) phi_all_kernel(Gra
         const f2 na2 = bc(na);
         f2 phi2 = 0ull, dphi2 = 0ull;
 #pragma unroll
-        for (int g4 = 0; g4 < 8; ++g4) {
-            if (4 * g4 + 3 >= ilo && 4 * g4 <= ihi) {
+        for (int gg = 0; gg < 16 / TNRD_PHI_GP; ++gg) {
+            if (2 * TNRD_PHI_GP * gg + 2 * TNRD_PHI_GP - 1 >= ilo && 2 * TNRD_PHI_GP * gg <= ihi) {
 #pragma unroll
-                for (int ip = 2 * g4; ip < 2 * g4 + 2; ++ip) {
+                for (int ip = TNRD_PHI_GP * gg; ip < TNRD_PHI_GP * gg + TNRD_PHI_GP; ++ip) {
                     const f2 d2 = fma2(pk(-(float)(2 * ip), -(float)(2 * ip + 1)), bc(s2), bc(xs));
                     const f2 t2 = mul2(d2, d2);
                     const f2 G2 = pk(ex2_ftz(-lo(t2)), ex2_ftz(-hi(t2)));
