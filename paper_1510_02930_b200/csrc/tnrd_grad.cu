@@ -252,6 +252,7 @@ __global__ void __launch_bounds__(kPhiThreads, TNRD_PHI_MINB) phi_all_kernel(Gra
     // 2^(-t) = 0 (flushed) for t = d^2 log2(e) / (2 gamma^2) > kPhiCut = 126: |d| > dmax
     const float dmax = sqrtf(kPhiCut / 0.72134752044448170f) * gam * 1.0001f + 1e-6f * (fabsf(mu0) + 64.0f * step);
     const float rstep = 1.0f / step;
+    const f2 s2v = bc(s2), m2s2 = bc(-2.0f * s2);
     f2 w2[16], acc2[16];
 #pragma unroll
     for (int ip = 0; ip < 16; ++ip) {
@@ -277,12 +278,16 @@ __global__ void __launch_bounds__(kPhiThreads, TNRD_PHI_MINB) phi_all_kernel(Gra
         const float xs = (x - base) * sc;
         const f2 na2 = bc(na);
         f2 phi2 = 0ull, dphi2 = 0ull;
+        const f2 xs2 = bc(xs);
 #pragma unroll
         for (int gg = 0; gg < 16 / TNRD_PHI_GP; ++gg) {
             if (2 * TNRD_PHI_GP * gg + 2 * TNRD_PHI_GP - 1 >= ilo && 2 * TNRD_PHI_GP * gg <= ihi) {
+                // d' of the group's first pair from its constants, later pairs by
+                // steps of -2 s2 (one FADD2 each)
+                f2 d2 = fma2(pk(-(float)(2 * TNRD_PHI_GP * gg), -(float)(2 * TNRD_PHI_GP * gg + 1)), s2v, xs2);
 #pragma unroll
                 for (int ip = TNRD_PHI_GP * gg; ip < TNRD_PHI_GP * gg + TNRD_PHI_GP; ++ip) {
-                    const f2 d2 = fma2(pk(-(float)(2 * ip), -(float)(2 * ip + 1)), bc(s2), bc(xs));
+                    if (ip > TNRD_PHI_GP * gg) d2 = add2(d2, m2s2);
                     const f2 t2 = mul2(d2, d2);
                     const f2 G2 = pk(ex2_ftz(-lo(t2)), ex2_ftz(-hi(t2)));
                     phi2 = fma2(w2[ip], G2, phi2);
