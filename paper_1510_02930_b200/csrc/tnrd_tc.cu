@@ -825,7 +825,8 @@ namespace {
 // Tensor-core forward bank for the training gradient (tnrd_grad.cu): out[f][p] =
 // (k_f * E(in))(p) for all filters, the stage kernel's 3xTF32 implicit GEMM on
 // output pixels (M-block = two 64-pixel output rows; no halo), written to HBM in
-// filter-major maps.  Simple serial form, 512 threads.
+// filter-major maps.  512 threads, two TMEM slots: block i's MMA overlaps the
+// build of block i + 1 and the read-back of block i - 1.
 struct TcFwdArgs {
     const float *in;   // [B][H][W]
     const float *bf;   // bf_hi [NK x KTP], then bf_lo
@@ -841,8 +842,8 @@ __global__ void __launch_bounds__(512, 1) tc_fwdbank_kernel(const __grid_constan
     extern __shared__ __align__(1024) float4 smem4[];
     float *s_bf = reinterpret_cast<float *>(smem4);           // [2][NK x KTP]
     float *s_u = s_bf + 2 * NK * KTP;                         // [UH][UW]
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(s_u + round4(UH * UW));
-    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(mbar + 1);
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(s_u + round4(UH * UW));   // [2]
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(mbar + 2);
     const int tid = threadIdx.x, warp = tid >> 5, wg = tid >> 7, m = tid & 127;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const int H = a.H, W = a.W;
@@ -857,25 +858,29 @@ __global__ void __launch_bounds__(512, 1) tc_fwdbank_kernel(const __grid_constan
         s_u[j] = __ldg(ib + (long long)reflect(y0 - R + r, H) * W + reflect(x0 - R + c, W));
     }
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(s_tmem)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_tmem)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + 1)));
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *s_tmem, tl = tmem + lane_off, tV = tmem + 128;
+    // two slots: A (hi, lo) at slot * 2 KTP, V at 4 KTP + slot * NK; block i's MMA
+    // runs while block i + 1 is built and block i - 1 is read back
+    const uint32_t tmem = *s_tmem, tl = tmem + lane_off;
     const uint32_t bf_hi = smem_u32(s_bf), bf_lo = bf_hi + 4 * NK * KTP;
     constexpr uint32_t SBO_F = (KTP / 4) * 128;
     constexpr uint32_t id_f = idesc_tf32(NK);
-    uint32_t phase = 0;
-    for (int i = 0; i < kFwdOH / 2; ++i) {
-        const int y = 2 * i + (m >> 6), x = m & 63;     // output pixel of lane m (tile coordinates)
-        {   // im2col row (hi, lo): tap (ta, tb) reads u(y + R - ta, x + R - tb), tile offset R
+    constexpr int NB = kFwdOH / 2;
+    for (int i = 0; i <= NB; ++i) {
+        const int sl = i & 1;
+        if (i < NB) {   // im2col row (hi, lo) of block i: tap (ta, tb) reads u(y + R - ta, x + R - tb), tile offset R
+            const int y = 2 * i + (m >> 6), x = m & 63;
             const float *up = s_u + (y + 2 * R) * UW + x + 2 * R;
 #pragma unroll
             for (int ch = 0; ch < KTP / 8; ++ch) {
@@ -890,51 +895,49 @@ __global__ void __launch_bounds__(512, 1) tc_fwdbank_kernel(const __grid_constan
                     hv[e] = __float_as_uint(vh);
                     lv[e] = __float_as_uint(v - vh);
                 }
-                tmem_st8(tl + ch * 8, hv);
-                tmem_st8(tl + KTP + ch * 8, lv);
+                tmem_st8(tl + sl * 2 * KTP + ch * 8, hv);
+                tmem_st8(tl + sl * 2 * KTP + KTP + ch * 8, lv);
             }
+            tc_wait_st();
         }
-        tc_wait_st();
         tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
+        __syncthreads();   // A(i) written; every thread has read V(i - 2)
+        if (i < NB && warp == 0) {
             tc_fence_after();
+            const uint32_t tA = tmem + sl * 2 * KTP, tV = tmem + 4 * KTP + sl * NK;
 #pragma unroll
             for (int k = 0; k < KTP / 8; ++k) {
-                mma_tf32(tV, tmem + KTP + 8 * k, umma_desc(bf_hi + 256 * k, SBO_F), id_f, k > 0);
-                mma_tf32(tV, tmem + 8 * k, umma_desc(bf_lo + 256 * k, SBO_F), id_f, 1);
-                mma_tf32(tV, tmem + 8 * k, umma_desc(bf_hi + 256 * k, SBO_F), id_f, 1);
+                mma_tf32_warp(tV, tA + KTP + 8 * k, umma_desc(bf_hi + 256 * k, SBO_F), id_f, k > 0);
+                mma_tf32_warp(tV, tA + 8 * k, umma_desc(bf_lo + 256 * k, SBO_F), id_f, 1);
+                mma_tf32_warp(tV, tA + 8 * k, umma_desc(bf_hi + 256 * k, SBO_F), id_f, 1);
             }
-            mma_commit(mbar);
-            mbar_wait(mbar, phase);
+            mma_commit_warp(mbar + sl);
         }
-        phase ^= 1;
-        __syncthreads();
-        tc_fence_after();
-        {   // V -> out maps (this warpgroup's filters), lanes = consecutive pixels
+        if (i >= 1) {   // V(i - 1) -> out maps (this warpgroup's filters), lanes = consecutive pixels
+            const int ip = i - 1, sp = ip & 1;
+            mbar_wait(mbar + sp, (ip >> 1) & 1);
+            tc_fence_after();
             uint32_t vr[NFQ];
-            tmem_ld_nowait<NFQ>(tl + 128 + wg * NFQ, vr);
+            tmem_ld_nowait<NFQ>(tl + 4 * KTP + sp * NK + wg * NFQ, vr);
             tmem_wait_ld(vr);
-            const int gy = y0 + y, gx = x0 + x;
+            const int gy = y0 + 2 * ip + (m >> 6), gx = x0 + (m & 63);
             if (gy < H && gx < W) {
                 float *op = a.out + (long long)bi * H * W + (long long)gy * W + gx;
 #pragma unroll
                 for (int e = 0; e < NFQ; ++e) op[(long long)(wg * NFQ + e) * n] = __uint_as_float(vr[e]);
             }
         }
-        tc_fence_before();
-        __syncthreads();   // TMEM A / V columns are rewritten by the next block
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 template <int K, int NK>
 cudaError_t launch_tc_fwd(const float *in, const float *bf, float *out, int B, int H, int W, cudaStream_t s) {
     constexpr int R = K / 2;
     TcFwdArgs a{in, bf, out, B, H, W, (W + kTcVW - 1) / kTcVW, (H + kFwdOH - 1) / kFwdOH};
-    const size_t smem = sizeof(float) * (2 * (size_t)NK * tc_ktp(K) + round4((kFwdOH + 2 * R) * (kTcVW + 2 * R)) + 4);
+    const size_t smem = sizeof(float) * (2 * (size_t)NK * tc_ktp(K) + round4((kFwdOH + 2 * R) * (kTcVW + 2 * R)) + 8);
     cudaError_t e = cudaFuncSetAttribute(tc_fwdbank_kernel<K, NK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const long long nt = (long long)B * a.tiles_x * a.tiles_y;
