@@ -652,8 +652,9 @@ cudaError_t launch_tc(StageArgs &a, int B, cudaStream_t s) {
 // gn -= sum_f K_f^T b_f, K_f the symmetric-boundary convolution of the forward
 // bank, as one GEMM per M-block (Z[q][t] = sum_f b_f(q) k_f[t], 3xTF32) and the
 // exact-transpose gather of the stage kernel's R2 path (b = 0 outside the image,
-// mirror-image terms at image edges).  Simple serial form: one M-block at a time,
-// 512 threads (lane m of each warpgroup loads and splits NK/4 of the maps).
+// mirror-image terms at image edges).  512 threads (lane m of each warpgroup loads
+// and splits NK/4 of the maps, one block ahead); two TMEM slots, so block i's MMA
+// overlaps the gather of block i - 1.
 struct TcAdjArgs {
     const float *b;    // [NK][B*H*W]
     const float *ba;   // ba_hi [NZ x NK], then ba_lo
@@ -669,8 +670,8 @@ __global__ void __launch_bounds__(512, 1) tc_adjoint_kernel(const __grid_constan
     const int OH = a.oh, VH = OH + 2 * R;
     float *s_z = s_ba + 2 * NZ * NK;                          // [KT][kZP]
     float *s_d = s_z + KT * kZP;                              // [OH][OW]
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(s_d + round4(OH * OW));
-    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(mbar + 1);
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(s_d + round4(OH * OW));   // [2]
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(mbar + 2);
     const int tid = threadIdx.x, warp = tid >> 5, wg = tid >> 7, m = tid & 127;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const int H = a.H, W = a.W;
@@ -681,62 +682,73 @@ __global__ void __launch_bounds__(512, 1) tc_adjoint_kernel(const __grid_constan
     for (int j = tid; j < (2 * NZ * NK) / 4; j += 512) smem4[j] = __ldg(reinterpret_cast<const float4 *>(a.ba) + j);
     for (int j = tid; j < OH * OW; j += 512) s_d[j] = 0.0f;
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(s_tmem)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_tmem)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + 1)));
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *s_tmem, tl = tmem + lane_off, tZ = tmem + 128;
+    // two slots: W (hi, lo) at slot * 2 NK, Z at 256 + slot * NZ; block i's MMA runs
+    // while block i - 1 is gathered, and block i + 1's maps are already in flight
+    const uint32_t tmem = *s_tmem, tl = tmem + lane_off;
     const uint32_t ba_hi = smem_u32(s_ba), ba_lo = ba_hi + 4 * NZ * NK;
     constexpr uint32_t SBO_A = (NK / 4) * 128;
     constexpr uint32_t id_a = idesc_tf32(NZ);
+    static_assert(256 + 2 * NZ <= 512 && 4 * NK <= 256, "TMEM plan");
     const float *bb = a.b + (long long)bi * H * W;
-    uint32_t phase = 0;
     const int nmb = VH / 2;
-    for (int i = 0; i < nmb; ++i) {
-        {   // W (hi, lo) of pixel m: the b maps, 0 outside the image
-            const int gy = y0 - R + 2 * i + (m >> 6), gx = x0 - R + (m & 63);
-            const bool in = (unsigned)gy < (unsigned)H && (unsigned)gx < (unsigned)W;
-            const long long off = (long long)gy * W + gx;
+    float wv[NFQ];
+    const auto load_w = [&](int i) {   // the b maps of pixel m of block i, 0 outside the image
+        const int gy = y0 - R + 2 * i + (m >> 6), gx = x0 - R + (m & 63);
+        const bool in = (unsigned)gy < (unsigned)H && (unsigned)gx < (unsigned)W;
+        const long long off = (long long)gy * W + gx;
+#pragma unroll
+        for (int e = 0; e < NFQ; ++e) wv[e] = in ? __ldg(bb + (long long)(wg * NFQ + e) * n + off) : 0.0f;
+    };
+    load_w(0);
+    for (int i = 0; i <= nmb; ++i) {
+        const int sl = i & 1;
+        if (i < nmb) {
             uint32_t wh[NFQ], wl[NFQ];
 #pragma unroll
             for (int e = 0; e < NFQ; ++e) {
-                const float x = in ? __ldg(bb + (long long)(wg * NFQ + e) * n + off) : 0.0f;
-                const float xh = tf32_hi(x);
+                const float xh = tf32_hi(wv[e]);
                 wh[e] = __float_as_uint(xh);
-                wl[e] = __float_as_uint(x - xh);
+                wl[e] = __float_as_uint(wv[e] - xh);
             }
-            tmem_st<NFQ>(tl + wg * NFQ, wh);
-            tmem_st<NFQ>(tl + NK + wg * NFQ, wl);
+            tmem_st<NFQ>(tl + sl * 2 * NK + wg * NFQ, wh);
+            tmem_st<NFQ>(tl + sl * 2 * NK + NK + wg * NFQ, wl);
+            tc_wait_st();
+            if (i + 1 < nmb) load_w(i + 1);
         }
-        tc_wait_st();
         tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
+        __syncthreads();   // W(i) written; the gather of block i - 2 is done with s_z
+        if (i < nmb && warp == 0) {
             tc_fence_after();
+            const uint32_t tW = tmem + sl * 2 * NK, tZ = tmem + 256 + sl * NZ;
 #pragma unroll
             for (int k = 0; k < NK / 8; ++k) {
-                mma_tf32(tZ, tmem + NK + 8 * k, umma_desc(ba_hi + 256 * k, SBO_A), id_a, k > 0);
-                mma_tf32(tZ, tmem + 8 * k, umma_desc(ba_lo + 256 * k, SBO_A), id_a, 1);
-                mma_tf32(tZ, tmem + 8 * k, umma_desc(ba_hi + 256 * k, SBO_A), id_a, 1);
+                mma_tf32_warp(tZ, tW + NK + 8 * k, umma_desc(ba_hi + 256 * k, SBO_A), id_a, k > 0);
+                mma_tf32_warp(tZ, tW + 8 * k, umma_desc(ba_lo + 256 * k, SBO_A), id_a, 1);
+                mma_tf32_warp(tZ, tW + 8 * k, umma_desc(ba_hi + 256 * k, SBO_A), id_a, 1);
             }
-            mma_commit(mbar);
-            mbar_wait(mbar, phase);
+            mma_commit_warp(mbar + sl);
         }
-        phase ^= 1;
-        __syncthreads();
+        if (i == 0) continue;
+        const int ib = i - 1, sp = ib & 1;
+        mbar_wait(mbar + sp, (ib >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int ch = 0; ch < NZ / 8; ++ch) {
             if (ch % 4 != wg || ch * 8 >= KT) continue;
             uint32_t z[8];
-            tmem_ld_nowait<8>(tl + 128 + ch * 8, z);
+            tmem_ld_nowait<8>(tl + 256 + sp * NZ + ch * 8, z);
             tmem_wait_ld(z);
 #pragma unroll
             for (int e = 0; e < 8; ++e)
@@ -744,9 +756,9 @@ __global__ void __launch_bounds__(512, 1) tc_adjoint_kernel(const __grid_constan
         }
         tc_fence_before();
         __syncthreads();
-        // d(q) += sum_t sum_{x in M(q)} Z[x + a_t][t] over this block's rows (mirror
+        // d(q) += sum_t sum_{x in M(q)} Z[x + a_t][t] over block ib's rows (mirror
         // images M(q): q, across the nearest vertical / horizontal edge, both)
-        const int j0 = 2 * i;
+        const int j0 = 2 * ib;
         const auto S_cols = [&](int jj, int ta, int xc) {
             const float *zp = s_z + (ta * K) * kZP + jj * 64;
             float S = 0.0f;
@@ -782,7 +794,6 @@ __global__ void __launch_bounds__(512, 1) tc_adjoint_kernel(const __grid_constan
             }
             s_d[y * OW + x] = d;
         }
-        // the next block writes s_z only after two more CTA barriers
     }
     __syncthreads();
     float *gb = a.gn + (long long)bi * H * W;
@@ -792,14 +803,14 @@ __global__ void __launch_bounds__(512, 1) tc_adjoint_kernel(const __grid_constan
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 template <int K, int NK>
 cudaError_t launch_tc_adj(const float *b, const float *ba, float *gn, int B, int H, int W, int oh, cudaStream_t s) {
     constexpr int R = K / 2, OW = kTcVW - 2 * R;
     TcAdjArgs a{b, ba, gn, B, H, W, oh, (W + OW - 1) / OW, (H + oh - 1) / oh};
-    const size_t smem = sizeof(float) * (2 * (size_t)tc_nz(K) * NK + (size_t)K * K * kZP + round4(oh * OW) + 4);
+    const size_t smem = sizeof(float) * (2 * (size_t)tc_nz(K) * NK + (size_t)K * K * kZP + round4(oh * OW) + 8);
     cudaError_t e = cudaFuncSetAttribute(tc_adjoint_kernel<K, NK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const long long nt = (long long)B * a.tiles_x * a.tiles_y;
