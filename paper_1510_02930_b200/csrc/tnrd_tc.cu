@@ -1045,6 +1045,9 @@ __global__ void __launch_bounds__(kKgThreads, 1) tc_kgrad_kernel(const __grid_co
             const uint32_t ab = tmem + bb * 128, sb = smem_u32(s_bm + bb * 4 * BMF);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
+#ifdef TNRD_KG_EXP_NOMMA
+                if (c >= 0) break;
+#endif
                 const uint32_t ko = 256 * k;
                 mma_tf32_warp(tmem + kDin, ab + 32 + 8 * k, umma_desc(sb + ko, SBO), id, c > 0 || k > 0);
                 mma_tf32_warp(tmem + kDin, ab + 8 * k, umma_desc(sb + 4 * BMF + ko, SBO), id, 1);
@@ -1070,27 +1073,45 @@ __global__ void __launch_bounds__(kKgThreads, 1) tc_kgrad_kernel(const __grid_co
         // ring slots with cp.async (zero-filled outside the image)
         const int nbt = kKgBuilders - QA * 128;
         const int bt = ((warp >> 2) * (4 - QA) + (q - QA)) * 32 + lane;
+        // this thread's float4 slots j = bt + r nbt (r < NJ): per slot the map /
+        // filter offset in global memory, the pixel offset 4 kq within the chunk and
+        // the element offset in the canonical Bm block (all chunk-invariant)
+        constexpr int NJ = (2 * NK * 8 + (kKgBuilders - QA * 128) - 1) / (kKgBuilders - QA * 128);
+        long long goff[NJ];
+        int kq4[NJ], soff[NJ];
+#pragma unroll
+        for (int r = 0; r < NJ; ++r) {
+            const int j = bt + r * nbt;
+            const int fl = j & 7, kq = (j >> 3) & 7, fg = (j >> 6) % (NK / 8), map = j / (8 * NK);
+            goff[r] = (long long)(fg * 8 + fl) * n + (map ? (a.w - a.b) : 0);
+            kq4[r] = 4 * kq;
+            soff[r] = 2 * map * BMF + (fg * 8 + kq) * 32 + fl * 4;
+        }
+        // 16-byte copies need every chunk row segment 16-byte aligned
+        const bool al16 = (W % 4) == 0 && (n % 4) == 0 && ((reinterpret_cast<uintptr_t>(a.b) | reinterpret_cast<uintptr_t>(a.w)) & 15) == 0 &&
+                          ((a.w - a.b) % 4) == 0;
         auto prefetch = [&](int cc) {
             if (cc < nch) {
                 const int tile = blockIdx.x + (cc / (2 * kKgTH)) * gridDim.x, chh = cc % (2 * kKgTH);
                 const int bi = tile / per_img, rem = tile - bi * per_img;
                 const int ty = rem / a.tiles_x, x0 = (rem - ty * a.tiles_x) * kTcVW;
                 const int gy = ty * kKgTH + (chh >> 1), xb = x0 + (chh & 1) * 32;
+                const float *pb = a.b + (long long)bi * H * W + (long long)gy * W + xb;
+                const int wrem = gy < H ? W - xb : 0;          // valid pixels from xb on
                 const uint32_t st = smem_u32(s_st + (cc % kKgS) * 2 * BMF);
-                for (int j = bt; j < 2 * NK * 8; j += nbt) {
-                    const int fl = j & 7, kq = (j >> 3) & 7, fg = (j >> 6) % (NK / 8), map = j / (8 * NK);
-                    const int gx = xb + 4 * kq;
-                    const int valid = gy < H ? min(max(W - gx, 0), 4) : 0;
-                    const float *mb = map ? a.w : a.b;
-                    const float *src = valid > 0 ? mb + (long long)(fg * 8 + fl) * n + (long long)bi * H * W +
-                                                       (long long)gy * W + gx
-                                                 : mb;
-                    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-                        cp_async16(st + 16 * j, src, 4 * valid);
-                    } else {
 #pragma unroll
-                        for (int e4 = 0; e4 < 4; ++e4)
-                            cp_async4(st + 16 * j + 4 * e4, e4 < valid ? src + e4 : mb, e4 < valid ? 4 : 0);
+                for (int r = 0; r < NJ; ++r) {
+                    if (r < NJ - 1 || bt + r * nbt < 2 * NK * 8) {
+                        const int valid = min(max(wrem - kq4[r], 0), 4);
+                        const float *src = valid > 0 ? pb + goff[r] + kq4[r] : a.b;
+                        const uint32_t dst = st + 16 * (bt + r * nbt);
+                        if (al16) {
+                            cp_async16(dst, src, 4 * valid);
+                        } else {
+#pragma unroll
+                            for (int e4 = 0; e4 < 4; ++e4)
+                                cp_async4(dst + 4 * e4, e4 < valid ? src + e4 : a.b, e4 < valid ? 4 : 0);
+                        }
                     }
                 }
             }
@@ -1118,12 +1139,20 @@ __global__ void __launch_bounds__(kKgThreads, 1) tc_kgrad_kernel(const __grid_co
                 if (chunk >= kKgBuf) mbar_wait(empty + bb, (chunk / kKgBuf - 1) & 1);   // MMAs of chunk - kKgBuf done
                 tc_fence_after();
                 const int gy = y0 + yr;
+#ifdef TNRD_KG_EXP_NOA
+                if (q < QA) {
+                } else
+#endif
                 if (q < QA) {   // A: lane t = tap t, 8 pixels per thread
                     uint32_t ih[8], il[8], oh[8], ol[8];
                     const int xc = xc0 + 8 * sub;
                     const float *pu = tu + (yr + 2 * R - ta) * UW + xc + 2 * R - tb;
+#ifdef TNRD_KG_EXP_NOEDGE
+                    const bool r1edge = false;
+#else
                     const bool r1edge = a.boundary == 0 &&
                                         (gy < R || gy >= H - R || x0 + xc < R || x0 + xc + 7 >= W - R);
+#endif
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         float vi = 0.0f, vo = 0.0f;
@@ -1140,23 +1169,32 @@ __global__ void __launch_bounds__(kKgThreads, 1) tc_kgrad_kernel(const __grid_co
                         oh[i] = __float_as_uint(hi_o); ol[i] = __float_as_uint(vo - hi_o);
                     }
                     if (r1edge && t < KT) {   // Ẽ_t(q): every in-image preimage p of q (warp-uniform branch)
-                        const int dy = ta - R, dx = tb - R;
+                        // the mirror is separable: p ranges over (rows py with
+                        // reflect(py - dy) = qy) x (columns px with reflect(px - dx) = qx),
+                        // at most 2 x 2 pixels, all inside this tile's halo (raw e there)
+                        const int dy = ta - R, dx = tb - R, qy = gy;
+                        int ro[3];
+#pragma unroll
+                        for (int iy = 0; iy < 3; ++iy) {
+                            const int py = iy == 0 ? qy + dy : (iy == 1 ? dy - 1 - qy : 2 * H - 1 - qy + dy);
+                            const bool ok = qy < H && py >= 0 && py < H && reflect(py - dy, H) == qy &&
+                                            (iy == 0 || py != qy + dy);
+                            ro[iy] = ok ? (py - y0 + R) * UW : -1;
+                        }
+#pragma unroll
                         for (int i = 0; i < 8; ++i) {
-                            const int qy = gy, qx = x0 + xc + i;
+                            const int qx = x0 + xc + i;
                             float sum = 0.0f;
-                            if (qy < H && qx < W) {
-                                const int cy[3] = {qy + dy, dy - 1 - qy, 2 * H - 1 - qy + dy};
-                                const int cx[3] = {qx + dx, dx - 1 - qx, 2 * W - 1 - qx + dx};
 #pragma unroll
-                                for (int iy = 0; iy < 3; ++iy) {
-                                    const int py = cy[iy];
-                                    if (py < 0 || py >= H || reflect(py - dy, H) != qy) continue;
+                            for (int ix = 0; ix < 3; ++ix) {
+                                const int px = ix == 0 ? qx + dx : (ix == 1 ? dx - 1 - qx : 2 * W - 1 - qx + dx);
+                                const bool ok = qx < W && px >= 0 && px < W && reflect(px - dx, W) == qx &&
+                                                (ix == 0 || px != qx + dx);
+                                if (ok) {
+                                    const int co = px - x0 + R;
 #pragma unroll
-                                    for (int ix = 0; ix < 3; ++ix) {
-                                        const int px = cx[ix];
-                                        if (px < 0 || px >= W || reflect(px - dx, W) != qx) continue;
-                                        sum += __ldg(eb + (long long)py * W + px);
-                                    }
+                                    for (int iy = 0; iy < 3; ++iy)
+                                        if (ro[iy] >= 0) sum += te[ro[iy] + co];
                                 }
                             }
                             const float hs = tf32_hi(sum);
@@ -1171,18 +1209,22 @@ __global__ void __launch_bounds__(kKgThreads, 1) tc_kgrad_kernel(const __grid_co
                     tc_wait_st();
                     tc_fence_before();
                 } else {        // Bm: b and w of this chunk's 32 pixels, float4 per (map, filter, 4 pixels)
+#ifdef TNRD_KG_EXP_NOB
+                    if (chunk >= 0) { __syncwarp(); if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(full + bb)) : "memory"); continue; }
+#endif
                     prefetch(chunk + kKgS - 1);
                     cp_async_wait<kKgS - 1>();   // this thread's copies of this chunk have landed
                     float *sbm = s_bm + bb * 4 * BMF;
                     const float *st = s_st + (chunk % kKgS) * 2 * BMF;
-                    for (int j = bt; j < 2 * NK * 8; j += nbt) {
-                        const int fl = j & 7, kq = (j >> 3) & 7, fg = (j >> 6) % (NK / 8), map = j / (8 * NK);
-                        const float4 v = *reinterpret_cast<const float4 *>(st + 4 * j);
-                        const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-                        const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-                        const int o = (fg * 8 + kq) * 32 + fl * 4;
-                        *reinterpret_cast<float4 *>(sbm + (2 * map) * BMF + o) = h;
-                        *reinterpret_cast<float4 *>(sbm + (2 * map + 1) * BMF + o) = l;
+#pragma unroll
+                    for (int r = 0; r < NJ; ++r) {
+                        if (r < NJ - 1 || bt + r * nbt < 2 * NK * 8) {
+                            const float4 v = *reinterpret_cast<const float4 *>(st + 4 * (bt + r * nbt));
+                            const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+                            const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+                            *reinterpret_cast<float4 *>(sbm + soff[r]) = h;
+                            *reinterpret_cast<float4 *>(sbm + soff[r] + BMF) = l;
+                        }
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
