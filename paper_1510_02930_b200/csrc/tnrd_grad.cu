@@ -194,26 +194,71 @@ __global__ void __launch_bounds__(kGradThreads) fwd_pair_kernel(GradFilterArgs g
 
 // a_f = Kbar_f^T e on the pixels within r of an image edge (R1), where the exact
 // transpose differs from the mirrored convolution the tensor forward bank computed.
+// A block takes kBorderPix border pixels: first E~_t(q) for every (pixel q, tap t),
+// the sum of e over the preimages p of q (the mirror is separable: rows py with
+// mirror(py - dy) = qy times columns px with mirror(px - dx) = qx, at most 2 x 2),
+// into shared memory; then a_f(q) = sum_t kbar_f[t] E~_t(q) in tap order for every
+// (pixel, filter).
+constexpr int kBorderThreads = 128;
+constexpr int kBorderMaxF = 64;
+constexpr int kBorderPix = 32;
+
+__device__ __forceinline__ bool border_pixel(long long idx, int r, int H, int W, long long nb, long long &b, int &y,
+                                             int &x) {
+    const long long top = (long long)r * W;
+    b = idx / nb;
+    const long long k = idx - b * nb;
+    if (k < top) { y = (int)(k / W); x = (int)(k - (long long)y * W); }
+    else if (k < 2 * top) { const long long q = k - top; y = H - r + (int)(q / W); x = (int)(q % W); }
+    else { const long long q = k - 2 * top; y = r + (int)(q / (2 * r)); const int c = (int)(q % (2 * r)); x = c < r ? c : W - 2 * r + c; }
+    return y >= 0 && y < H;
+}
+
 template <int m>
-__global__ void __launch_bounds__(kGradThreads) adj_border_kernel(GradFilterArgs g, const float *__restrict__ e,
-                                                                  float *__restrict__ ao) {
-    constexpr int r = m / 2;
-    __shared__ float sk[m * m];
-    const int f = blockIdx.y;
-    for (int j = threadIdx.x; j < m * m; j += blockDim.x) sk[j] = g.kbar[(long long)(g.fi0 + f) * m * m + j];
-    __syncthreads();
+__global__ void __launch_bounds__(kBorderThreads) adj_border_kernel(GradFilterArgs g, int F, const float *__restrict__ e,
+                                                                    float *__restrict__ ao) {
+    constexpr int r = m / 2, mm = m * m;
+    __shared__ float sk[kBorderMaxF * mm];
+    __shared__ float set[kBorderPix][mm + 1];
+    for (int j = threadIdx.x; j < F * mm; j += blockDim.x) sk[j] = g.kbar[(long long)g.fi0 * mm + j];
     const int H = g.H, W = g.W;
-    const long long top = (long long)r * W, mid = (long long)2 * r * (H - 2 * r > 0 ? H - 2 * r : 0);
-    const long long nb = 2 * top + mid;  // border pixels per image
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (long long)g.B * nb;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const long long b = idx / nb, k = idx - b * nb;
-        int y, x;
-        if (k < top) { y = (int)(k / W); x = (int)(k - (long long)y * W); }
-        else if (k < 2 * top) { const long long q = k - top; y = H - r + (int)(q / W); x = (int)(q % W); }
-        else { const long long q = k - 2 * top; y = r + (int)(q / (2 * r)); const int c = (int)(q % (2 * r)); x = c < r ? c : W - 2 * r + c; }
-        if (y < 0 || y >= H) continue;
-        ao[(long long)f * g.n + b * H * W + (long long)y * W + x] = adj_at<m>(e + b * H * W, sk, y, x, H, W, false);
+    const long long nb = 2LL * r * W + 2LL * r * (H - 2 * r > 0 ? H - 2 * r : 0);  // border pixels per image
+    const long long total = (long long)g.B * nb;
+    for (long long i0 = (long long)blockIdx.x * kBorderPix; i0 < total; i0 += (long long)gridDim.x * kBorderPix) {
+        __syncthreads();   // sk loaded / the previous pixels' set consumed
+        for (int w = threadIdx.x; w < kBorderPix * mm; w += blockDim.x) {
+            const int pi = w / mm, t = w - pi * mm;
+            long long b;
+            int y, x;
+            float v = 0.0f;
+            if (i0 + pi < total && border_pixel(i0 + pi, r, H, W, nb, b, y, x)) {
+                const int dy = t / m - r, dx = t % m - r;
+                const float *eb = e + b * H * W;
+#pragma unroll
+                for (int iy = 0; iy < 3; ++iy) {
+                    const int py = iy == 0 ? y + dy : (iy == 1 ? dy - 1 - y : 2 * H - 1 - y + dy);
+                    if (py < 0 || py >= H || mirror(py - dy, H) != y) continue;
+#pragma unroll
+                    for (int ix = 0; ix < 3; ++ix) {
+                        const int px = ix == 0 ? x + dx : (ix == 1 ? dx - 1 - x : 2 * W - 1 - x + dx);
+                        if (px < 0 || px >= W || mirror(px - dx, W) != x) continue;
+                        v += __ldg(eb + (long long)py * W + px);
+                    }
+                }
+            }
+            set[pi][t] = v;
+        }
+        __syncthreads();
+        for (int w = threadIdx.x; w < kBorderPix * F; w += blockDim.x) {
+            const int pi = w % kBorderPix, f = w / kBorderPix;
+            long long b;
+            int y, x;
+            if (i0 + pi >= total || !border_pixel(i0 + pi, r, H, W, nb, b, y, x)) continue;
+            float v = 0.0f;
+#pragma unroll
+            for (int t = 0; t < mm; ++t) v = fmaf(sk[f * mm + t], set[pi][t], v);
+            ao[(long long)f * g.n + b * H * W + (long long)y * W + x] = v;
+        }
     }
 }
 
@@ -474,11 +519,12 @@ cudaError_t grad_chunk(const GradChunk &c, cudaStream_t s) {
         if (c.boundary == 0) {  // R1: Kbar^T e differs from k * E(e) only within r of an edge
             const int r = c.m / 2;
             const long long nb = (long long)c.B * (2LL * r * c.W + 2LL * r * std::max(c.H - 2 * r, 0));
-            const dim3 bgrid((unsigned)std::max<long long>(1, std::min<long long>((nb + kGradThreads - 1) / kGradThreads, 1024)), c.F);
+            if (c.F > kBorderMaxF) return cudaErrorInvalidValue;
+            const unsigned bgrid = (unsigned)std::max<long long>(1, std::min<long long>((nb + kBorderPix - 1) / kBorderPix, 8192));
             switch (c.m) {
-                case 3: adj_border_kernel<3><<<bgrid, kGradThreads, 0, s>>>(g, c.e, c.a); break;
-                case 5: adj_border_kernel<5><<<bgrid, kGradThreads, 0, s>>>(g, c.e, c.a); break;
-                case 7: adj_border_kernel<7><<<bgrid, kGradThreads, 0, s>>>(g, c.e, c.a); break;
+                case 3: adj_border_kernel<3><<<bgrid, kBorderThreads, 0, s>>>(g, c.F, c.e, c.a); break;
+                case 5: adj_border_kernel<5><<<bgrid, kBorderThreads, 0, s>>>(g, c.F, c.e, c.a); break;
+                case 7: adj_border_kernel<7><<<bgrid, kBorderThreads, 0, s>>>(g, c.F, c.e, c.a); break;
                 default: return cudaErrorInvalidValue;
             }
         }
