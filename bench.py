@@ -196,7 +196,8 @@ def grad_bench(args):
     torch.cuda.set_device(0)
     f = torch.from_numpy(p.f[:1]).cuda()
     gt = torch.from_numpy(p.clean[:1]).cuda()
-    eng = P.TNRD(p.model, device=0)
+    eng = P.TNRD(p.model, device=0,
+                 engine={"auto": P.ENGINE_AUTO, "fp32": P.ENGINE_FP32, "tensor": P.ENGINE_TENSOR}[args.engine])
     for _ in range(args.warmup):
         eng.loss_grad(f, gt)
     torch.cuda.synchronize()
@@ -214,7 +215,11 @@ def grad_bench(args):
             "value": H * W / 1e6 / (ms / 1e3), "unit": "MPix/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "dtype": "f32",
             "data": "synthetic", "config": {"workload": f"{p.cfg['name']} image 0 vs its clean image, "
-                                                        f"T={p.model.T}, Nk={p.model.Nk}, k={p.model.k}, M={p.model.M}"},
+                                                        f"T={p.model.T}, Nk={p.model.Nk}, k={p.model.k}, M={p.model.M}",
+                                            "engine": args.engine,
+                                            "tape": "tensor engine" if args.engine == "tensor" else "fp32 engine",
+                                            "backward_banks": "fp32" if args.engine == "fp32" else
+                                            "tensor cores (3xTF32) where (k, N_k) has them"},
             "stage_launches_per_step": (P.tnrd_launch_count(eng.h) - n0) // args.steps,
             "clocks": clk.summary()}
     print(json.dumps(line), flush=True)

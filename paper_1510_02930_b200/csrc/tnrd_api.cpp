@@ -889,7 +889,15 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
     // ---- forward with tape (the fused stage kernel also writes ut)
     TNRD_K(cudaMemcpy2DAsync(tape_u, sizeof(float) * W, f, sizeof(float) * ld, sizeof(float) * W, (size_t)B * H,
                              cudaMemcpyDeviceToDevice, s));
-    const Plan plan = plan_for(h, B, H, W, true);   // the tape: the same engine as tnrd_denoise
+    // backward banks on the tensor cores unless the engine is FP32; the tape on the FP32
+    // engine unless TENSOR is selected explicitly (env TNRD_GRAD_TAPE=tensor too): the
+    // tensor tape's 3xTF32 forward error reaches the gradient
+    const Plan bank_plan = plan_for(h, B, H, W, true);
+    static const char *tape_env = getenv("TNRD_GRAD_TAPE");
+    static const char *eng_env = getenv("TNRD_ENGINE");
+    const bool tape_tc = h->engine == TNRD_ENGINE_TENSOR || (tape_env && tape_env[0] == 't') ||
+                         (eng_env && eng_env[0] == 't');
+    const Plan plan = tape_tc ? bank_plan : plan_for(h, B, H, W, false);
     for (int t = 0; t < T; ++t) {
         StageArgs a{};
         a.u_in = {tape_u + (size_t)t * n, W, (long long)H * W, 0};
@@ -917,10 +925,10 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
             c.gn = gn; c.x = cx; c.a = ca; c.b = cb; c.w = cw; c.t = ct; c.partial = part;
             c.red = red_f + (size_t)(t * Nk + i0) * per_f; c.red_stride = (int)per_f;
             static const char *adj_env = getenv("TNRD_GRAD_ADJ");  // tests: "fp32" keeps the CUDA-core adjoint
-            if (plan.tc_oh > 0 && F == Nk && !(adj_env && adj_env[0] == 'f')) {
+            if (bank_plan.tc_oh > 0 && F == Nk && !(adj_env && adj_env[0] == 'f')) {
                 c.tc_ba = h->d_tc + (size_t)t * h->tc_stride + 2 * (size_t)Nk * tnrd::tc_ktp(K);
                 c.tc_bf = h->d_tc + (size_t)t * h->tc_stride;
-                c.tc_oh = plan.tc_oh;
+                c.tc_oh = bank_plan.tc_oh;
                 static const char *kg_env = getenv("TNRD_GRAD_KG");  // tests: "fp32" keeps the CUDA-core k-gradient
                 if (!(kg_env && kg_env[0] == 'f')) c.tc_kg_nblk = kg_nblk;
             }

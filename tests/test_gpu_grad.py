@@ -61,6 +61,26 @@ def test_loss_grad_parity(torch_cuda, B, H, W, T, Nk, k, M, boundary):
     _check(gl, rlam, "d lambda")
 
 
+@pytest.mark.parametrize("boundary", [0, 1])
+def test_loss_grad_tensor_tape(torch_cuda, boundary):
+    """ENGINE_TENSOR puts the forward tape on the tensor engine as well (the default
+    AUTO tapes on the FP32 engine); same bound."""
+    import paper_1510_02930_b200 as P
+    torch = torch_cuda
+    B, H, W, T, Nk, k, M = 1, 45, 131, 2, 24, 5, 63
+    f, gt, m = _case(5 + k + T, B, H, W, T, Nk, k, M, w_scale=3.0)
+    eng = P.TNRD(m, boundary=boundary, engine=P.ENGINE_TENSOR)
+    assert eng.engine_for(B, H, W) == P.ENGINE_TENSOR
+    loss, gf, gw, gl = eng.loss_grad(torch.from_numpy(f).cuda(), torch.from_numpy(gt).cuda())
+    eng.close()
+    rl, rf, rw, rlam = oracle.loss_grad(f, gt, m, boundary)
+    assert abs(loss - rl) <= 1e-5 * abs(rl), (loss, rl)
+    for t in range(T):
+        _check(gf[t], rf[t], f"d filters t={t}")
+        _check(gw[t], rw[t], f"d rbf_w t={t}")
+    _check(gl, rlam, "d lambda")
+
+
 @pytest.mark.parametrize("Nk,k", [(4, 3), (48, 7)])
 def test_loss_grad_is_deterministic_and_batch_additive(torch_cuda, Nk, k):
     """Bitwise reproducible, and the batch gradient is the sum over images (CUDA-core

@@ -16,6 +16,8 @@ from synth import make_model  # noqa: E402
 
 CASES = [(2, 24, 20, 2, 4, 3, 15), (1, 33, 40, 3, 6, 5, 31), (1, 40, 36, 2, 8, 7, 63), (1, 96, 80, 8, 48, 7, 63),
          (2, 37, 70, 2, 8, 3, 63), (1, 45, 131, 2, 24, 5, 63), (2, 70, 67, 3, 48, 7, 63)]
+if len(sys.argv) > 1:   # one case: B,H,W,T,Nk,k,M
+    CASES = [tuple(int(v) for v in sys.argv[1].split(","))]
 out = {"bound": 2e-5, "cases": []}
 worst = 0.0
 for (B, H, W, T, Nk, k, M) in CASES:
