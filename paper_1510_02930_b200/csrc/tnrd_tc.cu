@@ -974,7 +974,8 @@ cudaError_t launch_tc_fwd(const float *in, const float *bf, float *out, int B, i
 // Work: 32-pixel chunks (half a tile row of a 64 x kKgTH tile), kKgBuf chunks in
 // flight in TMEM and shared memory between 16 builder warps and one MMA warp
 // (mbarriers full / empty); b and w arrive through a cp.async ring kKgS - 1 chunks
-// ahead; one CTA per SM, tiles grid-strided over the CTAs.
+// ahead; one CTA per SM, tiles grid-strided over the CTAs.  TNRD_KG_EXP_* are
+// timing experiments (wrong results), never set in the product build.
 struct TcKgArgs {
     const float *u, *e;       // [B][H][W]
     const float *b, *w;       // [NK][B*H*W]
