@@ -201,7 +201,10 @@ __global__ void __launch_bounds__(kGradThreads) fwd_pair_kernel(GradFilterArgs g
 // (pixel, filter).
 constexpr int kBorderThreads = 128;
 constexpr int kBorderMaxF = 64;
-constexpr int kBorderPix = 32;
+#ifndef TNRD_BORDER_PIX
+#define TNRD_BORDER_PIX 8
+#endif
+constexpr int kBorderPix = TNRD_BORDER_PIX;
 
 __device__ __forceinline__ bool border_pixel(long long idx, int r, int H, int W, long long nb, long long &b, int &y,
                                              int &x) {
