@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kPhiThreads, TNRD_PHI_MINB) phi_all_kernel(Gra
     const float s2 = 2.0f * step * sc, base = fmaf((float)h, step, mu0), invg2 = 1.0f / (gam * gam);
     // 2^(-t) = 0 (flushed) for t = d^2 log2(e) / (2 gamma^2) > kPhiCut = 126: |d| > dmax
     const float dmax = sqrtf(kPhiCut / 0.72134752044448170f) * gam * 1.0001f + 1e-6f * (fabsf(mu0) + 64.0f * step);
-    const float rstep = 1.0f / step;
+    const float rstep = 1.0f / step, bscale = invg2 / sc;
     const f2 s2v = bc(s2), m2s2 = bc(-2.0f * s2);
     f2 w2[16], acc2[16];
 #pragma unroll
@@ -321,8 +321,12 @@ __global__ void __launch_bounds__(kPhiThreads, TNRD_PHI_MINB) phi_all_kernel(Gra
         const float wmin = warp_min(valid ? x : 3.0e38f), wmax = warp_max(valid ? x : -3.0e38f);
         // the warp's centre range (its 16 pixels), as local indices i = j >> 1 of
         // both halves: warp-uniform
-        const int ilo = max((int)floorf((wmin - dmax - mu0) * rstep), -2) >> 1;
-        const int ihi = min((int)ceilf((wmax + dmax - mu0) * rstep), 64) >> 1;
+        // floor / ceil by directed-rounding adds of 1.5 * 2^23 (no F2I on the XU pipe the
+        // exponentials use), after clamping into [-4, 68]
+        const float flo = fminf(fmaxf((wmin - dmax - mu0) * rstep, -4.0f), 68.0f);
+        const float fhi = fminf(fmaxf((wmax + dmax - mu0) * rstep, -4.0f), 68.0f);
+        const int ilo = max(__float_as_int(__fadd_rd(flo, 12582912.0f)) - 0x4B400000, -2) >> 1;
+        const int ihi = min(__float_as_int(__fadd_ru(fhi, 12582912.0f)) - 0x4B400000, 64) >> 1;
         const float xs = (x - base) * sc;
         const f2 na2 = bc(na);
         f2 phi2 = 0ull, dphi2 = 0ull;
@@ -350,7 +354,7 @@ __global__ void __launch_bounds__(kPhiThreads, TNRD_PHI_MINB) phi_all_kernel(Gra
         const float phi_t = h ? phi_o + phi : phi + phi_o, dphi_t = h ? dphi_o + dphi : dphi + dphi_o;
         if (valid && h == 0) {
             wo[(long long)f * n + p] = phi_t;
-            bo[(long long)f * n + p] = (dphi_t / sc) * invg2 * na;   // -(sum w d G / gamma^2) a
+            bo[(long long)f * n + p] = dphi_t * bscale * na;   // -(sum w d G / gamma^2) a
         }
     }
     // block sum of acc: lanes of a half, then warps, in fixed orders
