@@ -217,9 +217,8 @@ def grad_bench(args):
             "data": "synthetic", "config": {"workload": f"{p.cfg['name']} image 0 vs its clean image, "
                                                         f"T={p.model.T}, Nk={p.model.Nk}, k={p.model.k}, M={p.model.M}",
                                             "engine": args.engine,
-                                            "tape": "tensor engine" if args.engine == "tensor" else "fp32 engine",
-                                            "backward_banks": "fp32" if args.engine == "fp32" else
-                                            "tensor cores (3xTF32) where (k, N_k) has them"},
+                                            "tape_and_banks": "fp32 engine" if args.engine == "fp32" else
+                                            "tensor cores (3xTF32, round-to-nearest split) where (k, N_k) has them"},
             "stage_launches_per_step": (P.tnrd_launch_count(eng.h) - n0) // args.steps,
             "clocks": clk.summary()}
     print(json.dumps(line), flush=True)

@@ -138,10 +138,8 @@ TNRD_API tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out);
  * Derived fp32 evaluation constants are computed on the host in double.
  * Synchronous (uploads with a blocking copy). */
 /* Select the engine (tnrd_engine) for later tnrd_denoise* and tnrd_loss_grad calls
- * on h.  tnrd_loss_grad: AUTO runs its forward tape on the FP32 engine (the tensor
- * engine's 3xTF32 forward error would reach the gradient) and the
- * backward banks on the tensor cores where they apply; TENSOR puts the tape on the
- * tensor engine too; FP32 keeps everything on the CUDA cores.  EINVAL: bad value.
+ * on h (tnrd_loss_grad: its forward tape and backward banks; on the tensor engine the
+ * tape splits operands with round-to-nearest).  EINVAL: bad value.
  * Host-only. */
 TNRD_API tnrd_status tnrd_set_engine(tnrd_handle *h, int engine);
 

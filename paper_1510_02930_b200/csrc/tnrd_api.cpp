@@ -889,21 +889,19 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
     // ---- forward with tape (the fused stage kernel also writes ut)
     TNRD_K(cudaMemcpy2DAsync(tape_u, sizeof(float) * W, f, sizeof(float) * ld, sizeof(float) * W, (size_t)B * H,
                              cudaMemcpyDeviceToDevice, s));
-    // backward banks on the tensor cores unless the engine is FP32; the tape on the FP32
-    // engine unless TENSOR is selected explicitly (env TNRD_GRAD_TAPE=tensor too): the
-    // tensor tape's 3xTF32 forward error reaches the gradient
+    // the tape and the backward banks on the tensor cores unless the engine is FP32; the
+    // tape's tensor stage kernel splits its operands with round-to-nearest (unbiased
+    // errors); env TNRD_GRAD_TAPE=fp32 tapes on the FP32 engine
     const Plan bank_plan = plan_for(h, B, H, W, true);
     static const char *tape_env = getenv("TNRD_GRAD_TAPE");
-    static const char *eng_env = getenv("TNRD_ENGINE");
-    const bool tape_tc = h->engine == TNRD_ENGINE_TENSOR || (tape_env && tape_env[0] == 't') ||
-                         (eng_env && eng_env[0] == 't');
-    const Plan plan = tape_tc ? bank_plan : plan_for(h, B, H, W, false);
+    const Plan plan = (tape_env && tape_env[0] == 'f') ? plan_for(h, B, H, W, false) : bank_plan;
     for (int t = 0; t < T; ++t) {
         StageArgs a{};
         a.u_in = {tape_u + (size_t)t * n, W, (long long)H * W, 0};
         a.f = {f, ld, (long long)H * ld, 0};
         a.u_out = tape_u + (size_t)(t + 1) * n; a.out_ld = W; a.out_img_stride = (long long)H * W; a.out_row_base = 0;
         a.ut_out = tape_ut + (size_t)t * n;
+        a.tc_rn = 1;
         a.H = H; a.W = W; a.y_begin = 0; a.y_end = H; a.avail_lo = 0; a.avail_hi = H;
         st = launch_one(h, t, plan, a, B, s);
         if (st != TNRD_OK) return st;

@@ -92,6 +92,7 @@ struct StageArgs {
     // tensor-core engine (tnrd_tc.cu): output rows per tile and floats of the
     // stage's operand block at `params` (pstride = phi floats per filter there)
     int tc_oh, tc_par_floats;
+    int tc_rn;                 // tensor engine: round-to-nearest operand split (gradient tape)
 };
 
 // Kernel launchers (tnrd_kernels.cu).  Return cudaSuccess or the launch error.

@@ -59,6 +59,15 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)_
 // high part of the 3xTF32 split of a data operand: x truncated to its high 19 bits
 // (TF32); x - hi is exact in fp32 and |x - hi| < 2^-10 |x|
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+// the same split with the high part rounded to nearest (ties away): |x - hi| <= 2^-11 |x|
+// and the rounding errors are unbiased — the training gradient's operands (its tape and
+// banks), whose sums over whole images would accumulate truncation's one-sided bias
+// (DESIGN.md §5.9); one more integer add than truncation
+__device__ __forceinline__ float tf32_hi_rn(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+template <bool RN>
+__device__ __forceinline__ float tf32_hi_t(float x) { return RN ? tf32_hi_rn(x) : tf32_hi(x); }
 
 // UMMA shared-memory descriptor, K-major, no swizzle (sm_100 version 1): 8-row x
 // 16-byte core matrices, K-adjacent core matrices 128 B apart (LBO), 8-row groups
@@ -291,7 +300,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 //   last warp   lane 0 issues the 3xTF32 MMAs: F(i) on A_full(i) -> V_full(i),
 //               Adj(i) on W_full(i) -> Z_full(i), in the order F(0..2), Adj(0),
 //               F(3), Adj(1), F(4), ...
-template <int K, int NK, bool TABLE, bool R2>
+template <int K, int NK, bool TABLE, bool R2, bool RN>
 __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant__ StageArgs a) {
     using G = TcGeo<K, NK>;
     constexpr int R = G::R, KT = G::KT, KTP = G::KTP, NZ = G::NZ, OW = G::OW, UW = G::UW, NFW = G::NFW;
@@ -407,7 +416,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
 #pragma unroll
             for (int e = 0; e < NFW; ++e) {
                 const float x = zero_w ? 0.0f : ((e & 1) ? hi(w[e / 2]) : lo(w[e / 2]));
-                const float xh = tf32_hi(x);
+                const float xh = tf32_hi_t<RN>(x);
                 wh[e] = __float_as_uint(xh);
                 wl[e] = __float_as_uint(x - xh);
             }
@@ -438,7 +447,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
                     const int t = ch * 8 + e;
                     float x = 0.0f;
                     if (t < KT) x = up[-(t / K) * UW - (t % K)];
-                    const float xh = tf32_hi(x);
+                    const float xh = tf32_hi_t<RN>(x);
                     hv[e] = __float_as_uint(xh);
                     lv[e] = __float_as_uint(x - xh);
                 }
@@ -617,10 +626,14 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
 template <int K, int NK>
 cudaError_t launch_tc(StageArgs &a, int B, cudaStream_t s) {
     using G = TcGeo<K, NK>;
-    auto kern = a.boundary == 1 ? (a.mode == MODE_TABLE ? tc_stage_kernel<K, NK, true, true>
-                                                        : tc_stage_kernel<K, NK, false, true>)
-                                : (a.mode == MODE_TABLE ? tc_stage_kernel<K, NK, true, false>
-                                                        : tc_stage_kernel<K, NK, false, false>);
+    // exact phi with the round-to-nearest split only for the training gradient's tape
+    if (a.tc_rn && a.mode == MODE_TABLE) return cudaErrorInvalidValue;
+    auto kern = a.tc_rn ? (a.boundary == 1 ? tc_stage_kernel<K, NK, false, true, true>
+                                           : tc_stage_kernel<K, NK, false, false, true>)
+              : a.boundary == 1 ? (a.mode == MODE_TABLE ? tc_stage_kernel<K, NK, true, true, false>
+                                                        : tc_stage_kernel<K, NK, false, true, false>)
+                                : (a.mode == MODE_TABLE ? tc_stage_kernel<K, NK, true, false, false>
+                                                        : tc_stage_kernel<K, NK, false, false, false>);
     if (a.tc_oh <= 0 || a.tc_oh % 2 != 0) return cudaErrorInvalidValue;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -718,7 +731,7 @@ __global__ void __launch_bounds__(512, 1) tc_adjoint_kernel(const __grid_constan
             uint32_t wh[NFQ], wl[NFQ];
 #pragma unroll
             for (int e = 0; e < NFQ; ++e) {
-                const float xh = tf32_hi(wv[e]);
+                const float xh = tf32_hi_rn(wv[e]);
                 wh[e] = __float_as_uint(xh);
                 wl[e] = __float_as_uint(wv[e] - xh);
             }
@@ -902,7 +915,7 @@ __global__ void __launch_bounds__(512, 1) tc_fwdbank_kernel(const __grid_constan
                     const int t = ch * 8 + e;
                     float v = 0.0f;
                     if (t < KT) v = up[-(t / K) * UW - (t % K)];
-                    const float vh = tf32_hi(v);
+                    const float vh = tf32_hi_rn(v);
                     hv[e] = __float_as_uint(vh);
                     lv[e] = __float_as_uint(v - vh);
                 }
@@ -1165,7 +1178,7 @@ __global__ void __launch_bounds__(kKgThreads, 1) tc_kgrad_kernel(const __grid_co
                                 vo = te[(yr + ta) * UW + xc + i + tb];
                             }
                         }
-                        const float hi_i = tf32_hi(vi), hi_o = tf32_hi(vo);
+                        const float hi_i = tf32_hi_rn(vi), hi_o = tf32_hi_rn(vo);
                         ih[i] = __float_as_uint(hi_i); il[i] = __float_as_uint(vi - hi_i);
                         oh[i] = __float_as_uint(hi_o); ol[i] = __float_as_uint(vo - hi_o);
                     }
@@ -1198,7 +1211,7 @@ __global__ void __launch_bounds__(kKgThreads, 1) tc_kgrad_kernel(const __grid_co
                                         if (ro[iy] >= 0) sum += te[ro[iy] + co];
                                 }
                             }
-                            const float hs = tf32_hi(sum);
+                            const float hs = tf32_hi_rn(sum);
                             oh[i] = __float_as_uint(hs); ol[i] = __float_as_uint(sum - hs);
                         }
                     }
@@ -1221,7 +1234,7 @@ __global__ void __launch_bounds__(kKgThreads, 1) tc_kgrad_kernel(const __grid_co
                     for (int r = 0; r < NJ; ++r) {
                         if (r < NJ - 1 || bt + r * nbt < 2 * NK * 8) {
                             const float4 v = *reinterpret_cast<const float4 *>(st + 4 * (bt + r * nbt));
-                            const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+                            const float4 h = make_float4(tf32_hi_rn(v.x), tf32_hi_rn(v.y), tf32_hi_rn(v.z), tf32_hi_rn(v.w));
                             const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
                             *reinterpret_cast<float4 *>(sbm + soff[r]) = h;
                             *reinterpret_cast<float4 *>(sbm + soff[r] + BMF) = l;

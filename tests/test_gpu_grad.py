@@ -62,15 +62,15 @@ def test_loss_grad_parity(torch_cuda, B, H, W, T, Nk, k, M, boundary):
 
 
 @pytest.mark.parametrize("boundary", [0, 1])
-def test_loss_grad_tensor_tape(torch_cuda, boundary):
-    """ENGINE_TENSOR puts the forward tape on the tensor engine as well (the default
-    AUTO tapes on the FP32 engine); same bound."""
+def test_loss_grad_fp32_engine_on_tensor_shapes(torch_cuda, boundary):
+    """ENGINE_FP32 keeps the tape and the backward banks on the CUDA cores for a
+    (k, N_k) that has tensor instantiations (AUTO uses them); same bound."""
     import paper_1510_02930_b200 as P
     torch = torch_cuda
     B, H, W, T, Nk, k, M = 1, 45, 131, 2, 24, 5, 63
     f, gt, m = _case(5 + k + T, B, H, W, T, Nk, k, M, w_scale=3.0)
-    eng = P.TNRD(m, boundary=boundary, engine=P.ENGINE_TENSOR)
-    assert eng.engine_for(B, H, W) == P.ENGINE_TENSOR
+    eng = P.TNRD(m, boundary=boundary, engine=P.ENGINE_FP32)
+    assert eng.engine_for(B, H, W) == P.ENGINE_FP32
     loss, gf, gw, gl = eng.loss_grad(torch.from_numpy(f).cuda(), torch.from_numpy(gt).cuda())
     eng.close()
     rl, rf, rw, rlam = oracle.loss_grad(f, gt, m, boundary)
