@@ -198,28 +198,32 @@ def grad_bench(args):
     gt = torch.from_numpy(p.clean[:1]).cuda()
     eng = P.TNRD(p.model, device=0,
                  engine={"auto": P.ENGINE_AUTO, "fp32": P.ENGINE_FP32, "tensor": P.ENGINE_TENSOR}[args.engine])
+    t0 = time.perf_counter()
     for _ in range(args.warmup):
         eng.loss_grad(f, gt)
     torch.cuda.synchronize()
+    # at least ~0.5 s of timed steps, so the 100 ms clock sampler sees the region
+    est = (time.perf_counter() - t0) / max(args.warmup, 1)
+    steps = max(args.steps, int(0.5 / max(est, 1e-4)) + 1)
     n0 = P.tnrd_launch_count(eng.h)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(0) as clk:
         ev0.record()
-        for _ in range(args.steps):
+        for _ in range(steps):
             eng.loss_grad(f, gt)
         ev1.record()
         torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = ev0.elapsed_time(ev1) / steps
     _, H, W = p.f.shape
     line = {"metric": "training-gradient MPix/s (loss + dl/dTheta, P Eq.14-20, fp32)", "mode": "grad",
-            "value": H * W / 1e6 / (ms / 1e3), "unit": "MPix/s", "n_gpus": 1, "steps": args.steps,
+            "value": H * W / 1e6 / (ms / 1e3), "unit": "MPix/s", "n_gpus": 1, "steps": steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "dtype": "f32",
             "data": "synthetic", "config": {"workload": f"{p.cfg['name']} image 0 vs its clean image, "
                                                         f"T={p.model.T}, Nk={p.model.Nk}, k={p.model.k}, M={p.model.M}",
                                             "engine": args.engine,
                                             "tape_and_banks": "fp32 engine" if args.engine == "fp32" else
                                             "tensor cores (3xTF32, round-to-nearest split) where (k, N_k) has them"},
-            "stage_launches_per_step": (P.tnrd_launch_count(eng.h) - n0) // args.steps,
+            "stage_launches_per_step": (P.tnrd_launch_count(eng.h) - n0) // steps,
             "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
     eng.close()
