@@ -1174,7 +1174,7 @@ __global__ void __launch_bounds__(kKgThreads, 1) tc_kgrad_kernel(const __grid_co
                             vi = pu[i];
                             if (a.boundary == 1) {
                                 vo = te[(yr + 2 * R - ta) * UW + xc + i + 2 * R - tb];
-                            } else if (!r1edge) {
+                            } else {   // interior value; the edge pixels are redone below
                                 vo = te[(yr + ta) * UW + xc + i + tb];
                             }
                         }
@@ -1195,9 +1195,11 @@ __global__ void __launch_bounds__(kKgThreads, 1) tc_kgrad_kernel(const __grid_co
                                             (iy == 0 || py != qy + dy);
                             ro[iy] = ok ? (py - y0 + R) * UW : -1;
                         }
+                        const bool rowedge = gy < R || gy >= H - R;
 #pragma unroll
                         for (int i = 0; i < 8; ++i) {
                             const int qx = x0 + xc + i;
+                            if (!rowedge && qx >= R && qx < W - R) continue;   // interior pixel (uniform)
                             float sum = 0.0f;
 #pragma unroll
                             for (int ix = 0; ix < 3; ++ix) {
