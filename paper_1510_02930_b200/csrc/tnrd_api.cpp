@@ -856,8 +856,14 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
     const int T = h->d.T, Nk = h->d.n_filters, K = h->d.ksize, M = h->d.n_rbf;
     const size_t mm = (size_t)K * K, n = (size_t)B * H * W, TN = (size_t)T * Nk;
     if (M > 64) return fail(h, TNRD_EUNSUPPORTED, "training gradient built for n_rbf <= 64");
-    // filters per backward chunk: 5 per-filter images (x, a, b, w, t) within ~1 GB
-    const int F = (int)std::max<size_t>(1, std::min<size_t>((size_t)Nk, ((size_t)1 << 30) / (5 * n * sizeof(float))));
+    // filters per backward chunk: 5 per-filter images (x, a, b, w, t) within half the
+    // device memory (at least 1 GB; from the total, not the free memory, so that the
+    // chunking — and with it the summation order — is the same on every call); all
+    // N_k in one chunk enables the tensor banks (C4's 256 x 512^2 batch: 64 GB)
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) total_b = 0;
+    const size_t budget = std::max<size_t>((size_t)1 << 30, total_b / 2);
+    const int F = (int)std::max<size_t>(1, std::min<size_t>((size_t)Nk, budget / (5 * n * sizeof(float))));
     // tape u_0..u_T and ut_0..ut_{T-1} (2T+1 images) + g, gn, e + the chunk images
     const size_t imgs = 2 * (size_t)T + 1 + 3 + 5 * (size_t)F;
     st = grow(h, &h->g_buf, &h->g_buf_bytes, sizeof(float) * n * imgs, "gradient tape");
