@@ -74,6 +74,7 @@ NcclApi &nccl() {
 struct tnrd_handle {
     tnrd_desc d{};
     int num_sms = 148;
+    size_t total_mem = 0;          // device memory (bytes), queried once at create
     bool allow_large_tile = true;  // the 2x64x64 tile pair fits in shared memory
     int pstride_max = 0;
     std::vector<int> pstride;     // per stage
@@ -516,6 +517,10 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
         delete hh;
     };
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, d->device);
+    {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) h->total_mem = total_b;
+    }
     h->pstride_max = std::max(pstride_for(*d, tnrd::MODE_HORNER), pstride_for(*d, tnrd::MODE_DIRECT));
     h->pstride.assign(d->T, 0);
     h->mode.assign(d->T, 0);
@@ -860,9 +865,7 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
     // device memory (at least 1 GB; from the total, not the free memory, so that the
     // chunking — and with it the summation order — is the same on every call); all
     // N_k in one chunk enables the tensor banks (C4's 256 x 512^2 batch: 64 GB)
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) total_b = 0;
-    const size_t budget = std::max<size_t>((size_t)1 << 30, total_b / 2);
+    const size_t budget = std::max<size_t>((size_t)1 << 30, h->total_mem / 2);
     const int F = (int)std::max<size_t>(1, std::min<size_t>((size_t)Nk, budget / (5 * n * sizeof(float))));
     // tape u_0..u_T and ut_0..ut_{T-1} (2T+1 images) + g, gn, e + the chunk images
     const size_t imgs = 2 * (size_t)T + 1 + 3 + 5 * (size_t)F;

@@ -313,11 +313,27 @@ __global__ void __launch_bounds__(kPhiThreads, TNRD_PHI_MINB) phi_all_kernel(Gra
     const float *xf = xv + (long long)f * n, *af = av + (long long)f * n;
     const long long pstep = (long long)gridDim.x * (kPhiThreads / 32) * 16;
     long long p = ((long long)blockIdx.x * (kPhiThreads / 32) + warp) * 16 + (lane & 15);
-    float xn = p < n ? xf[p] : 0.0f, an = p < n ? af[p] : 0.0f;
+    // loads run TNRD_PHI_PF iterations ahead (a register ring)
+#ifndef TNRD_PHI_PF
+#define TNRD_PHI_PF 2
+#endif
+    constexpr int PF = TNRD_PHI_PF;
+    float xr[PF], ar[PF];
+#pragma unroll
+    for (int k = 0; k < PF; ++k) {
+        const long long q = p + k * pstep;
+        xr[k] = q < n ? xf[q] : 0.0f;
+        ar[k] = q < n ? af[q] : 0.0f;
+    }
     for (; p - (lane & 15) < n; p += pstep) {
         const bool valid = p < n;
-        const float x = xn, na = valid ? -an : 0.0f;
-        if (p + pstep < n) { xn = xf[p + pstep]; an = af[p + pstep]; }   // next pixel's loads in flight
+        const float x = xr[0], na = valid ? -ar[0] : 0.0f;
+#pragma unroll
+        for (int k = 0; k + 1 < PF; ++k) { xr[k] = xr[k + 1]; ar[k] = ar[k + 1]; }
+        {
+            const long long q = p + PF * pstep;
+            if (q < n) { xr[PF - 1] = xf[q]; ar[PF - 1] = af[q]; }
+        }
         const float wmin = warp_min(valid ? x : 3.0e38f), wmax = warp_max(valid ? x : -3.0e38f);
         // the warp's centre range (its 16 pixels), as local indices i = j >> 1 of
         // both halves: warp-uniform
