@@ -99,3 +99,40 @@ def test_loss_grad_is_deterministic_and_batch_additive(torch_cuda, Nk, k):
         s = sum(np.asarray(p[j], np.float64) for p in parts)
         assert np.max(np.abs(a[j] - s)) <= 1e-5 * np.max(np.abs(s)) + 1e-9
     assert abs(a[0] - sum(p[0] for p in parts)) <= 1e-6 * abs(a[0])
+
+
+_KG_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, "tests")
+import paper_1510_02930_b200 as P
+from test_gpu_grad import _case
+B, H, W, T, Nk, k, M, bnd = map(int, sys.argv[1:9])
+f, gt, m = _case(11, B, H, W, T, Nk, k, M, w_scale=3.0)
+eng = P.TNRD(m, boundary=bnd)
+loss, gf, gw, gl = eng.loss_grad(torch.from_numpy(f).cuda(), torch.from_numpy(gt).cuda())
+eng.close()
+np.save(sys.argv[9], np.stack([np.asarray(g, np.float64) for g in gf]))
+"""
+
+
+@pytest.mark.parametrize("boundary", [0, 1])
+def test_filter_gradient_tensor_gemm_vs_cuda_cores(torch_cuda, tmp_path, boundary):
+    """The tensor-core filter-gradient GEMM against the CUDA-core tap sums
+    (TNRD_GRAD_KG=fp32) on the same tape: same filter gradient to the test bound,
+    on a ragged (k, N_k) = (7, 48) batch."""
+    import os
+    import subprocess
+    import sys
+    args = ["2", "37", "70", "2", "48", "7", "63", str(boundary)]
+    out = {}
+    for name, extra in (("tc", {}), ("fp32", {"TNRD_GRAD_KG": "fp32"})):
+        env = dict(os.environ, **extra)
+        path = str(tmp_path / f"{name}.npy")
+        subprocess.run([sys.executable, "-c", _KG_SCRIPT, *args, path], check=True, env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        out[name] = np.load(path)
+    a, b = out["tc"], out["fp32"]
+    for t in range(a.shape[0]):
+        scale = float(np.max(np.abs(b[t])))
+        err = float(np.max(np.abs(a[t] - b[t])))
+        assert err <= 2e-5 * scale, (t, err, scale)
