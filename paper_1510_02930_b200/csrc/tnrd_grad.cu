@@ -277,7 +277,10 @@ __global__ void __launch_bounds__(kBorderThreads) adj_border_kernel(GradFilterAr
 // [jlo, jhi], the centres within dmax of some value of the warp; beyond dmax every
 // G_j is exactly 0 (ex2.approx.ftz of < -126 flushes, kPhiCut = 126), so skipping
 // changes no sum.  (A cut at 2^-40 instead measured no faster: DESIGN.md §5.9.)
-constexpr int kPhiThreads = 256;
+#ifndef TNRD_PHI_THREADS
+#define TNRD_PHI_THREADS 512
+#endif
+constexpr int kPhiThreads = TNRD_PHI_THREADS;
 #ifndef TNRD_PHI_CUT
 #define TNRD_PHI_CUT 126.0f
 #endif
@@ -287,7 +290,7 @@ constexpr int kPhiThreads = 256;
 constexpr float kPhiCut = TNRD_PHI_CUT;   // 2^(-t) for t > kPhiCut is not evaluated (exactly 0 at 126)
 
 #ifndef TNRD_PHI_MINB
-#define TNRD_PHI_MINB 2
+#define TNRD_PHI_MINB 1
 #endif
 __global__ void __launch_bounds__(kPhiThreads, TNRD_PHI_MINB) phi_all_kernel(GradFilterArgs g, const float *__restrict__ xv,
                                                                  const float *__restrict__ av, float *__restrict__ wo,

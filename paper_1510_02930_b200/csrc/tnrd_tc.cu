@@ -996,8 +996,14 @@ struct TcKgArgs {
     int boundary, B, H, W, tiles_x, tiles_y;
 };
 
-constexpr int kKgTH = 8;     // tile rows
-constexpr int kKgS = 4;      // Bm prefetch depth (chunks in flight, cp.async)
+#ifndef TNRD_KG_TH
+#define TNRD_KG_TH 4
+#endif
+constexpr int kKgTH = TNRD_KG_TH;     // tile rows
+#ifndef TNRD_KG_S
+#define TNRD_KG_S 4
+#endif
+constexpr int kKgS = TNRD_KG_S;      // Bm prefetch depth (chunks in flight, cp.async)
 constexpr int kKgBuf = 3;    // chunks in TMEM / shared memory between the builders and the MMA warp
 constexpr int kKgBuilders = 512;              // 16 builder warps
 constexpr int kKgThreads = kKgBuilders + 32;  // + the MMA warp
