@@ -822,6 +822,9 @@ __global__ void __launch_bounds__(512, 1) tc_adjoint_kernel(const __grid_constan
 template <int K, int NK>
 cudaError_t launch_tc_adj(const float *b, const float *ba, float *gn, int B, int H, int W, int oh, cudaStream_t s) {
     constexpr int R = K / 2, OW = kTcVW - 2 * R;
+#ifdef TNRD_ADJ_OH
+    oh = TNRD_ADJ_OH;
+#endif
     TcAdjArgs a{b, ba, gn, B, H, W, oh, (W + OW - 1) / OW, (H + oh - 1) / oh};
     const size_t smem = sizeof(float) * (2 * (size_t)tc_nz(K) * NK + (size_t)K * K * kZP + round4(oh * OW) + 8);
     cudaError_t e = cudaFuncSetAttribute(tc_adjoint_kernel<K, NK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -858,7 +861,10 @@ struct TcFwdArgs {
     int B, H, W, tiles_x, tiles_y;
 };
 
-constexpr int kFwdOH = 32;   // output rows per tile of the gradient's forward bank
+#ifndef TNRD_FWD_OH
+#define TNRD_FWD_OH 32
+#endif
+constexpr int kFwdOH = TNRD_FWD_OH;   // output rows per tile of the gradient's forward bank
 
 template <int K, int NK>
 __global__ void __launch_bounds__(512, 1) tc_fwdbank_kernel(const __grid_constant__ TcFwdArgs a) {
