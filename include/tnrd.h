@@ -199,8 +199,12 @@ TNRD_API unsigned long long tnrd_launch_count(const tnrd_handle *h);
  *   loss             host                  the loss (double)
  * Reaction 0 and TNRD_PHI_EXACT only (else EUNSUPPORTED).  Runs the forward pass
  * with a tape (2T+1 images of scratch, owned by the handle), then the backward
- * stages; all sums are fixed-order (bitwise reproducible).  Synchronous: returns
- * after the host outputs are written. */
+ * stages: where (k, N_k) has tensor instantiations and the engine is not FP32, the
+ * tape, both filter banks and the filter-gradient sums run as 3xTF32 tcgen05 GEMMs
+ * (round-to-nearest operand split); the backward's per-filter scratch is chunked
+ * within half the device memory.  All sums are fixed-order (bitwise reproducible).
+ * ENOMEM if the scratch cannot be allocated.  Synchronous: returns after the host
+ * outputs are written. */
 TNRD_API tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f_dev, const float *u_gt_dev, int B, int H,
                                     int W, long long ld, float *grad_filters, float *grad_rbf_w,
                                     float *grad_lambda, double *loss, void *cuda_stream);
