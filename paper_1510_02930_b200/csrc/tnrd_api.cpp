@@ -866,11 +866,17 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
     // chunking — and with it the summation order — is the same on every call); all
     // N_k in one chunk enables the tensor banks (C4's 256 x 512^2 batch: 64 GB)
     const size_t budget = std::max<size_t>((size_t)1 << 30, h->total_mem / 2);
-    const int F = (int)std::max<size_t>(1, std::min<size_t>((size_t)Nk, budget / (5 * n * sizeof(float))));
-    // tape u_0..u_T and ut_0..ut_{T-1} (2T+1 images) + g, gn, e + the chunk images
-    const size_t imgs = 2 * (size_t)T + 1 + 3 + 5 * (size_t)F;
-    st = grow(h, &h->g_buf, &h->g_buf_bytes, sizeof(float) * n * imgs, "gradient tape");
-    if (st != TNRD_OK) return st;
+    int F = (int)std::max<size_t>(1, std::min<size_t>((size_t)Nk, budget / (5 * n * sizeof(float))));
+    // tape u_0..u_T and ut_0..ut_{T-1} (2T+1 images) + g, gn, e + the chunk images; if
+    // the device is short of memory (other allocations), halve the chunk and retry
+    for (;;) {
+        const size_t imgs = 2 * (size_t)T + 1 + 3 + 5 * (size_t)F;
+        st = grow(h, &h->g_buf, &h->g_buf_bytes, sizeof(float) * n * imgs, "gradient tape");
+        if (st == TNRD_OK) break;
+        if (st != TNRD_ENOMEM || F == 1) return st;
+        cudaGetLastError();   // the failed cudaMalloc is not sticky; clear it
+        F = std::max(1, F / 2);
+    }
     const int grid = tnrd::grad_grid((long long)n, h->num_sms);
     const int gx = tnrd::grad_chunk_grid((long long)n, F, h->num_sms);
     const int kg_nblk = tnrd::tc_kgrad_blocks(B, H, W, h->num_sms);
