@@ -481,6 +481,19 @@ __global__ void __launch_bounds__(kGradThreads) reduce_f_kernel(const float *__r
     if (threadIdx.x == 0) out[(long long)f * out_stride + out_off + j] = red[0];
 }
 
+// The same sums with one warp per (j, f): lane l takes blocks l, l + 32, ... in order,
+// then a fixed shuffle tree (for the short partial lists of the phi and tensor-core
+// filter-gradient kernels: <= a few hundred blocks).
+__global__ void __launch_bounds__(32) reduce_f_warp_kernel(const float *__restrict__ partial, int nblk, int np,
+                                                          double *__restrict__ out, int out_stride, int out_off) {
+    const int f = blockIdx.y, j = blockIdx.x, lane = threadIdx.x;
+    double s = 0.0;
+    for (int b = lane; b < nblk; b += 32) s += (double)partial[((long long)f * nblk + b) * np + j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[(long long)f * out_stride + out_off + j] = s;
+}
+
 // out[j] = sum over blocks of partial[blk * stride + j], j < np, in double: block j
 // sums parameter j; thread t takes blocks t, t + 256, ... in order, then a fixed
 // shared-memory tree (bitwise reproducible).
@@ -563,7 +576,7 @@ cudaError_t grad_chunk(const GradChunk &c, cudaStream_t s) {
             occ = 1;
         const int gphi = std::max(1, std::min(c.gx, std::max(1, c.num_sms * std::max(occ, 1) / c.F)));
         phi_all_kernel<<<dim3(gphi, c.F), kPhiThreads, 0, s>>>(g, c.x, c.a, c.w, c.b, c.partial);
-        reduce_f_kernel<<<dim3(c.M, c.F), kGradThreads, 0, s>>>(c.partial, gphi, 64, c.red, c.red_stride, 2 * mm);
+        reduce_f_warp_kernel<<<dim3(c.M, c.F), 32, 0, s>>>(c.partial, gphi, 64, c.red, c.red_stride, 2 * mm);
     }
     if (c.tc_ba) {  // gn -= sum_f K_f^T b_f on the tensor cores (all N_k filters in this chunk)
         const cudaError_t e = launch_tc_adjoint(c.m, c.F, c.b, c.tc_ba, c.gn, c.B, c.H, c.W, c.tc_oh, s);
@@ -576,7 +589,7 @@ cudaError_t grad_chunk(const GradChunk &c, cudaStream_t s) {
         const cudaError_t e = launch_tc_kgrad(c.m, c.F, c.u, c.e, c.b, c.w, c.boundary, c.B, c.H, c.W, c.partial,
                                               c.tc_kg_nblk, s);
         if (e != cudaSuccess) return e;
-        reduce_f_kernel<<<dim3(2 * mm, c.F), kGradThreads, 0, s>>>(c.partial, c.tc_kg_nblk, 2 * mm, c.red,
+        reduce_f_warp_kernel<<<dim3(2 * mm, c.F), 32, 0, s>>>(c.partial, c.tc_kg_nblk, 2 * mm, c.red,
                                                                      c.red_stride, 0);
     } else {
         TNRD_M(kgrad_pair_kernel, g, c.u, c.e, c.boundary, c.b, c.w, c.partial)
