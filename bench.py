@@ -7,13 +7,18 @@
 A step is one full inference pass (T = 8 fused stage launches) over the
 workload: by default BASELINE.json configs[3] (C4: 256 independent 512x512
 images, 48 7x7 filters, 63 RBFs, T = 8), its images sharded over the ranks
-(no data-path collective; reported "scaling": "weak" per the task rule for partitioned paths -- DESIGN.md §6).  --config 5 runs
-C5 (one 8192^2 image) as row slabs with the per-stage NCCL halo exchange.
+(no data-path collective).  --config 5 runs C5 (one 8192^2 image) as row slabs
+with the per-stage NCCL halo exchange.  Both configs fix the total work, so N > 1
+is reported as "scaling": "strong".
 
-For N > 1 launch with torchrun (one process per GPU); rank 0 prints one JSON
-line.  Timing: CUDA events on the launching stream, barrier + synchronize on
-both sides, max over ranks.  Inputs (~0.8 GB resident per step) exceed the
-126 MB L2, so no flush is needed.  See DESIGN.md §8.
+For N > 1: under torchrun (WORLD_SIZE set) one process per GPU; launched plainly
+with --gpus N, bench.py re-launches itself through torch.distributed.run with N
+ranks (an error if fewer than N GPUs are visible).  --dry-run runs the same
+multi-rank plumbing on CPU with gloo (shards, barriers, max-over-ranks) without
+touching a GPU (tests/test_multiproc_gloo.py).  Rank 0 prints one JSON line.
+Timing: CUDA events on the launching stream, barrier + synchronize on both
+sides, max over ranks.  Inputs (~0.8 GB resident per step) exceed the 126 MB L2,
+so no flush is needed.  See DESIGN.md §8.
 """
 from __future__ import annotations
 
@@ -141,7 +146,7 @@ def reference_arm(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(p, world, args),
         "cpu_baseline": {"value": value, "unit": "MPix/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "MPix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -150,12 +155,18 @@ def reference_arm(args, rank, world):
     return 0
 
 
+def parallelism(config, world):
+    if world == 1:
+        return "single-gpu (no partition)"
+    return ("batch-shard" if config != 5 else "row-slab+nccl-halo") + f"x{world}"
+
+
 def workload_config(p, world, args):
     c = p.cfg
     return {"workload": f"{c['name']}: {c['B']}x{c['H']}x{c['W']} fp32, peaks {c['peaks']}, T={c['T']}, "
                         f"Nk={c['Nk']}, k={c['k']}, M={c['M']} (BASELINE.json configs[{args.config - 1}])",
             "batch": c["B"], "H": c["H"], "W": c["W"], "T": c["T"], "Nk": c["Nk"], "k": c["k"], "M": c["M"],
-            "parallelism": ("batch-shard" if args.config != 5 else "row-slab+nccl-halo") + f"x{world}",
+            "parallelism": parallelism(args.config, world),
             "l2": "no flush: per-step working set (f, u, scratch) > 126 MB L2",
             "phi": args.phi,
             "flop_per_px_stage": (F_TAB if args.phi == "table" else F_ALG)(c["Nk"], c["k"], c["M"])}
@@ -183,6 +194,58 @@ def cpu_baseline(p, budget_s=12.0):
     return {"value": px / 1e6 / dt, "unit": "MPix/s", "cores": oracle.num_threads(), "kind": "oracle",
             "sample": f"{n} centred {side}x{side} window(s) of images 0..{n - 1} (T={p.model.T}, full model), "
                       f"double precision, OpenMP over rows, {dt:.1f} s"}
+
+
+def relaunch(args):
+    """bench.py --gpus N without torchrun: re-launch as N ranks on this node through
+    torch.distributed.run (rank 0's JSON line is passed through)."""
+    if not args.dry_run:
+        import torch
+        n_vis = torch.cuda.device_count()
+        if args.gpus > n_vis:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} but only {n_vis} GPU(s) are visible\n")
+            return 2
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dry_run(args, rank, world):
+    """--dry-run: the N > 1 plumbing on CPU (gloo): each rank takes its shard of the
+    workload exactly as the GPU path does, the timed region is bracketed by
+    barriers, the time is the max over ranks, and rank 0 prints one line listing
+    every rank's shard.  No GPU, no kernel: a test of the launcher, not a number."""
+    import torch
+    import torch.distributed as dist
+    from paper_1510_02930_b200.partition import batch_shard, slab_rows
+    from synth.generator import CONFIGS
+    c = CONFIGS[args.config]
+    if world > 1:
+        dist.init_process_group("gloo")
+    shard = slab_rows(c["H"], rank, world) if args.config == 5 else batch_shard(c["B"], rank, world)
+    t0 = time.perf_counter()
+    if world > 1:
+        dist.barrier()
+    ms = torch.tensor([1e3 * (time.perf_counter() - t0)], dtype=torch.float64)
+    shards = [None] * world
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        dist.all_gather_object(shards, (rank, shard))
+    else:
+        shards = [(rank, shard)]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "config": {"workload": c["name"], "parallelism": parallelism(args.config, world)},
+                          "scaling": "strong", "shards": [list(s) for _, s in sorted(shards)],
+                          "ms_max_over_ranks": float(ms[0])}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
 
 
 def grad_bench(args):
@@ -246,8 +309,15 @@ def main():
                     help="stage engine (tnrd_set_engine): auto = tensor cores where they apply")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU only: the multi-rank plumbing (launch, shards, barriers, max over ranks) "
+                         "over gloo without any GPU work")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     rank, world, local = dist_env()
+    if args.dry_run:
+        return dry_run(args, rank, world)
     if args.impl == "reference":
         return reference_arm(args, rank, world)
     if args.mode == "grad":
@@ -283,7 +353,7 @@ def main():
 
         def step():
             if world > 1:
-                P.tnrd_denoise_slab(eng.h, f_dev, u_dev, H, r0, 0.1)
+                P.tnrd_denoise_slab(eng.h, f_dev, u_dev, H, r0, float(p.peaks[0]))
             else:
                 P.tnrd_denoise(eng.h, f_dev[None], u_dev[None])
         px_rank = (r1 - r0) * W
@@ -411,7 +481,9 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 storage; conv products 3xTF32 (tensor engine)" if tensor else "f32",
+            "data": "synthetic",
             "config": dict(workload_config(p, world, args), engine="tensor" if tensor else "fp32",
                            conv_arithmetic=("3xTF32 tcgen05: fp32 operands split hi + lo, three TF32 products "
                                             "per term, fp32 accumulation (products exact to < 2^-20 relative); "

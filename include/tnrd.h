@@ -102,8 +102,11 @@ typedef enum {
 } tnrd_engine;
 
 /* Model shape.  T >= 1 stages, n_filters = N_k >= 1 (P l.423: N_k = m^2 - 1 if
- * not specified, not enforced), ksize = m in {3, 5, 7}, n_rbf = M in [1, 256],
- * device = CUDA ordinal, reaction = tnrd_reaction (0 = the paper's Eq.13). */
+ * not specified, not enforced), ksize = m odd >= 3 (P l.458-469, Fig.3, studies
+ * m = 3..9; this build runs m in {3, 5, 7, 9, 11}: the tensor engine for
+ * (m, N_k) in {(3, 8), (5, 24), (7, 48)}, the FP32 engine for every m),
+ * n_rbf = M in [1, 256], device = CUDA ordinal, reaction = tnrd_reaction
+ * (0 = the paper's Eq.13). */
 typedef struct {
     int T;
     int n_filters;
@@ -123,8 +126,20 @@ TNRD_API const char *tnrd_status_string(tnrd_status s);
 
 /* Create a handle for model shape *d on d->device.  *out receives the handle
  * (owned by the caller, released with tnrd_destroy).  Allocates the device
- * parameter store.  EINVAL: bad shape; EUNSUPPORTED: ksize outside {3,5,7}; ECUDA/ENOMEM: device errors.  Synchronous. */
+ * parameter store.  EINVAL: bad shape (T, N_k or M out of range; ksize even or
+ * < 3; bad enum); EUNSUPPORTED: odd ksize > 11, or a model whose stage operands
+ * exceed the shared memory of one CTA; ECUDA/ENOMEM: device errors.  Synchronous. */
 TNRD_API tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out);
+
+/* Select the engine (tnrd_engine) for later tnrd_denoise* and tnrd_loss_grad calls
+ * on h (tnrd_loss_grad: its forward tape and backward banks; on the tensor engine the
+ * tape splits operands with round-to-nearest, DESIGN.md §5.9).  EINVAL: bad value.
+ * Host-only. */
+TNRD_API tnrd_status tnrd_set_engine(tnrd_handle *h, int engine);
+
+/* The engine (TNRD_ENGINE_FP32 or TNRD_ENGINE_TENSOR) tnrd_denoise would use for
+ * a B x H x W batch now; -1 if h is null or a stage is unset.  Host-only. */
+TNRD_API int tnrd_engine_for(tnrd_handle *h, int B, int H, int W);
 
 /* Set Theta^t = {lambda^t, phi_i^t, k_i^t} of stage t in [0, T) (P l.206-207).
  * All pointers are HOST arrays, copied before return (the caller may free them):
@@ -137,16 +152,6 @@ TNRD_API tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out);
  * EINVAL on non-finite values, step/gamma <= 0, lambda <= 0, t out of range.
  * Derived fp32 evaluation constants are computed on the host in double.
  * Synchronous (uploads with a blocking copy). */
-/* Select the engine (tnrd_engine) for later tnrd_denoise* and tnrd_loss_grad calls
- * on h (tnrd_loss_grad: its forward tape and backward banks; on the tensor engine the
- * tape splits operands with round-to-nearest, DESIGN.md §5.9).  EINVAL: bad value.
- * Host-only. */
-TNRD_API tnrd_status tnrd_set_engine(tnrd_handle *h, int engine);
-
-/* The engine (TNRD_ENGINE_FP32 or TNRD_ENGINE_TENSOR) tnrd_denoise would use for
- * a B x H x W batch now; -1 if h is null or a stage is unset.  Host-only. */
-TNRD_API int tnrd_engine_for(tnrd_handle *h, int B, int H, int W);
-
 TNRD_API tnrd_status tnrd_set_stage_params(tnrd_handle *h, int t, const float *filters, const float *rbf_w,
                                   const float *rbf_mu0, const float *rbf_step,
                                   const float *rbf_gamma, float lambda);
@@ -201,13 +206,23 @@ TNRD_API unsigned long long tnrd_launch_count(const tnrd_handle *h);
  * with a tape (2T+1 images of scratch, owned by the handle), then the backward
  * stages: where (k, N_k) has tensor instantiations and the engine is not FP32, the
  * tape, both filter banks and the filter-gradient sums run as 3xTF32 tcgen05 GEMMs
- * (round-to-nearest operand split); the backward's per-filter scratch is chunked
- * within half the device memory.  All sums are fixed-order (bitwise reproducible).
- * ENOMEM if the scratch cannot be allocated.  Synchronous: returns after the host
- * outputs are written. */
+ * (round-to-nearest operand split) when all N_k filters fit one backward chunk.
+ * The backward's per-filter scratch (5 images per filter) is chunked by filters:
+ * F = min(N_k, tnrd_set_grad_chunk's cap, filters whose scratch fits half the
+ * device's TOTAL memory) -- a function of the shape and the device, never of the
+ * memory that happens to be free, so every call with the same arguments uses the
+ * same chunks and summation order (bitwise reproducible).  ENOMEM if that scratch
+ * cannot be allocated (nothing is retried smaller).  Synchronous: returns after the
+ * host outputs are written. */
 TNRD_API tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f_dev, const float *u_gt_dev, int B, int H,
                                     int W, long long ld, float *grad_filters, float *grad_rbf_w,
                                     float *grad_lambda, double *loss, void *cuda_stream);
+
+/* Cap the filters per backward chunk of tnrd_loss_grad (0 = automatic, the
+ * default).  F < N_k keeps the filter-bank steps on the CUDA cores (the tensor
+ * banks need every filter of a stage in one chunk).  EINVAL if max_filters < 0.
+ * Host-only. */
+TNRD_API tnrd_status tnrd_set_grad_chunk(tnrd_handle *h, int max_filters);
 
 /* ---------------- steps either side of the path ----------------
  * Poisson noise (P Eq.1, l.103-111): f_dev[b][y][x] ~ Poisson(u_dev[b][y][x]) as
@@ -223,7 +238,7 @@ TNRD_API tnrd_status tnrd_sample_poisson(const float *u_dev, float *f_dev, int B
 /* PSNR per image (reading C15: 10 log10(peak_b^2 / MSE(u_b, clean_b)), unclamped;
  * +inf for equal images): u_dev, clean_dev device [B][H][ld]; peak host [B];
  * psnr_out host [B].  Squared errors summed in double in a fixed order.
- * Synchronous. */
+ * EINVAL: B outside [1, 65535], H or W < 1, ld < W.  Synchronous. */
 TNRD_API tnrd_status tnrd_psnr(const float *u_dev, const float *clean_dev, int B, int H, int W, long long ld,
                                const float *peak, double *psnr_out, void *cuda_stream);
 
@@ -258,6 +273,16 @@ TNRD_API tnrd_status tnrd_denoise_slab(tnrd_handle *h, const float *f_slab_dev, 
  * to test the partition on one GPU; result equals tnrd_denoise bitwise. */
 TNRD_API tnrd_status tnrd_denoise_slabs_loopback(tnrd_handle *h, const float *f_dev, float *u_dev, int H,
                                         int W, long long ld, int nslabs, void *cuda_stream);
+
+/* The same single-device slab partition with every halo transfer done by NCCL:
+ * per stage one grouped exchange of ncclSend / ncclRecv pairs whose peer is the
+ * caller's own rank, on the handle's communicator, which must have been created
+ * with tnrd_comm_init(h, id, 0, 1) (else ESTATE).  Moves exactly the rows and
+ * bytes the multi-rank path moves (2r rows per seam and direction), so it runs the
+ * NCCL transport of the slab path on one GPU; result equals tnrd_denoise bitwise.
+ * ENCCL on an NCCL failure. */
+TNRD_API tnrd_status tnrd_denoise_slabs_nccl_self(tnrd_handle *h, const float *f_dev, float *u_dev, int H,
+                                         int W, long long ld, int nslabs, void *cuda_stream);
 
 /* ---------------- instrumentation and micro-parity ---------------- */
 

@@ -76,6 +76,7 @@ def _load() -> ctypes.CDLL:
         "tnrd_comm_init": ([vp, vp, i, i], i),
         "tnrd_denoise_slab": ([vp, vp, vp, i, i, i, i, ll, f, vp], i),
         "tnrd_denoise_slabs_loopback": ([vp, vp, vp, i, i, ll, i, vp], i),
+        "tnrd_denoise_slabs_nccl_self": ([vp, vp, vp, i, i, ll, i, vp], i),
         "tnrd_set_profiling": ([vp, i], i),
         "tnrd_get_launch_times": ([vp, fp, i, ctypes.POINTER(i)], i),
         "tnrd_debug_phi": ([vp, i, i, vp, vp, ll, vp], i),
@@ -85,6 +86,7 @@ def _load() -> ctypes.CDLL:
         "tnrd_psnr": ([vp, vp, i, i, i, ll, fp, ctypes.POINTER(ctypes.c_double), vp], i),
         "tnrd_set_engine": ([vp, i], i),
         "tnrd_engine_for": ([vp, i, i, i], i),
+        "tnrd_set_grad_chunk": ([vp, i], i),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -98,8 +100,9 @@ EXPORTED = (
     "tnrd_abi_version", "tnrd_status_string", "tnrd_create", "tnrd_set_stage_params",
     "tnrd_denoise", "tnrd_denoise_host", "tnrd_destroy", "tnrd_last_error", "tnrd_launch_count",
     "tnrd_nccl_unique_id", "tnrd_comm_init", "tnrd_denoise_slab", "tnrd_denoise_slabs_loopback",
+    "tnrd_denoise_slabs_nccl_self",
     "tnrd_set_profiling", "tnrd_get_launch_times", "tnrd_debug_phi", "tnrd_debug_prox", "tnrd_loss_grad",
-    "tnrd_sample_poisson", "tnrd_psnr", "tnrd_set_engine", "tnrd_engine_for",
+    "tnrd_sample_poisson", "tnrd_psnr", "tnrd_set_engine", "tnrd_engine_for", "tnrd_set_grad_chunk",
 )
 
 
@@ -231,8 +234,18 @@ def tnrd_denoise_slabs_loopback(h: int, f, u, nslabs: int, stream=None) -> None:
                                             nslabs, _stream_ptr(stream)), h)
 
 
+def tnrd_denoise_slabs_nccl_self(h: int, f, u, nslabs: int, stream=None) -> None:
+    H, W = f.shape
+    _check(_lib.tnrd_denoise_slabs_nccl_self(h, _dev_ptr(f), _dev_ptr(u), H, W, f.stride(0),
+                                             nslabs, _stream_ptr(stream)), h)
+
+
 def tnrd_set_engine(h: int, engine: int) -> None:
     _check(_lib.tnrd_set_engine(h, engine), h)
+
+
+def tnrd_set_grad_chunk(h: int, max_filters: int) -> None:
+    _check(_lib.tnrd_set_grad_chunk(h, int(max_filters)), h)
 
 
 def tnrd_engine_for(h: int, B: int, H: int, W: int) -> int:

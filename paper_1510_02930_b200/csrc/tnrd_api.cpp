@@ -89,6 +89,7 @@ struct tnrd_handle {
     int tc_stride = 0;
     std::vector<char> tc_ok;      // per stage: block packed (Horner phi)
     int engine = TNRD_ENGINE_AUTO;
+    int grad_max_f = 0;           // tnrd_set_grad_chunk: cap on filters per backward chunk (0 = auto)
     // raw stage parameters (training gradient, tnrd_loss_grad)
     std::vector<float> raw_mu0, raw_step, raw_gamma;   // host [T][Nk]
     float *d_raw = nullptr;       // device: k [T][Nk][m*m], kbar [T][Nk][m*m], w [T][Nk][M]
@@ -101,9 +102,9 @@ struct tnrd_handle {
     float *scratch = nullptr;
     size_t scratch_bytes = 0;
     float *e2e_f = nullptr, *e2e_u = nullptr;
-    size_t e2e_bytes = 0;
+    size_t e2e_f_bytes = 0, e2e_u_bytes = 0;   // one capacity per buffer (grow() may free one)
     float *slab_buf[2] = {nullptr, nullptr};
-    size_t slab_bytes = 0;
+    size_t slab_bytes[2] = {0, 0};
     std::vector<float *> lb_bufs;  // loopback slab buffers
     size_t lb_bytes = 0;
     ncclComm_t comm = nullptr;
@@ -162,8 +163,11 @@ tnrd_status grow(tnrd_handle *h, float **p, size_t *have, size_t need, const cha
         *have = 0;
     }
     cudaError_t e = cudaMalloc(p, need);
-    if (e != cudaSuccess) return fail(h, TNRD_ENOMEM, "cudaMalloc(%zu) for %s: %s", need, what,
-                                      cudaGetErrorString(e));
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        cudaGetLastError();   // a failed cudaMalloc is not sticky; do not leave it for later checks
+        return fail(h, TNRD_ENOMEM, "cudaMalloc(%zu) for %s: %s", need, what, cudaGetErrorString(e));
+    }
     *have = need;
     return TNRD_OK;
 }
@@ -495,7 +499,7 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
         return fail(nullptr, TNRD_EINVAL, "need T >= 1, n_filters >= 1, 1 <= n_rbf <= 256");
     if (d->ksize < 3 || d->ksize % 2 == 0)
         return fail(nullptr, TNRD_EINVAL, "ksize must be odd and >= 3 (got %d)", d->ksize);
-    if (d->ksize > 7) return fail(nullptr, TNRD_EUNSUPPORTED, "ksize %d not built (3, 5, 7)", d->ksize);
+    if (d->ksize > 11) return fail(nullptr, TNRD_EUNSUPPORTED, "ksize %d not built (3, 5, 7, 9, 11)", d->ksize);
     if (d->boundary != 0 && d->boundary != 1) return fail(nullptr, TNRD_EINVAL, "bad boundary %d", d->boundary);
     if (d->phi_mode != TNRD_PHI_EXACT && d->phi_mode != TNRD_PHI_TABLE)
         return fail(nullptr, TNRD_EINVAL, "bad phi_mode %d", d->phi_mode);
@@ -664,6 +668,13 @@ tnrd_status tnrd_set_stage_params(tnrd_handle *h, int t, const float *filters, c
     return TNRD_OK;
 }
 
+tnrd_status tnrd_set_grad_chunk(tnrd_handle *h, int max_filters) {
+    if (!h) return fail(nullptr, TNRD_EINVAL, "null handle");
+    if (max_filters < 0) return fail(h, TNRD_EINVAL, "max_filters must be >= 0");
+    h->grad_max_f = max_filters;
+    return TNRD_OK;
+}
+
 tnrd_status tnrd_set_engine(tnrd_handle *h, int engine) {
     if (!h) return fail(nullptr, TNRD_EINVAL, "null handle");
     if (engine < TNRD_ENGINE_AUTO || engine > TNRD_ENGINE_TENSOR) return fail(h, TNRD_EINVAL, "bad engine %d", engine);
@@ -725,12 +736,10 @@ tnrd_status tnrd_denoise_host(tnrd_handle *h, const float *f_host, float *u_host
     if (B < 1 || H < 1 || W < 1) return fail(h, TNRD_EINVAL, "bad size");
     DeviceGuard g(h->d.device);
     const size_t bytes = sizeof(float) * (size_t)B * H * W;
-    size_t have_f = h->e2e_bytes, have_u = h->e2e_bytes;
-    st = grow(h, &h->e2e_f, &have_f, bytes, "e2e f");
+    st = grow(h, &h->e2e_f, &h->e2e_f_bytes, bytes, "e2e f");
     if (st != TNRD_OK) return st;
-    st = grow(h, &h->e2e_u, &have_u, bytes, "e2e u");
+    st = grow(h, &h->e2e_u, &h->e2e_u_bytes, bytes, "e2e u");
     if (st != TNRD_OK) return st;
-    h->e2e_bytes = std::min(have_f, have_u);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     // Pipeline over batch chunks: H2D of chunk c+1 and D2H of chunk c-1 (own
     // streams) overlap the stages of chunk c (caller's stream).  Chunks keep at
@@ -863,20 +872,17 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
     if (M > 64) return fail(h, TNRD_EUNSUPPORTED, "training gradient built for n_rbf <= 64");
     // filters per backward chunk: 5 per-filter images (x, a, b, w, t) within half the
     // device memory (at least 1 GB; from the total, not the free memory, so that the
-    // chunking — and with it the summation order — is the same on every call); all
-    // N_k in one chunk enables the tensor banks (C4's 256 x 512^2 batch: 64 GB)
+    // chunking — and with it the summation order — is the same on every call with the
+    // same batch); all N_k in one chunk enables the tensor banks (C4's 256 x 512^2
+    // batch: 64 GB).  tnrd_set_grad_chunk caps F explicitly.  A failed allocation is
+    // TNRD_ENOMEM: the chunk is never shrunk to what happens to be free.
     const size_t budget = std::max<size_t>((size_t)1 << 30, h->total_mem / 2);
     int F = (int)std::max<size_t>(1, std::min<size_t>((size_t)Nk, budget / (5 * n * sizeof(float))));
-    // tape u_0..u_T and ut_0..ut_{T-1} (2T+1 images) + g, gn, e + the chunk images; if
-    // the device is short of memory (other allocations), halve the chunk and retry
-    for (;;) {
-        const size_t imgs = 2 * (size_t)T + 1 + 3 + 5 * (size_t)F;
-        st = grow(h, &h->g_buf, &h->g_buf_bytes, sizeof(float) * n * imgs, "gradient tape");
-        if (st == TNRD_OK) break;
-        if (st != TNRD_ENOMEM || F == 1) return st;
-        cudaGetLastError();   // the failed cudaMalloc is not sticky; clear it
-        F = std::max(1, F / 2);
-    }
+    if (h->grad_max_f > 0) F = std::min(F, h->grad_max_f);
+    // tape u_0..u_T and ut_0..ut_{T-1} (2T+1 images) + g, gn, e + the chunk images
+    st = grow(h, &h->g_buf, &h->g_buf_bytes, sizeof(float) * n * (2 * (size_t)T + 1 + 3 + 5 * (size_t)F),
+              "gradient tape");
+    if (st != TNRD_OK) return st;
     const int grid = tnrd::grad_grid((long long)n, h->num_sms);
     const int gx = tnrd::grad_chunk_grid((long long)n, F, h->num_sms);
     const int kg_nblk = tnrd::tc_kgrad_blocks(B, H, W, h->num_sms);
@@ -884,14 +890,8 @@ tnrd_status tnrd_loss_grad(tnrd_handle *h, const float *f, const float *u_gt, in
     st = grow(h, &h->g_partial, &h->g_partial_bytes, sizeof(float) * part_floats, "partials");
     if (st != TNRD_OK) return st;
     const size_t per_f = 2 * mm + M, nred = TN * per_f + T + 1;
-    {
-        float *tmp = reinterpret_cast<float *>(h->g_red);
-        size_t have = h->g_red_bytes;
-        st = grow(h, &tmp, &have, sizeof(double) * nred, "reductions");
-        if (st != TNRD_OK) return st;
-        h->g_red = reinterpret_cast<double *>(tmp);
-        h->g_red_bytes = have;
-    }
+    st = grow(h, reinterpret_cast<float **>(&h->g_red), &h->g_red_bytes, sizeof(double) * nred, "reductions");
+    if (st != TNRD_OK) return st;
     float *tape_u = h->g_buf;                       // [T+1][n]
     float *tape_ut = tape_u + (size_t)(T + 1) * n;  // [T][n]
     float *wk = tape_ut + (size_t)T * n;
@@ -996,6 +996,7 @@ tnrd_status tnrd_psnr(const float *u, const float *c, int B, int H, int W, long 
                       double *out, void *stream) {
     if (!u || !c || !peak || !out) return fail(nullptr, TNRD_EINVAL, "null pointer");
     if (B < 1 || H < 1 || W < 1 || ld < W) return fail(nullptr, TNRD_EINVAL, "bad size");
+    if (B > 65535) return fail(nullptr, TNRD_EINVAL, "B must be <= 65535 (grid.y)");
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1107,6 +1108,79 @@ struct LoopbackExchange : SlabExchange {
         return TNRD_OK;
     }
 };
+// The slab halos of an nslabs partition moved by NCCL point-to-point on a 1-rank
+// communicator (every send and receive has the caller's own rank as peer): one
+// grouped exchange per stage, posted when the last slab's exchange is requested
+// (the earlier slabs' buffers are complete by then).  NCCL matches sends and
+// receives of one peer in posting order, so the sends list every slab's bottom
+// owned rows then every slab's top owned rows, and the receives the matching halo
+// rows of the neighbours in the same order.  Tests the NCCL transfer of the real
+// slab buffers and sizes on one GPU (tnrd_denoise_slabs_nccl_self).
+struct NcclSelfExchange : SlabExchange {
+    tnrd_handle *h; std::vector<SlabDesc> *sl; int W; cudaStream_t s;
+    NcclSelfExchange(tnrd_handle *h_, std::vector<SlabDesc> *sl_, int W_, cudaStream_t s_) : h(h_), sl(sl_), W(W_), s(s_) {}
+    tnrd_status exchange(int k, float *buf) override {
+        std::vector<SlabDesc> &v = *sl;
+        if (k + 1 < (int)v.size()) return TNRD_OK;
+        NcclApi &api = nccl();
+        const int halo = h->d.ksize - 1, n = (int)v.size();
+        const int par = (buf == v[k].buf[0]) ? 0 : 1;
+        const size_t cnt = (size_t)halo * W;
+        ncclResult_t r = api.GroupStart();
+        for (int j = 0; j + 1 < n && r == ncclSuccess; ++j)   // bottom owned rows of j -> halo of j + 1
+            r = api.Send(v[j].buf[par] + (size_t)v[j].rows * W, cnt, ncclFloat32, h->rank, h->comm, s);
+        for (int j = 1; j < n && r == ncclSuccess; ++j)       // top owned rows of j -> halo of j - 1
+            r = api.Send(v[j].buf[par] + (size_t)halo * W, cnt, ncclFloat32, h->rank, h->comm, s);
+        for (int j = 1; j < n && r == ncclSuccess; ++j)
+            r = api.Recv(v[j].buf[par], cnt, ncclFloat32, h->rank, h->comm, s);
+        for (int j = 0; j + 1 < n && r == ncclSuccess; ++j)
+            r = api.Recv(v[j].buf[par] + (size_t)(halo + v[j].rows) * W, cnt, ncclFloat32, h->rank, h->comm, s);
+        ncclResult_t r2 = api.GroupEnd();
+        if (r != ncclSuccess || r2 != ncclSuccess)
+            return fail(h, TNRD_ENCCL, "self halo exchange: %s", api.GetErrorString(r != ncclSuccess ? r : r2));
+        return TNRD_OK;
+    }
+};
+
+// Slab descriptors of an nslabs partition of one image, with handle-owned buffers.
+tnrd_status setup_loopback(tnrd_handle *h, const float *f, float *u, int H, int W, long long ld, int nslabs,
+                           std::vector<SlabDesc> &sl) {
+    const int halo = h->d.ksize - 1;
+    sl.assign(nslabs, SlabDesc{});
+    int maxrows = 0;
+    for (int k = 0; k < nslabs; ++k) {
+        const int r0 = (int)((long long)H * k / nslabs), r1 = (int)((long long)H * (k + 1) / nslabs);
+        tnrd_status st = slab_args_ok(h, H, W, r0, r1 - r0, ld);
+        if (st != TNRD_OK) return st;
+        sl[k].row0 = r0; sl[k].rows = r1 - r0;
+        maxrows = std::max(maxrows, r1 - r0);
+    }
+    const size_t bytes = sizeof(float) * (size_t)(maxrows + 2 * halo) * W;
+    if ((int)h->lb_bufs.size() < 2 * nslabs || h->lb_bytes < bytes) {
+        cudaDeviceSynchronize();
+        for (float *p : h->lb_bufs) cudaFree(p);
+        h->lb_bufs.clear();
+        h->lb_bytes = 0;
+        std::vector<float *> bufs(2 * nslabs, nullptr);
+        for (auto &p : bufs) {
+            cudaError_t e = cudaMalloc(&p, bytes);
+            if (e != cudaSuccess) {   // release the partial set: the handle keeps none
+                for (float *q : bufs) cudaFree(q);
+                cudaGetLastError();
+                return fail(h, TNRD_ENOMEM, "loopback buffers: %s", cudaGetErrorString(e));
+            }
+        }
+        h->lb_bufs = bufs;
+        h->lb_bytes = bytes;
+    }
+    for (int k = 0; k < nslabs; ++k) {
+        sl[k].buf[0] = h->lb_bufs[2 * k];
+        sl[k].buf[1] = h->lb_bufs[2 * k + 1];
+        sl[k].f = f + (size_t)sl[k].row0 * ld; sl[k].f_ld = ld;
+        sl[k].u = u + (size_t)sl[k].row0 * ld; sl[k].u_ld = ld;
+    }
+    return TNRD_OK;
+}
 }  // namespace
 
 tnrd_status tnrd_denoise_slab(tnrd_handle *h, const float *f_slab, float *u_slab, int H, int W, int row0, int rows,
@@ -1121,12 +1195,10 @@ tnrd_status tnrd_denoise_slab(tnrd_handle *h, const float *f_slab, float *u_slab
     DeviceGuard g(h->d.device);
     const int halo = h->d.ksize - 1;
     const size_t bytes = sizeof(float) * (size_t)(rows + 2 * halo) * W;
-    size_t have0 = h->slab_bytes, have1 = h->slab_bytes;
-    st = grow(h, &h->slab_buf[0], &have0, bytes, "slab buffer");
-    if (st != TNRD_OK) return st;
-    st = grow(h, &h->slab_buf[1], &have1, bytes, "slab buffer");
-    if (st != TNRD_OK) return st;
-    h->slab_bytes = std::min(have0, have1);
+    for (int k = 0; k < 2; ++k) {
+        st = grow(h, &h->slab_buf[k], &h->slab_bytes[k], bytes, "slab buffer");
+        if (st != TNRD_OK) return st;
+    }
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     std::vector<SlabDesc> sl{{row0, rows, {h->slab_buf[0], h->slab_buf[1]}, f_slab, ld, u_slab, ld}};
     NcclExchange ex(h, rows, W, s);
@@ -1144,35 +1216,27 @@ tnrd_status tnrd_denoise_slabs_loopback(tnrd_handle *h, const float *f, float *u
     if (!f || !u || f == u) return fail(h, TNRD_EINVAL, "bad pointers");
     if (nslabs < 1 || nslabs > H) return fail(h, TNRD_EINVAL, "nslabs");
     DeviceGuard g(h->d.device);
-    const int halo = h->d.ksize - 1;
-    std::vector<SlabDesc> sl(nslabs);
-    int maxrows = 0;
-    for (int k = 0; k < nslabs; ++k) {
-        const int r0 = (int)((long long)H * k / nslabs), r1 = (int)((long long)H * (k + 1) / nslabs);
-        st = slab_args_ok(h, H, W, r0, r1 - r0, ld);
-        if (st != TNRD_OK) return st;
-        sl[k].row0 = r0; sl[k].rows = r1 - r0;
-        maxrows = std::max(maxrows, r1 - r0);
-    }
-    const size_t bytes = sizeof(float) * (size_t)(maxrows + 2 * halo) * W;
-    if ((int)h->lb_bufs.size() < 2 * nslabs || h->lb_bytes < bytes) {
-        cudaDeviceSynchronize();
-        for (float *p : h->lb_bufs) cudaFree(p);
-        h->lb_bufs.assign(2 * nslabs, nullptr);
-        for (auto &p : h->lb_bufs) {
-            cudaError_t e = cudaMalloc(&p, bytes);
-            if (e != cudaSuccess) return fail(h, TNRD_ENOMEM, "loopback buffers: %s", cudaGetErrorString(e));
-        }
-        h->lb_bytes = bytes;
-    }
-    for (int k = 0; k < nslabs; ++k) {
-        sl[k].buf[0] = h->lb_bufs[2 * k];
-        sl[k].buf[1] = h->lb_bufs[2 * k + 1];
-        sl[k].f = f + (size_t)sl[k].row0 * ld; sl[k].f_ld = ld;
-        sl[k].u = u + (size_t)sl[k].row0 * ld; sl[k].u_ld = ld;
-    }
+    std::vector<SlabDesc> sl;
+    st = setup_loopback(h, f, u, H, W, ld, nslabs, sl);
+    if (st != TNRD_OK) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     LoopbackExchange ex(h, &sl, W, s);
+    return run_slabs(h, sl, H, W, ex, s);
+}
+
+tnrd_status tnrd_denoise_slabs_nccl_self(tnrd_handle *h, const float *f, float *u, int H, int W, long long ld,
+                                         int nslabs, void *stream) {
+    tnrd_status st = check_ready(h);
+    if (st != TNRD_OK) return st;
+    if (!h->comm || h->nranks != 1) return fail(h, TNRD_ESTATE, "needs a 1-rank communicator (tnrd_comm_init)");
+    if (!f || !u || f == u) return fail(h, TNRD_EINVAL, "bad pointers");
+    if (nslabs < 1 || nslabs > H) return fail(h, TNRD_EINVAL, "nslabs");
+    DeviceGuard g(h->d.device);
+    std::vector<SlabDesc> sl;
+    st = setup_loopback(h, f, u, H, W, ld, nslabs, sl);
+    if (st != TNRD_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    NcclSelfExchange ex(h, &sl, W, s);
     return run_slabs(h, sl, H, W, ex, s);
 }
 

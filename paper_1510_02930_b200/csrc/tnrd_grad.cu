@@ -571,9 +571,17 @@ cudaError_t grad_chunk(const GradChunk &c, cudaStream_t s) {
         TNRD_M(fwd_pair_kernel, g, c.u, c.e, c.boundary, c.x, c.a)
     }
     {   // phi_all: one full wave of resident blocks (its grid-stride loop then balances)
-        static int occ = 0;
-        if (occ == 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, phi_all_kernel, kPhiThreads, 0) != cudaSuccess)
-            occ = 1;
+        // resident blocks per SM, cached per device (it sets the grid and with it the
+        // summation order, so it must not depend on which device ran first)
+        static int occ_cache[64] = {0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int occ = dev < 64 ? occ_cache[dev] : 0;
+        if (occ == 0) {
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, phi_all_kernel, kPhiThreads, 0) != cudaSuccess)
+                occ = 1;
+            if (dev < 64) occ_cache[dev] = occ;
+        }
         const int gphi = std::max(1, std::min(c.gx, std::max(1, c.num_sms * std::max(occ, 1) / c.F)));
         phi_all_kernel<<<dim3(gphi, c.F), kPhiThreads, 0, s>>>(g, c.x, c.a, c.w, c.b, c.partial);
         reduce_f_warp_kernel<<<dim3(c.M, c.F), 32, 0, s>>>(c.partial, gphi, 64, c.red, c.red_stride, 2 * mm);

@@ -665,6 +665,10 @@ size_t stage_smem_bytes(int ksize, int tile, int Nk, int pstride) {
         case 11: return smem_bytes<5, Cfg1>(Nk, pstride);
         case 14: return smem_bytes<7, Cfg0>(Nk, pstride);
         case 15: return smem_bytes<7, Cfg1>(Nk, pstride);
+        case 18: return smem_bytes<9, Cfg0>(Nk, pstride);
+        case 19: return smem_bytes<9, Cfg1>(Nk, pstride);
+        case 22: return smem_bytes<11, Cfg0>(Nk, pstride);
+        case 23: return smem_bytes<11, Cfg1>(Nk, pstride);
     }
     return 0;
 }
@@ -686,6 +690,10 @@ cudaError_t launch_stage(int ksize, int tile, StageArgs &a, int B, cudaStream_t 
         case 11: return launch<5, Cfg1>(a, B, s);
         case 14: return launch<7, Cfg0>(a, B, s);
         case 15: return launch<7, Cfg1>(a, B, s);
+        case 18: return launch<9, Cfg0>(a, B, s);
+        case 19: return launch<9, Cfg1>(a, B, s);
+        case 22: return launch<11, Cfg0>(a, B, s);
+        case 23: return launch<11, Cfg1>(a, B, s);
     }
     return cudaErrorInvalidValue;
 }

@@ -43,8 +43,10 @@ def test_abi_version_and_status_strings():
 
 def test_create_rejects_bad_shapes_before_touching_the_device():
     import paper_1510_02930_b200 as P
-    for args, status in [((0, 8, 3, 63), 1), ((2, 8, 4, 63), 1), ((2, 0, 3, 63), 1),
-                         ((2, 8, 9, 63), 6), ((2, 8, 3, 0), 1)]:
+    # ksize: even or < 3 is invalid (S l.31-32); odd sizes up to 11 are built (P l.458-469
+    # studies 3..9), larger odd sizes are EUNSUPPORTED
+    for args, status in [((0, 8, 3, 63), 1), ((2, 8, 4, 63), 1), ((2, 8, 10, 63), 1), ((2, 8, 1, 63), 1),
+                         ((2, 0, 3, 63), 1), ((2, 8, 13, 63), 6), ((2, 8, 3, 0), 1)]:
         with pytest.raises(P.TNRDError) as ei:
             P.tnrd_create(*args)
         assert ei.value.status == status, (args, str(ei.value))

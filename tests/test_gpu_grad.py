@@ -136,3 +136,26 @@ def test_filter_gradient_tensor_gemm_vs_cuda_cores(torch_cuda, tmp_path, boundar
         scale = float(np.max(np.abs(b[t])))
         err = float(np.max(np.abs(a[t] - b[t])))
         assert err <= 2e-5 * scale, (t, err, scale)
+
+
+@pytest.mark.parametrize("F", [1, 5, 16])
+def test_loss_grad_multi_chunk(torch_cuda, F):
+    """The backward split into chunks of F < N_k filters (tnrd_set_grad_chunk; the
+    CUDA-core banks, since the tensor banks need all filters in one chunk): same
+    oracle bound, and two calls with the same cap are bitwise equal."""
+    import paper_1510_02930_b200 as P
+    torch = torch_cuda
+    f, gt, m = _case(41 + F, 2, 40, 52, 2, 48, 7, 63, w_scale=3.0)
+    eng = P.TNRD(m)
+    P.tnrd_set_grad_chunk(eng.h, F)
+    ft, gtt = torch.from_numpy(f).cuda(), torch.from_numpy(gt).cuda()
+    loss, gf, gw, gl = eng.loss_grad(ft, gtt)
+    loss2, gf2, gw2, gl2 = eng.loss_grad(ft, gtt)
+    eng.close()
+    assert loss == loss2 and np.array_equal(gf, gf2) and np.array_equal(gw, gw2) and np.array_equal(gl, gl2)
+    rl, rf, rw, rlam = oracle.loss_grad(f, gt, m, 0)
+    assert abs(loss - rl) <= 1e-5 * abs(rl), (loss, rl)
+    for t in range(m.T):
+        _check(gf[t], rf[t], f"F={F} d filters t={t}")
+        _check(gw[t], rw[t], f"F={F} d rbf_w t={t}")
+    _check(gl, rlam, f"F={F} d lambda")

@@ -131,16 +131,37 @@ def _windows(H, W, n_rand, rng, size=64):
     return wins
 
 
+def _seam_windows(H, W, rng, n_seam=2, n_int=1, size=48, oh=128, ow=58):
+    """Windows centred on tile seams of the tensor engine's launch geometry (output
+    tiles of ow columns; row seams every oh rows, and the persistent kernel's row
+    segments start anywhere, so row seams are drawn at random too) plus interior
+    windows away from every image edge."""
+    wins = []
+    for _ in range(n_seam):
+        ky = int(rng.integers(1, max(2, H // oh)))
+        kx = int(rng.integers(1, max(2, W // ow)))
+        yc = min(max(ky * oh + int(rng.integers(-6, 7)), size // 2), H - size // 2)
+        xc = min(max(kx * ow + int(rng.integers(-6, 7)), size // 2), W - size // 2)
+        wins.append((yc - size // 2, yc + size // 2, xc - size // 2, xc + size // 2))
+    for _ in range(n_int):
+        y, x = int(rng.integers(64, H - 64 - size)), int(rng.integers(64, W - 64 - size))
+        wins.append((y, y + size, x, x + size))
+    return wins
+
+
 def test_c4_full_batch_windows(torch_cuda, P):
     """C4: all 256 images at 512^2 in one call (the bench's launch); windows of one
-    image per peak plus random images are checked against the oracle."""
+    image per peak plus random images are checked against the oracle: the four
+    corners and an edge (image boundaries), tile-seam windows and an interior one,
+    each also on |dPSNR| < 0.01 dB against its clean window."""
     p = make_problem(4)
     u = _gpu_denoise(P, torch_cuda, p.model, p.f, peak=p.peaks)
     rng = np.random.default_rng(4)
     for b in [0, 1, 2, 3, 4, 137, 255]:
-        for (y0, y1, x0, x1) in _windows(512, 512, 1, rng)[:5]:
+        for (y0, y1, x0, x1) in _windows(512, 512, 0, rng)[:5] + _seam_windows(512, 512, rng):
             ref = oracle.denoise_window(p.f[b], p.model, y0, y1, x0, x1)
-            _assert_parity(u[b, y0:y1, x0:x1], ref, float(p.peaks[b]), what=f"C4 b={b} win=({y0},{x0})")
+            _assert_parity(u[b, y0:y1, x0:x1], ref, float(p.peaks[b]), p.clean[b, y0:y1, x0:x1],
+                           what=f"C4 b={b} win=({y0},{x0})")
 
 
 def test_c4_c5_fp32_engine_windows_and_engine_agreement(torch_cuda, P):
@@ -165,18 +186,21 @@ def test_c4_c5_fp32_engine_windows_and_engine_agreement(torch_cuda, P):
 
 
 def test_c5_full_image_windows(torch_cuda, P):
+    """C5 (one 8192^2 image, peak 0.1) in the bench's one-GPU launch: corner, edge,
+    random, tile-seam and 8-way slab-seam windows against the oracle, each with
+    |dPSNR| < 0.01 dB against its clean window."""
     p = make_problem(5)
     u = _gpu_denoise(P, torch_cuda, p.model, p.f)[0]
     rng = np.random.default_rng(5)
-    worst = 0.0
-    for (y0, y1, x0, x1) in _windows(8192, 8192, 6, rng, size=48):
+    clean = p.clean[0]
+    for (y0, y1, x0, x1) in _windows(8192, 8192, 6, rng, size=48) + _seam_windows(8192, 8192, rng, 3, 0):
         ref = oracle.denoise_window(p.f[0], p.model, y0, y1, x0, x1)
-        worst = max(worst, _assert_parity(u[y0:y1, x0:x1], ref, 0.1, what=f"C5 win=({y0},{x0})"))
+        _assert_parity(u[y0:y1, x0:x1], ref, 0.1, clean[y0:y1, x0:x1], what=f"C5 win=({y0},{x0})")
     # also the seams of an 8-way slab partition (rows 1024*k)
     for k in (1, 4, 7):
         y = 1024 * k - 24
         ref = oracle.denoise_window(p.f[0], p.model, y, y + 48, 4000, 4048)
-        _assert_parity(u[y:y + 48, 4000:4048], ref, 0.1, what=f"C5 seam {k}")
+        _assert_parity(u[y:y + 48, 4000:4048], ref, 0.1, clean[y:y + 48, 4000:4048], what=f"C5 seam {k}")
 
 
 # ------------------------------------------------------------------ edge cases
@@ -195,6 +219,21 @@ def test_ragged_and_minimum_sizes(torch_cuda, P, k, H, W):
     u = _gpu_denoise(P, torch_cuda, model, f)
     for b in range(2):
         _assert_parity(u[b], oracle.denoise(f[b], model), 4.0, what=f"k{k} {H}x{W} b{b}")
+
+
+@pytest.mark.parametrize("k,H,W,bc", [(9, 9, 9, 0), (9, 41, 70, 0), (9, 38, 45, 1), (11, 47, 33, 0)])
+def test_large_ksize_fp32_engine(torch_cuda, P, k, H, W, bc):
+    """P l.458-469 (Fig.3) studies filters up to 9x9 (N_k = m^2 - 1 = 80): the FP32
+    engine against the oracle, R1 and R2, at minimum and ragged sizes; and 11x11."""
+    rng = np.random.default_rng(900 + k + H)
+    nk = k * k - 1 if k <= 9 else 48   # 11x11: fewer filters so the operands fit shared memory
+    model = make_model(rng, 2, nk, k, 63, 6.0)
+    f = rng.poisson(rng.uniform(0, 4, (1, H, W))).astype(np.float32)
+    eng = P.TNRD(model, boundary=bc)
+    assert eng.engine_for(1, H, W) == P.ENGINE_FP32
+    eng.close()
+    u = _gpu_denoise(P, torch_cuda, model, f, boundary=bc)
+    _assert_parity(u[0], oracle.denoise(f[0], model, boundary=bc), 4.0, what=f"k{k} {H}x{W} bc{bc}")
 
 
 def test_stress_stage_phi_nonlinear(torch_cuda, P):
@@ -291,6 +330,48 @@ def test_loopback_slabs_bitwise_equal_full(torch_cuda, P, nslabs, engine, bounda
     torch.cuda.synchronize()
     assert torch.equal(full, u)
     eng.close()
+
+
+@pytest.mark.parametrize("nslabs", [2, 3, 8])
+def test_nccl_self_exchange_slabs_bitwise_equal_full(torch_cuda, P, nslabs):
+    """The slab halos moved by real NCCL point-to-point (ncclSend / ncclRecv to the
+    own rank of a 1-rank communicator, grouped per stage): bitwise equal to the
+    single-image result, like the copy loopback (P15)."""
+    torch = torch_cuda
+    p = make_problem(3)
+    eng = P.TNRD(p.model)
+    P.tnrd_comm_init(eng.h, P.tnrd_nccl_unique_id(), 0, 1)
+    f = torch.from_numpy(p.f[0]).cuda()
+    full = eng.denoise(f)
+    u = torch.empty_like(f)
+    P.tnrd_denoise_slabs_nccl_self(eng.h, f, u, nslabs)
+    torch.cuda.synchronize()
+    assert torch.equal(full, u)
+    eng.close()
+
+
+def test_c5_eight_slabs_full_size_every_seam(torch_cuda, P):
+    """C5 at full size (8192^2, peak 0.1) as the 8-way slab partition (halos by NCCL
+    to self, the multi-GPU bench's row split): bitwise equal to the one-call result,
+    and oracle windows (with dPSNR) straddling each of the 7 seams."""
+    torch = torch_cuda
+    p = make_problem(5)
+    eng = P.TNRD(p.model)
+    P.tnrd_comm_init(eng.h, P.tnrd_nccl_unique_id(), 0, 1)
+    f = torch.from_numpy(p.f[0]).cuda()
+    full = eng.denoise(f)
+    u = torch.empty_like(f)
+    P.tnrd_denoise_slabs_nccl_self(eng.h, f, u, 8)
+    torch.cuda.synchronize()
+    assert torch.equal(full, u)
+    un = u.cpu().numpy()
+    eng.close()
+    rng = np.random.default_rng(55)
+    for k in range(1, 8):
+        y = 1024 * k - 24
+        x = int(rng.integers(0, 8192 - 48))
+        ref = oracle.denoise_window(p.f[0], p.model, y, y + 48, x, x + 48)
+        _assert_parity(un[y:y + 48, x:x + 48], ref, 0.1, p.clean[0, y:y + 48, x:x + 48], what=f"C5 8-slab seam {k}")
 
 
 def test_host_entry_point_matches_device_path(torch_cuda, P):
@@ -414,9 +495,10 @@ def test_table_phi_c4_windows(torch_cuda, P):
     u = _gpu_denoise(P, torch_cuda, p.model, p.f, peak=p.peaks, phi_mode=P.PHI_TABLE)
     rng = np.random.default_rng(44)
     for b in [0, 1, 2, 3, 4, 200]:
-        for (y0, y1, x0, x1) in _windows(512, 512, 1, rng)[:3]:
+        for (y0, y1, x0, x1) in _windows(512, 512, 0, rng)[:3] + _seam_windows(512, 512, rng):
             ref = oracle.denoise_window(p.f[b], p.model, y0, y1, x0, x1)
-            _assert_parity(u[b, y0:y1, x0:x1], ref, float(p.peaks[b]), what=f"table C4 b={b} win=({y0},{x0})")
+            _assert_parity(u[b, y0:y1, x0:x1], ref, float(p.peaks[b]), p.clean[b, y0:y1, x0:x1],
+                           what=f"table C4 b={b} win=({y0},{x0})")
 
 
 def test_table_phi_stress_and_micro(torch_cuda, P):

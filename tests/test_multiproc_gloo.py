@@ -135,3 +135,25 @@ def test_halo_of_r_rows_is_not_enough(tmp_path):
     e0 = r0 - r  # only r rows of halo from above
     ut = oracle.stage(f[e0:], f[e0:], model, 0)
     assert not np.array_equal(ut[r0 - e0:], ref[r0:])
+
+
+@pytest.mark.parametrize("config,expect", [(4, [[0, 128], [128, 256]]), (5, [[0, 4096], [4096, 8192]])])
+def test_bench_gpus_flag_relaunches_ranks(config, expect):
+    """bench.py --gpus 2 without torchrun re-launches itself as 2 ranks
+    (torch.distributed.run); --dry-run runs that plumbing over gloo on CPU. Rank 0
+    prints exactly one JSON line with n_gpus = 2 and every rank's shard."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run",
+                        "--config", str(config), "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, env=env, timeout=300, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    out = json.loads(lines[0])
+    assert out["n_gpus"] == 2 and out["dry_run"] and out["scaling"] == "strong"
+    assert out["shards"] == expect
+    assert out["config"]["parallelism"].endswith("x2")

@@ -343,9 +343,11 @@ def test_p14_batch_independence():
 
 
 # ---------------------------------------------------------------- P16 fp32 noise floor
-# Gate: fp32 drift <= P16_GATE x tolerance, i.e. >= 5x headroom for the kernel's own
-# (different) fp32 rounding order.  Measured: 0.006-0.10 x tol.
-P16_GATE = 0.2
+# Gate: fp32 drift <= 0.1 x tolerance, i.e. >= 10x headroom for the
+# kernel's own (different) fp32 rounding order.  The emulation is deterministic numpy;
+# measured 0.003-0.069 x tol on the C1-C3 / C5 cases and 0.006-0.0999 on the C4
+# peaks (peak 0.1 is the tightest: DESIGN.md §4).
+P16_GATE = 0.1
 
 
 @pytest.mark.parametrize("cfg,window", [(1, None), (2, (100, 50, 96)), (3, (100, 50, 80)),
@@ -420,6 +422,42 @@ def test_reactions_with_zero_filters_are_scalar_iterations():
         lam = float(m.lam[t])
         v = v - lam * (1.0 - np.where(f == 0, 0.0, f / v))
     assert np.max(np.abs(up - v)) < 1e-12
+
+
+def test_direct_poisson_gradient_reads_u_t_not_u_tilde():
+    """P Eq.3 (l.134-141): psi(u_t, f) is evaluated at the stage input u_t, not at the
+    diffused u_tilde.  One stage with a shift filter and linear phi makes u_tilde !=
+    u_t everywhere; the expectation is assembled here with numpy slicing:
+    v(p,q) = E(u)(p, q-1), w = c v, (kbar * w)(p,q) = E(w)(p, q+1), u_tilde = u - kbar*w,
+    u_next = u_tilde - lam (1 - f/u_t) (f/u_t := 0 where f = 0, l.163-167)."""
+    rng = _rng(23)
+    H, W = 9, 11
+    mdl = make_model(rng, 1, 1, 3, 63, 4.0)
+    mdl.filters[...] = 0
+    mdl.filters[0, 0, 1, 2] = 1.0          # true convolution: v(p, q) = u(p, q - 1)
+    mdl.rbf_w[0, 0, 0] = np.float32(0.375)  # phi_0(z) = 0.375 z (PHI_LINEAR)
+    c = float(mdl.rbf_w[0, 0, 0])
+    lam = float(mdl.lam[0])
+    u = rng.uniform(0.5, 3.0, (H, W))
+    f = rng.integers(0, 5, (H, W)).astype(np.float64)
+    v = np.empty_like(u)
+    v[:, 1:] = u[:, :-1]
+    v[:, 0] = u[:, 0]                       # half-sample mirror at q = -1
+    w = c * v
+    d = np.empty_like(u)
+    d[:, :-1] = w[:, 1:]
+    d[:, -1] = w[:, -1]                     # mirror at q = W
+    ut = u - d
+    ratio = np.where(f == 0, 0.0, f / np.where(f == 0, 1.0, u))
+    expect = ut - lam * (1.0 - ratio)
+    got = oracle.stage(u, f, mdl, 0, phi_mode=oracle.PHI_LINEAR, reaction=oracle.REACTION_POISSON_GRADIENT)
+    assert np.max(np.abs(got - expect)) < 1e-12
+    # negative control: psi evaluated at u_tilde would differ by lam f |1/u - 1/u_tilde|
+    wrong = ut - lam * (1.0 - np.where(f == 0, 0.0, f / np.where(f == 0, 1.0, ut)))
+    assert np.max(np.abs(got - wrong)) > 1e-2
+    # the Gaussian reaction reads u_t the same way: u_tilde - lam (u_t - f)
+    got_g = oracle.stage(u, f, mdl, 0, phi_mode=oracle.PHI_LINEAR, reaction=oracle.REACTION_GAUSSIAN)
+    assert np.max(np.abs(got_g - (ut - lam * (u - f)))) < 1e-12
 
 
 def test_direct_poisson_gradient_loses_positivity_and_prox_does_not():

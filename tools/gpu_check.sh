@@ -16,7 +16,7 @@ import json; d=json.loads(open('gpurun_out/bench_$tag.json').read().strip().spli
 print('BENCH', d['value'], 'MPix/s', 'launch_ms', d['roofline']['mean_launch_ms'], 'frac', d['roofline']['frac'])" || tail -5 gpurun_out/bench_$tag.err
 for what in "$@"; do
   case $what in
-    ncu) timeout 600 ncu --set full --import-source on --clock-control none -k regex:stage_kernel --launch-skip 8 --launch-count 1 \
+    ncu) timeout 600 ncu --set full --import-source on --clock-control none -k regex:stage_kernel --launch-skip 9 --launch-count 1 \
            -o gpurun_out/${tag}_stage python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/${tag}_ncu.log 2>&1; tail -1 gpurun_out/${tag}_ncu.log ;;
   esac
 done
