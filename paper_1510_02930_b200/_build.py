@@ -45,7 +45,6 @@ def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()
     ptxas_log = []
     for src, extra in [("tnrd_kernels.cu", ARCH + ["-lineinfo", "-fmad=false", "-Xptxas", "-v"] + ["-D" + d for d in defines]),
                        ("tnrd_tc.cu", ARCH + ["-lineinfo", "-fmad=false", "-Xptxas", "-v"] + ["-D" + d for d in defines]),
-                       ("tnrd_stream.cu", ARCH + ["-lineinfo", "-fmad=false", "-Xptxas", "-v"] + ["-D" + d for d in defines]),
                        ("tnrd_grad.cu", ARCH + ["-lineinfo", "-Xptxas", "-v"] + ["-D" + d for d in defines]),
                        ("tnrd_data.cu", ARCH + ["-lineinfo"]),
                        ("tnrd_api.cpp", [])]:

@@ -87,7 +87,6 @@ struct tnrd_handle {
     // tensor-core engine (tnrd_tc.cu): per stage operand block [T][tc_stride]
     float *d_tc = nullptr;
     int tc_stride = 0;
-    float *d_tcs = nullptr;       // streaming engine operand block [T][tc_stride] (tnrd_stream.cu)
     std::vector<char> tc_ok;      // per stage: block packed (Horner phi)
     int engine = TNRD_ENGINE_AUTO;
     int grad_max_f = 0;           // tnrd_set_grad_chunk: cap on filters per backward chunk (0 = auto)
@@ -184,7 +183,6 @@ tnrd_status check_ready(tnrd_handle *h) {
 struct Plan {
     int tile = 1;    // FP32 engine: 0 = "L" (tile pairs of 64x64), 1 = "S"
     int tc_oh = 0;   // > 0: tensor-core engine with tiles of tc_oh output rows
-    bool stream = false;   // tensor engine as the persistent streaming kernel where rows are TMA-able
 };
 
 // The tensor-core engine can run every stage of this handle: a built (ksize, N_k)
@@ -212,10 +210,6 @@ Plan plan_for(const tnrd_handle *h, int B, int H, int W, bool allow_tc) {
         p.tc_oh = tnrd::tc_choose_rows(h->d.ksize, B, H, W, h->num_sms);
         static const char *rows = getenv("TNRD_TC_ROWS");  // tests: force the tile height
         if (rows && atoi(rows) >= 2 && atoi(rows) % 2 == 0) p.tc_oh = atoi(rows);
-        // the persistent streaming kernel is an opt-in experiment:
-        // TNRD_STREAM=1 (it measured slower than the per-tile kernel, the default)
-        const char *stream = getenv("TNRD_STREAM");
-        p.stream = h->d_tcs != nullptr && stream && stream[0] == '1';
         return p;
     }
     static const char *force = getenv("TNRD_FORCE_TILE");
@@ -251,10 +245,7 @@ tnrd_status launch_one(tnrd_handle *h, int t, const Plan &plan, StageArgs &a, in
         }
         TNRD_CUDA(h, cudaEventRecord(h->ev[h->ev_used], s));
     }
-    const bool stream = plan.tc_oh > 0 && plan.stream && tnrd::stream_args_ok(a);
-    if (stream) a.params = h->d_tcs + (size_t)t * h->tc_stride;
-    cudaError_t e = stream ? tnrd::launch_stage_stream(h->d.ksize, a, B, h->num_sms, s)
-                  : plan.tc_oh > 0 ? tnrd::launch_stage_tc(h->d.ksize, a, B, s)
+    cudaError_t e = plan.tc_oh > 0 ? tnrd::launch_stage_tc(h->d.ksize, a, B, s)
                                    : tnrd::launch_stage(h->d.ksize, plan.tile, a, B, s);
     if (e != cudaSuccess) return cuda_fail(h, e, "stage kernel launch");
     if (h->profile) {
@@ -435,8 +426,7 @@ float tf32_rn_host(float x) {
     return r;
 }
 
-void pack_tc_stage(const tnrd_desc &d, const float *filters, const float *phi_host, int ps, int mode, float *out,
-                   bool stream = false) {
+void pack_tc_stage(const tnrd_desc &d, const float *filters, const float *phi_host, int ps, int mode, float *out) {
     const int K = d.ksize, Nk = d.n_filters, M = d.n_rbf, KT = K * K;
     const int KTP = tnrd::tc_ktp(K), NZ = tnrd::tc_nz(K), PPS = tnrd::tc_pair_stride(M), NB = (M + 7) / 8;
     std::memset(out, 0, sizeof(float) * tnrd::tc_par_floats(K, Nk, M));
@@ -447,11 +437,8 @@ void pack_tc_stage(const tnrd_desc &d, const float *filters, const float *phi_ho
         for (int t = 0; t < KT; ++t) {
             const float x = filters[(size_t)n * KT + t];
             const float hi = tf32_rn_host(x), lo = tf32_rn_host(x - hi);
-            // streaming engine: tap (ta, tb) is forward-GEMM column ta * 8 + (7 - tb)
-            // (tnrd_stream.cu E rows); per-tile engine: column t (taps row-major)
-            const int col = stream ? (t / K) * 8 + (7 - t % K) : t;
-            bf_hi[tnrd::tc_b_index(n, col, KTP)] = hi;
-            bf_lo[tnrd::tc_b_index(n, col, KTP)] = lo;
+            bf_hi[tnrd::tc_b_index(n, t, KTP)] = hi;   // forward-GEMM column t (taps row-major)
+            bf_lo[tnrd::tc_b_index(n, t, KTP)] = lo;
             ba_hi[tnrd::tc_b_index(t, n, Nk)] = hi;
             ba_lo[tnrd::tc_b_index(t, n, Nk)] = lo;
         }
@@ -530,7 +517,6 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
         cudaFree(hh->d_params);
         cudaFree(hh->d_raw);
         cudaFree(hh->d_tc);
-        cudaFree(hh->d_tcs);
         cudaFree(hh->d_table);
         delete hh;
     };
@@ -581,14 +567,6 @@ tnrd_status tnrd_create(const tnrd_desc *d, tnrd_handle **out) {
         if (e != cudaSuccess) {
             release(h);
             return fail(nullptr, TNRD_ENOMEM, "cudaMalloc tensor-core operands: %s", cudaGetErrorString(e));
-        }
-        if (tnrd::stream_supported(d->ksize, d->n_filters) && tnrd::tc_ktp(d->ksize) == 8 * d->ksize &&
-            (long long)tnrd::stream_smem_bytes(d->ksize, d->n_filters, h->tc_stride) <= smem_optin) {
-            e = cudaMalloc(&h->d_tcs, sizeof(float) * (size_t)d->T * h->tc_stride);
-            if (e != cudaSuccess) {
-                release(h);
-                return fail(nullptr, TNRD_ENOMEM, "cudaMalloc streaming operands: %s", cudaGetErrorString(e));
-            }
         }
     }
     if (d->phi_mode == TNRD_PHI_TABLE) {
@@ -681,11 +659,6 @@ tnrd_status tnrd_set_stage_params(tnrd_handle *h, int t, const float *filters, c
         pack_tc_stage(h->d, filters, host.data(), ps, mode, tc.data());
         TNRD_CUDA(h, cudaMemcpy(h->d_tc + (size_t)t * h->tc_stride, tc.data(), sizeof(float) * tc.size(),
                                 cudaMemcpyHostToDevice));
-        if (h->d_tcs) {
-            pack_tc_stage(h->d, filters, host.data(), ps, mode, tc.data(), true);
-            TNRD_CUDA(h, cudaMemcpy(h->d_tcs + (size_t)t * h->tc_stride, tc.data(), sizeof(float) * tc.size(),
-                                    cudaMemcpyHostToDevice));
-        }
         h->tc_ok[t] = 1;
     }
     h->pstride[t] = ps;
@@ -815,7 +788,6 @@ tnrd_status tnrd_destroy(tnrd_handle *h) {
         cudaDeviceSynchronize();
         cudaFree(h->d_params);
         cudaFree(h->d_tc);
-        cudaFree(h->d_tcs);
         cudaFree(h->d_table);
         cudaFree(h->d_raw);
         cudaFree(h->g_buf);

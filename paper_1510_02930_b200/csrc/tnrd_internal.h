@@ -135,15 +135,6 @@ size_t tc_min_smem_bytes(int ksize, int Nk, int par_floats);
 int tc_choose_rows(int ksize, int B, int H, int W, int num_sms);
 cudaError_t launch_stage_tc(int ksize, StageArgs &a, int B, cudaStream_t s);
 
-// Persistent streaming tensor-core engine (tnrd_stream.cu): the same
-// operand block as the tensor engine except the forward taps, which use the
-// streaming K order (tap row ta = chunk ta, word jw = tap column 7 - jw, word 0 = 0
-// for K = 7; pack with stream = true).  stream_args_ok: TMA-able rows.
-bool stream_supported(int ksize, int Nk);
-bool stream_args_ok(const StageArgs &a);
-size_t stream_smem_bytes(int ksize, int Nk, int par_floats);
-cudaError_t launch_stage_stream(int ksize, const StageArgs &a, int B, int num_sms, cudaStream_t s);
-
 // Training-gradient kernels (tnrd_grad.cu); all images dense [B][H][W] unless an ld is given.
 int grad_grid(long long n, int num_sms);
 cudaError_t grad_loss(const float *uT, const float *gt, long long gt_ld, int B, int H, int W, float *g,

@@ -38,8 +38,29 @@
 // are timing experiments / tuning knobs, never set in the product build.
 #include "tnrd_tc_common.cuh"
 
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
 namespace tnrd {
 namespace {
+
+#ifndef TNRD_TC_BG
+#define TNRD_TC_BG 8
+#endif
+constexpr int kBG = TNRD_TC_BG;                 // build / gather warps (4 or 8: one or two per lane quarter)
+constexpr int kNBG = 32 * kBG;                  // build / gather threads
+#ifndef TNRD_TC_MMAW
+#define TNRD_TC_MMAW 0
+#endif
+#ifndef TNRD_TC_2MMA
+#define TNRD_TC_2MMA 1
+#endif
+constexpr bool kMmaWarp = TNRD_TC_MMAW;         // MMAs issued by the converged warp (elected lane)
+constexpr int kNMMA = TNRD_TC_2MMA ? 2 : 1;     // MMA issuer warps (2: forward and adjoint banks apart)
+constexpr int kTNT = (4 * kPG + kBG + kNMMA) * 32;  // phi warps, build / gather warps, MMA warp(s)
+static_assert(kBG == 4 || kBG == 8, "build / gather warps");
 
 template <int K, int NK>
 struct TcGeo {
@@ -47,85 +68,122 @@ struct TcGeo {
     static constexpr int KTP = tc_ktp(K), NZ = tc_nz(K);
     static constexpr int OW = kTcVW - 2 * R;   // output columns per tile
     static constexpr int UW = kTcVW + 2 * R;   // u tile columns
+    static constexpr int UP = (UW + 3 + 3) / 4 * 4;   // u tile pitch = TMA box width (16-byte start, <= 3 lead)
     static constexpr int PG = (NK % (2 * kPG) == 0) ? kPG : 2;  // phi groups used
     static constexpr int NFW = NK / PG;        // filters per phi warp
     static constexpr int NCH = KTP / 8;        // 8-column chunks of an im2col row
     static constexpr int NZC = NZ / 8;         // 8-column chunks of a Z row
     static constexpr int SLOT = 2 * (KTP > NK ? KTP : NK);   // A / W columns of a slot
+    static constexpr int DR = 8;               // d ring rows (>= K + 1 rows live per block)
     static_assert(NK % 8 == 0 && NK <= 64 && NFW % 2 == 0, "N_k: multiple of 8, at most 64");
     static_assert(kSlots * (SLOT + (NK > NZ ? NK : NZ)) <= kTmemCols, "TMEM column plan");
+    static_assert(K + 1 <= DR, "d ring");
 };
 
 __host__ __device__ constexpr int round4(int x) { return (x + 3) / 4 * 4; }
+__host__ __device__ constexpr int round32(int x) { return (x + 31) / 32 * 32; }
 
-// Shared memory: operand block, u tile, d [OH][OW], Z of one M-block [KT][128],
-// 4 x kSlots mbarriers + TMEM address.
+// Kernel parameter: the stage arguments plus the TMA map of u_in's rows
+// [avail_lo, avail_hi) as a (W, rows, B) tensor with a (UP, UH, 1) box.
+struct alignas(64) TcArgs {
+    CUtensorMap tm_u;
+    StageArgs a;
+    int use_tma;   // 0: u tiles by per-element loads (rows not 16-byte aligned / no driver entry point)
+    unsigned long long *prof;   // TNRD_TC_PROF builds: per CTA and warp {wait cycles, total cycles}
+};
+#ifdef TNRD_TC_PROF
+#define TCP_WAIT(bar, par) { const long long t0_ = clock64(); mbar_wait(bar, par); tcp_wait += clock64() - t0_; }
+#else
+#define TCP_WAIT(bar, par) mbar_wait(bar, par)
+#endif
+
+// Shared memory (floats): operand block | u tiles [2][UH][UP] (128-byte aligned, TMA
+// destinations) | d ring [DR][OW] | Z of one M-block [KT][kZP] | mbarriers
+// (4 x kSlots + 2) | TMEM address.
+template <int K, int NK>
+__host__ __device__ constexpr int tc_u_floats(int oh) {
+    using G = TcGeo<K, NK>;
+    return round32((oh + 4 * G::R) * G::UP);
+}
 template <int K, int NK>
 __host__ __device__ constexpr int tc_smem_floats(int oh, int par_floats) {
     using G = TcGeo<K, NK>;
-    return par_floats + round4((oh + 4 * G::R) * G::UW) + round4(oh * G::OW) + G::KT * kZP + 8 * kSlots + 4;
+    return round32(par_floats) + 2 * tc_u_floats<K, NK>(oh) + round4(G::DR * G::OW) + G::KT * kZP +
+           2 * (4 * kSlots + 2) + 4;
 }
 
 
-// One CTA = one output tile of OW x OH.  The v region (64 x (OH + 2r) pixels) is
-// cut into M-blocks of two rows (TMEM lane m = pixel (2i + m/64, m%64) of block i);
-// block i lives in TMEM slot i % 3 (A / W columns, then V / Z columns).  Warp roles,
-// handing blocks over through mbarriers (no CTA-wide barrier until the epilogue):
+// Persistent: one CTA per SM walks the tiles blockIdx.x, + gridDim.x, ... (58 x OH
+// outputs each; v region 64 x (OH + 2r)).  The stage operands are loaded and TMEM
+// is allocated once per CTA, and the M-blocks of consecutive tiles form one
+// pipeline (global block g = tile n * nmb + i, TMEM slot g % 3), so the next
+// tile's first blocks are built and multiplied while the current tile's last ones
+// are in phi and the gather: there is no fill / drain per tile.  TMEM lane m =
+// pixel (2i + m/64, m%64) of block i.  Warp roles, handing blocks over through
+// mbarriers (no CTA-wide barrier until the end):
 //   4 PG phi warps: warp w serves lane quarter w % 4, filters [NFW (w/4), +NFW):
-//               wait V(i), tcgen05.ld, phi, W (hi, lo) -> TMEM, arrive W_full(i)
-//   4 build / gather warps (lane quarter w % 4): im2col A(i) -> TMEM, arrive
-//               A_full(i); wait Z(i), Z -> smem, A(i+3) into the freed slot, then
-//               d += the block's taps (blocks in order: d summed in v-row order)
-//   last warp   lane 0 issues the 3xTF32 MMAs: F(i) on A_full(i) -> V_full(i),
-//               Adj(i) on W_full(i) -> Z_full(i), in the order F(0..2), Adj(0),
+//               wait V(g), tcgen05.ld, phi, W (hi, lo) -> TMEM, arrive W_full(g)
+//   4 build / gather warps (lane quarter w % 4): im2col A(g) -> TMEM, arrive
+//               A_full(g); wait Z(g), Z -> smem, A(g+3) into the freed slot, then
+//               d += the block's taps (blocks in order: d summed in v-row order),
+//               then the epilogue of the two output rows the block completed
+//               (u - d, reaction, store).  u tiles are double buffered: tile n+1's
+//               is requested by TMA when tile n starts and waited for (plus the
+//               mirror fix-up of edge tiles) before its first im2col row.
+//   last warp   lane 0 issues the 3xTF32 MMAs: F(g) on A_full(g) -> V_full(g),
+//               Adj(g) on W_full(g) -> Z_full(g), in the order F(0..2), Adj(0),
 //               F(3), Adj(1), F(4), ...
 template <int K, int NK, bool TABLE, bool R2, bool RN>
-__global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant__ StageArgs a) {
+__global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant__ TcArgs p) {
     using G = TcGeo<K, NK>;
-    constexpr int R = G::R, KT = G::KT, KTP = G::KTP, NZ = G::NZ, OW = G::OW, UW = G::UW, NFW = G::NFW;
-    constexpr int NCH = G::NCH, NZC = G::NZC, SLOT = G::SLOT, PG = G::PG;
-    constexpr int WBG = 4 * kPG, WMMA = WBG + 4;   // first build / gather warp, MMA warp
+    constexpr int R = G::R, KT = G::KT, KTP = G::KTP, NZ = G::NZ, OW = G::OW, UW = G::UW, UP = G::UP;
+    constexpr int NFW = G::NFW, NCH = G::NCH, NZC = G::NZC, SLOT = G::SLOT, PG = G::PG, DR = G::DR;
+    constexpr int WBG = 4 * kPG, WMMA = WBG + kBG;   // first build / gather warp, MMA warp
     constexpr int VZ0 = kSlots * SLOT, VZW = NK > NZ ? NK : NZ;  // V / Z columns of slot s at VZ0 + VZW s
     constexpr int BAR_BG = 1;
+    const StageArgs &a = p.a;
     extern __shared__ __align__(1024) float4 smem4[];
     float *s_par = reinterpret_cast<float *>(smem4);
     const float *s_bf = s_par;                       // hi [NK x KTP], lo after it
     const float *s_ba = s_par + 2 * NK * KTP;        // hi [NZ x NK], lo after it
     const float *s_pp = s_ba + 2 * NZ * NK;          // [NK/2][pps] filter-pair phi
     const int OH = a.tc_oh, VH = OH + 2 * R, UH = OH + 4 * R;
-    float *s_u = s_par + a.tc_par_floats;
-    float *s_d = s_u + round4(UH * UW);              // [OH][OW]
-    float *s_z = s_d + round4(OH * OW);              // [KT][kZP]
+    const int UF = tc_u_floats<K, NK>(OH);
+    float *s_u0 = s_par + round32(a.tc_par_floats);  // u tile of local tile n: s_u0 + (n & 1) UF
+    float *s_d = s_u0 + 2 * UF;                      // ring: output row y at (y % DR) OW
+    float *s_z = s_d + round4(DR * OW);              // [KT][kZP]
     uint64_t *bar_a = reinterpret_cast<uint64_t *>(s_z + KT * kZP);   // A_full[kSlots]
     uint64_t *bar_v = bar_a + kSlots, *bar_w = bar_v + kSlots, *bar_z = bar_w + kSlots;
-    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(bar_z + kSlots);
+    uint64_t *bar_u = bar_z + kSlots;                // u tile landed [2]
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(bar_u + 2);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int quarter = warp & 3, m = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const int H = a.H, W = a.W;
-
-    // ---- tile
+    const int nmb = VH / 2;
+    const int ntl = (a.n_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // tiles of this CTA
+    const int nblk = ntl * nmb;                      // M-blocks of this CTA
     const int per_img = a.tiles_x * a.tiles_y;
-    const int b = blockIdx.x / per_img;
-    const int rem = blockIdx.x - b * per_img;
-    const int ty = rem / a.tiles_x;
-    const int x0 = (rem - ty * a.tiles_x) * OW;
-    const int y0 = a.y_begin + ty * OH;
+    struct Tile { int b, x0, y0; };
+    const auto tile_of = [&](int n) {                // local tile n
+        const int t = (int)blockIdx.x + n * (int)gridDim.x;
+        Tile T;
+        T.b = t / per_img;
+        const int rem = t - T.b * per_img;
+        const int ty = rem / a.tiles_x;
+        T.x0 = (rem - ty * a.tiles_x) * OW;
+        T.y0 = a.y_begin + ty * OH;
+        return T;
+    };
+    // tile column x0 - 2r + c lives at s_u[r UP + c + lead]: TMA boxes start 16-byte aligned
+    const auto lead_of = [](int x0) { const int gx = x0 - 2 * R; return gx - (gx >= 0 ? (gx & ~3) : -((-gx + 3) & ~3)); };
 
-    // ---- stage operands -> smem, u tile (+2r, mirrored), d = 0
+    // ---- stage operands -> smem, d ring = 0, TMEM, barriers
     {
         const float4 *src = reinterpret_cast<const float4 *>(a.params);
-        for (int j = tid; j < a.tc_par_floats / 4; j += kNT) smem4[j] = __ldg(src + j);
-        const float *ub = a.u_in.ptr + (long long)b * a.u_in.img_stride;
-        for (int j = tid; j < UH * UW; j += kNT) {
-            const int r = j / UW, c = j - r * UW;
-            int gy = reflect(y0 - 2 * R + r, H);
-            gy = min(max(gy, a.avail_lo), a.avail_hi - 1);
-            const int gx = reflect(x0 - 2 * R + c, W);
-            s_u[j] = __ldg(ub + (long long)(gy - a.u_in.row_base) * a.u_in.ld + gx);
-        }
-        for (int j = tid; j < OH * OW; j += kNT) s_d[j] = 0.0f;
+        for (int j = tid; j < a.tc_par_floats / 4; j += kTNT) smem4[j] = __ldg(src + j);
+        for (int j = tid; j < DR * OW; j += kTNT) s_d[j] = 0.0f;
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
@@ -134,11 +192,13 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
     }
     if (tid == 0) {
         for (int s = 0; s < kSlots; ++s) {
-            mbar_init(bar_a + s, 128);
+            mbar_init(bar_a + s, kBG);          // one arrival per warp (lane 0 after __syncwarp)
             mbar_init(bar_v + s, 1);
-            mbar_init(bar_w + s, 128 * PG);
+            mbar_init(bar_w + s, 4 * PG);
             mbar_init(bar_z + s, 1);
         }
+        mbar_init(bar_u, 1);
+        mbar_init(bar_u + 1, 1);
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // operands visible to the MMA (async proxy)
@@ -147,15 +207,20 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
     tc_fence_after();
     const uint32_t tmem = *s_tmem;
     const uint32_t tl = tmem + lane_off;
-    const int nmb = VH / 2;
+#ifdef TNRD_TC_PROF
+    long long tcp_wait = 0;
+    const long long tcp_t0 = clock64();
+#endif
 
     if (warp < 4 * PG) {
         // ======================= phi warps
         const int h = warp >> 2;
         const int pps = a.pstride;
-        for (int i = 0; i < nmb; ++i) {
-            const int s = i % kSlots;
-            mbar_wait(bar_v + s, (i / kSlots) & 1);
+        int tn = 0, ti = 0;            // tile / block of g (R2's out-of-image test)
+        Tile tT = tile_of(0);
+        for (int g = 0; g < nblk; ++g) {
+            const int s = g % kSlots;
+            TCP_WAIT(bar_v + s, (g / kSlots) & 1);
             tc_fence_after();
             uint32_t vr[NFW];
             tmem_ld_nowait<NFW>(tl + VZ0 + VZW * s + h * NFW, vr);
@@ -189,8 +254,12 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
 #endif
             // R2 (exact K^T): w is zero outside the image (the gather adds the mirror
             // images instead); R1 keeps the mirrored w of out-of-image pixels
-            const int gyp = y0 - R + 2 * i + (m >> 6), gxp = x0 - R + (m & 63);
-            const bool zero_w = R2 && ((unsigned)gyp >= (unsigned)H || (unsigned)gxp >= (unsigned)W);
+            bool zero_w = false;
+            if constexpr (R2) {
+                const int gyp = tT.y0 - R + 2 * ti + (m >> 6), gxp = tT.x0 - R + (m & 63);
+                zero_w = (unsigned)gyp >= (unsigned)H || (unsigned)gxp >= (unsigned)W;
+                if (++ti == nmb) { ti = 0; if (++tn < ntl) tT = tile_of(tn); }
+            }
             uint32_t wh[NFW], wl[NFW];
 #pragma unroll
             for (int e = 0; e < NFW; ++e) {
@@ -203,29 +272,85 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
             tmem_st<NFW>(tl + SLOT * s + NK + h * NFW, wl);
             tc_wait_st();
             tc_fence_before();
-            mbar_arrive(bar_w + s);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_w + s);
         }
     } else if (warp < WBG) {
-        // phi warps of an unused group (N_k not divisible): idle until the epilogue
+        // phi warps of an unused group (N_k not divisible): idle until the end
     } else if (warp < WMMA) {
         // ======================= build / gather warps
-        const auto build = [&](int i) {
-            // im2col row (hi, lo) of pixel m of block i: v-region (j, c) uses its mirror
+        const int gt = tid - 32 * WBG;  // 0 .. kNBG - 1
+        const int half = kBG == 8 ? gt >> 7 : 0;   // which of a lane quarter's BG warps
+        // u tile of local tile n -> s_u0 + (n & 1) UF: rows y0 - 2r .., columns x0 - 2r ..
+        // at [r][c + lead]; element (r, c) = u(clamp(mirror(y0 - 2r + r)), mirror(x0 - 2r + c))
+        const auto request_u = [&](int n) {       // TMA of the box (one thread)
+            if (!p.use_tma || gt != 0) return;
+            const Tile T = tile_of(n);
+            const int gx = T.x0 - 2 * R;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the buffer
+            mbar_expect_tx(bar_u + (n & 1), (uint32_t)(UH * UP * 4));
+            tma_load_3d(s_u0 + (n & 1) * UF, &p.tm_u, gx - lead_of(T.x0), T.y0 - 2 * R - a.avail_lo, T.b,
+                        bar_u + (n & 1));
+        };
+        const auto ensure_u = [&](int n) {        // all BG threads: tile n's u is complete in smem
+            const Tile T = tile_of(n);
+            float *su = s_u0 + (n & 1) * UF + lead_of(T.x0);
+            const float *ub = a.u_in.ptr + (long long)T.b * a.u_in.img_stride;
+            const int gy0 = T.y0 - 2 * R, gx0 = T.x0 - 2 * R;
+            const auto load = [&](int r, int c) {
+                int gy = reflect(gy0 + r, H);
+                gy = min(max(gy, a.avail_lo), a.avail_hi - 1);
+                const int gx = reflect(gx0 + c, W);
+                su[r * UP + c] = __ldg(ub + (long long)(gy - a.u_in.row_base) * a.u_in.ld + gx);
+            };
+            if (p.use_tma) {
+                mbar_wait(bar_u + (n & 1), (n >> 1) & 1);
+                // mirror fix-up (TMA zero-filled what lies outside rows [avail_lo, avail_hi)
+                // or columns [0, W)): rows [0, rA) and [rB, UH) whole, the others' columns
+                // [0, cA) and [cB, UW)
+                const int rA = min(max(a.avail_lo - gy0, 0), UH), rB = max(min(a.avail_hi - gy0, UH), rA);
+                const int cA = min(max(-gx0, 0), UW), cB = max(min(W - gx0, UW), cA);
+                const int nrow = rA + UH - rB, ncol = cA + UW - cB;
+                for (int j = gt; j < nrow * UW; j += kNBG) {
+                    const int q = j / UW, c = j - q * UW;
+                    load(q < rA ? q : rB + (q - rA), c);
+                }
+                for (int j = gt; j < (rB - rA) * ncol; j += kNBG) {
+                    const int q = j / ncol, c = j - q * ncol;
+                    load(rA + q, c < cA ? c : cB + (c - cA));
+                }
+            } else {
+                for (int j = gt; j < UH * UW; j += kNBG) {
+                    const int r = j / UW;
+                    load(r, j - r * UW);
+                }
+            }
+            named_sync(BAR_BG, kNBG);
+        };
+        int bn = 0, bi = 0;            // tile / block of the next build (builds run in g order)
+        Tile bT = tile_of(0);
+        const auto build = [&](int g) {
+            // im2col row (hi, lo) of pixel m of block g: v-region (j, c) uses its mirror
             // in the image (R1), clamped into the tile for pixels no output needs
-            const int s = i % kSlots;
+            const int s = g % kSlots;
+            const int n = bn, i = bi;
+            if (i == 0) ensure_u(n);
+            const Tile T = bT;
+            if (++bi == nmb) { bi = 0; if (++bn < ntl) bT = tile_of(bn); }
             const int j = 2 * i + (m >> 6), c = m & 63;
-            const int gy = reflect(y0 - R + j, H), gx = reflect(x0 - R + c, W);
-            const int pj = min(max(gy - y0 + R, 0), VH - 1);
-            const int pc = min(max(gx - x0 + R, 0), kTcVW - 1);
-            const float *up = s_u + (pj + 2 * R) * UW + pc + 2 * R;  // tap (ta, tb) reads up[-ta*UW - tb]
+            const int gy = reflect(T.y0 - R + j, H), gx = reflect(T.x0 - R + c, W);
+            const int pj = min(max(gy - T.y0 + R, 0), VH - 1);
+            const int pc = min(max(gx - T.x0 + R, 0), kTcVW - 1);
+            const float *up = s_u0 + (n & 1) * UF + lead_of(T.x0) + (pj + 2 * R) * UP + pc + 2 * R;  // tap (ta, tb) reads up[-ta*UP - tb]
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch) {
+                if (kBG == 8 && (ch < (NCH + 1) / 2) != (half == 0)) continue;   // chunks split by half
                 uint32_t hv[8], lv[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     const int t = ch * 8 + e;
                     float x = 0.0f;
-                    if (t < KT) x = up[-(t / K) * UW - (t % K)];
+                    if (t < KT) x = up[-(t / K) * UP - (t % K)];
                     const float xh = tf32_hi_t<RN>(x);
                     hv[e] = __float_as_uint(xh);
                     lv[e] = __float_as_uint(x - xh);
@@ -235,19 +360,30 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
             }
             tc_wait_st();
             tc_fence_before();
-            mbar_arrive(bar_a + s);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_a + s);
         };
-        for (int i = 0; i < kSlots && i < nmb; ++i) build(i);
-        const int gt = tid - 32 * WBG;  // 0..127
-        const bool r2_edge = R2 && (y0 - R < 0 || y0 + OH + R > H || x0 - R < 0 || x0 + OW + R > W);
-        for (int i = 0; i < nmb; ++i) {
-            const int s = i % kSlots;
-            mbar_wait(bar_z + s, (i / kSlots) & 1);
+        if (nblk > 0) request_u(0);
+        for (int g = 0; g < kSlots && g < nblk; ++g) build(g);
+        const int x = gt & 63;
+        int n = 0, i = 0;              // tile / block of g
+        Tile T = tile_of(0);
+        for (int g = 0; g < nblk; ++g) {
+            const int s = g % kSlots;
+            // the epilogue pixel of this block (threads gt < 128: output row 2i - (K-1) +
+            // gt/64, column x): its f is fetched now, used after the gather
+            const int ye = gt < 128 ? 2 * i - (K - 1) + (gt >> 6) : -1, oye = T.y0 + ye, oxe = T.x0 + x;
+            const bool epi = ye >= 0 && x < OW && oye < a.y_end && oxe < W;
+            float fv = 0.0f;
+            if (epi) fv = __ldg(a.f.ptr + (long long)T.b * a.f.img_stride + (long long)(oye - a.f.row_base) * a.f.ld + oxe);
+            TCP_WAIT(bar_z + s, (g / kSlots) & 1);
             tc_fence_after();
-            named_sync(BAR_BG, 128);  // every BG thread is done with gather(i - 1)
+            named_sync(BAR_BG, kNBG);  // every BG thread is done with gather(g - 1) and its epilogue
+            if (i == 0 && n + 1 < ntl) request_u(n + 1);   // its buffer's last reader was tile n - 1
 #pragma unroll
             for (int ch = 0; ch < NZC; ++ch) {
                 if (ch * 8 >= KT) continue;
+                if (kBG == 8 && (ch < ((KT + 7) / 8 + 1) / 2) != (half == 0)) continue;
                 uint32_t z[8];
                 tmem_ld_nowait<8>(tl + VZ0 + VZW * s + ch * 8, z);
                 tmem_wait_ld(z);
@@ -256,15 +392,19 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
                     if (ch * 8 + e < KT) s_z[(ch * 8 + e) * kZP + m] = __uint_as_float(z[e]);
             }
             tc_fence_before();
-            if (i + kSlots < nmb) build(i + kSlots);  // slot s is free: W(i) consumed, Z(i) read
-            named_sync(BAR_BG, 128);
-            // d(y, x) += sum_b Z[(y + a, x + b)][a K + b] over rows 2i, 2i + 1 (v row y + a)
-            const int j0 = 2 * i, x = gt & 63;
+            if (g + kSlots < nblk) build(g + kSlots);  // slot s is free: W(g) consumed, Z(g) read
+            named_sync(BAR_BG, kNBG);
+            // d(y, x) += sum_b Z[(y + a, x + b)][a K + b] over rows 2i, 2i + 1 (v row y + a):
+            // thread gt takes column x and the rows r = gt/64 (mod kNBG/64) of the block's
+            // K + 1; the epilogue rows (r = 0, 1) are last written by their epilogue thread
+            const int j0 = 2 * i;
+            const bool r2_edge = R2 && (T.y0 - R < 0 || T.y0 + OH + R > H || T.x0 - R < 0 || T.x0 + OW + R > W);
             if (!R2 || !r2_edge) {
-                for (int r = gt >> 6; r < K + 1; r += 2) {  // output rows j0 - (K-1) .. j0 + 1
+                for (int r = gt >> 6; r < K + 1; r += kNBG / 64) {  // output rows j0 - (K-1) .. j0 + 1
                     const int y = j0 - (K - 1) + r;
                     if (x >= OW || y < 0 || y >= OH) continue;
-                    float d = s_d[y * OW + x];
+                    float *dp = s_d + (y % DR) * OW + x;
+                    float d = *dp;
 #pragma unroll
                     for (int jj = 0; jj < 2; ++jj) {
                         const int ta = j0 + jj - y;
@@ -275,7 +415,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
                         for (int tb = 0; tb < K; ++tb) S += zp[tb * kZP + tb];
                         d += S;
                     }
-                    s_d[y * OW + x] = d;
+                    *dp = d;
                 }
             } else if constexpr (R2) {
                 // R2 tile at an image edge: d(q) = sum_t sum_{x in M(q)} Z[x + a_t][t] over
@@ -293,14 +433,15 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
                     }
                     return S;
                 };
-                for (int r = gt >> 6; r < K + 1; r += 2) {
+                for (int r = gt >> 6; r < K + 1; r += kNBG / 64) {
                     const int y = j0 - (K - 1) + r;
                     if (x >= OW || y < 0 || y >= OH) continue;
-                    const int gy = y0 + y, gx = x0 + x;
+                    const int gy = T.y0 + y, gx = T.x0 + x;
                     const int gym = gy < R ? -1 - gy : (gy >= H - R ? 2 * H - 1 - gy : INT_MIN);
                     const int gxm = gx < R ? -1 - gx : (gx >= W - R ? 2 * W - 1 - gx : INT_MIN);
-                    const int xm = gxm == INT_MIN ? 0 : gxm - x0;  // source col of tap b: xm + b
-                    float d = s_d[y * OW + x];
+                    const int xm = gxm == INT_MIN ? 0 : gxm - T.x0;  // source col of tap b: xm + b
+                    float *dp = s_d + (y % DR) * OW + x;
+                    float d = *dp;
 #pragma unroll
                     for (int jj = 0; jj < 2; ++jj) {
                         const int ta = j0 + jj - y;
@@ -309,18 +450,36 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
                             if (gxm != INT_MIN) d += S_cols(jj, ta, xm);
                         }
                         if (gym != INT_MIN) {
-                            const int ta2 = (y0 - R + j0 + jj) - gym + R;
+                            const int ta2 = (T.y0 - R + j0 + jj) - gym + R;
                             if (ta2 >= 0 && ta2 < K) {
                                 d += S_cols(jj, ta2, x);
                                 if (gxm != INT_MIN) d += S_cols(jj, ta2, xm);
                             }
                         }
                     }
-                    s_d[y * OW + x] = d;
+                    *dp = d;
                 }
             }
+            // epilogue: output row ye is complete (its last v row, ye + K - 1, is in this
+            // block): ut = u - d, u+ = reaction(ut); the ring row is cleared for reuse
+            if (ye >= 0 && x < OW) {
+                float *dp = s_d + (ye % DR) * OW + x;
+#ifdef TNRD_EXP_NOEPI
+                if (epi && fv == -1.0f) {
+#else
+                if (epi) {
+#endif
+                    const float u = s_u0[(n & 1) * UF + lead_of(T.x0) + (ye + 2 * R) * UP + x + 2 * R];
+                    const float ut = u - *dp;
+                    const long long oi = (long long)T.b * a.out_img_stride + (long long)(oye - a.out_row_base) * a.out_ld + oxe;
+                    a.u_out[oi] = reaction_step(a.reaction, u, ut, a.lambda, fv);
+                    if (a.ut_out) a.ut_out[oi] = ut;
+                }
+                *dp = 0.0f;
+            }
+            if (++i == nmb) { i = 0; if (++n < ntl) T = tile_of(n); }
         }
-    } else if (TABLE || lane == 0) {
+    } else if (TABLE || kMmaWarp || lane == 0) {
         // ======================= MMA issuer: one thread with the exact phi; the
         // converged warp with an elected lane for the tabulated phi, whose shorter phi
         // puts the MMA chain on the critical path
@@ -330,12 +489,11 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
         constexpr uint32_t id_f = idesc_tf32(NK), id_a = idesc_tf32(NZ);
         const uint64_t df_hi = umma_desc(bf_hi, SBO_F), df_lo = umma_desc(bf_lo, SBO_F);
         const uint64_t da_hi = umma_desc(ba_hi, SBO_A), da_lo = umma_desc(ba_lo, SBO_A);
-        const auto fwd = [&](int i) {  // V = A_lo B_hi + A_hi B_lo + A_hi B_hi
-            const int s = i % kSlots;
-            mbar_wait(bar_a + s, (i / kSlots) & 1);
+        const auto fwd = [&](int g) {  // V = A_lo B_hi + A_hi B_lo + A_hi B_hi (A_full(g) seen)
+            const int s = g % kSlots;
             tc_fence_after();
             const uint32_t tA = tmem + SLOT * s, tV = tmem + VZ0 + VZW * s;
-            if constexpr (TABLE) {
+            if constexpr (TABLE || kMmaWarp) {
 #pragma unroll
                 for (int k = 0; k < KTP / 8; ++k) {   // K-chunk k: descriptor + 16 k (256 B)
                     mma_tf32_warp(tV, tA + KTP + 8 * k, df_hi + 16 * k, id_f, k > 0);
@@ -353,13 +511,11 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
                 mma_commit(bar_v + s);
             }
         };
-        for (int i = 0; i < kSlots && i < nmb; ++i) fwd(i);
-        for (int i = 0; i < nmb; ++i) {  // Z = W_lo B_hi + W_hi B_lo + W_hi B_hi
-            const int s = i % kSlots;
-            mbar_wait(bar_w + s, (i / kSlots) & 1);
+        const auto adj = [&](int g) {  // Z = W_lo B_hi + W_hi B_lo + W_hi B_hi (W_full(g) seen)
+            const int s = g % kSlots;
             tc_fence_after();
             const uint32_t tW = tmem + SLOT * s, tZ = tmem + VZ0 + VZW * s;
-            if constexpr (TABLE) {
+            if constexpr (TABLE || kMmaWarp) {
 #pragma unroll
                 for (int k = 0; k < NK / 8; ++k) {
                     mma_tf32_warp(tZ, tW + NK + 8 * k, da_hi + 16 * k, id_a, k > 0);
@@ -376,30 +532,76 @@ __global__ void __launch_bounds__(kNT, 1) tc_stage_kernel(const __grid_constant_
                 }
                 mma_commit(bar_z + s);
             }
-            if (i + kSlots < nmb) fwd(i + kSlots);
+        };
+        // Issue F(g) once A_full(g) and Adj(g) once W_full(g) complete, whichever comes
+        // first (F(g) also needs slot g % 3 free: A(g) is built only after Z(g - 3) was
+        // read, which needed Adj(g - 3)).  Polling both keeps a late im2col block from
+        // holding up the adjoint of a block whose w is ready, and vice versa.
+        if constexpr (kNMMA == 2) {
+            // two issuers (warps on different SM sub-partitions): F(g) after A_full(g),
+            // Adj(g) after W_full(g); each commit tracks its own thread's MMAs
+            if (warp == WMMA) {
+                for (int g = 0; g < nblk; ++g) { mbar_wait(bar_a + g % kSlots, (g / kSlots) & 1); fwd(g); }
+            } else {
+                for (int g = 0; g < nblk; ++g) { mbar_wait(bar_w + g % kSlots, (g / kSlots) & 1); adj(g); }
+            }
+        } else {
+            int gf = 0, ga = 0;
+            while (ga < nblk) {
+                bool did = false;
+                if (gf < nblk && gf < ga + kSlots && mbar_test(bar_a + gf % kSlots, (gf / kSlots) & 1, TABLE || kMmaWarp)) {
+                    fwd(gf++);
+                    did = true;
+                }
+                if (ga < gf && mbar_test(bar_w + ga % kSlots, (ga / kSlots) & 1, TABLE || kMmaWarp)) {
+                    adj(ga++);
+                    did = true;
+                }
+                if (!did) __nanosleep(32);
+            }
         }
     }
-    __syncthreads();
-
-    // ---- epilogue: ut = u - d, u+ = reaction(ut)
-    {
-        const float *fb = a.f.ptr + (long long)b * a.f.img_stride;
-        float *ob = a.u_out + (long long)b * a.out_img_stride;
-        for (int it = tid; it < OH * OW; it += kNT) {
-            const int y = it / OW, x = it - y * OW;
-            const int oy = y0 + y, ox = x0 + x;
-            if (oy >= a.y_end || ox >= W) continue;
-            const float u = s_u[(y + 2 * R) * UW + x + 2 * R];
-            const float ut = u - s_d[it];
-            const float fv = __ldg(fb + (long long)(oy - a.f.row_base) * a.f.ld + ox);
-            const long long oi = (long long)(oy - a.out_row_base) * a.out_ld + ox;
-            ob[oi] = reaction_step(a.reaction, u, ut, a.lambda, fv);
-            if (a.ut_out) a.ut_out[(long long)b * a.out_img_stride + oi] = ut;
-        }
+#ifdef TNRD_TC_PROF
+    if (lane == 0 && p.prof) {
+        p.prof[(blockIdx.x * 32 + warp) * 2] = tcp_wait;
+        p.prof[(blockIdx.x * 32 + warp) * 2 + 1] = clock64() - tcp_t0;
     }
+#endif
     tc_fence_before();
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+}
+
+// u_in rows [avail_lo, avail_hi) as a (W, rows, B) tensor map with a (UP, UH, 1) box
+template <int K, int NK>
+bool encode_u_tiles(CUtensorMap *tm, const StageArgs &a, int B) {
+    using G = TcGeo<K, NK>;
+    EncodeTiled enc = encoder();
+    const int rows = a.avail_hi - a.avail_lo, UH = a.tc_oh + 4 * G::R;
+    if (!enc || rows < 1 || UH > 256) return false;
+    const float *base = a.u_in.ptr + (long long)(a.avail_lo - a.u_in.row_base) * a.u_in.ld;
+    const long long s2 = B > 1 ? a.u_in.img_stride : (long long)rows * a.u_in.ld;
+    if (!aligned16(base) || a.u_in.ld % 4 != 0 || s2 % 4 != 0) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)a.W, (cuuint64_t)rows, (cuuint64_t)B};
+    cuuint64_t strides[2] = {(cuuint64_t)a.u_in.ld * 4, (cuuint64_t)s2 * 4};
+    cuuint32_t boxd[3] = {(cuuint32_t)G::UP, (cuuint32_t)UH, 1}, es[3] = {1, 1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(base), dims, strides, boxd, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct DevInfo { int optin = 0, sms = 0; };
+DevInfo dev_info() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static DevInfo cache[64];  // per device, filled on first use
+    DevInfo d = dev < 64 ? cache[dev] : DevInfo{};
+    if (d.sms == 0) {
+        cudaDeviceGetAttribute(&d.optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+        if (dev < 64) cache[dev] = d;
+    }
+    return d;
 }
 
 template <int K, int NK>
@@ -414,16 +616,11 @@ cudaError_t launch_tc(StageArgs &a, int B, cudaStream_t s) {
                                 : (a.mode == MODE_TABLE ? tc_stage_kernel<K, NK, true, false, false>
                                                         : tc_stage_kernel<K, NK, false, false, false>);
     if (a.tc_oh <= 0 || a.tc_oh % 2 != 0) return cudaErrorInvalidValue;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    static int optin_cache[64] = {0};  // per device, filled on first use
-    int optin = dev < 64 ? optin_cache[dev] : 0;
-    if (optin == 0) {
-        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        if (dev < 64) optin_cache[dev] = optin;
-    }
+    // the u tile of tile n + 1 is requested when tile n starts: a tile needs >= 4 M-blocks
+    a.tc_oh = std::max(a.tc_oh, 8 - 2 * G::R);
+    const DevInfo di = dev_info();
     size_t smem = sizeof(float) * (size_t)tc_smem_floats<K, NK>(a.tc_oh, a.tc_par_floats);
-    while (smem > (size_t)optin && a.tc_oh > 8) {  // fewer rows per tile until it fits
+    while (smem > (size_t)di.optin && a.tc_oh > 8) {  // fewer rows per tile until it fits
         a.tc_oh -= 8;
         smem = sizeof(float) * (size_t)tc_smem_floats<K, NK>(a.tc_oh, a.tc_par_floats);
     }
@@ -432,10 +629,36 @@ cudaError_t launch_tc(StageArgs &a, int B, cudaStream_t s) {
     a.tiles_x = (a.W + G::OW - 1) / G::OW;
     a.tiles_y = (a.y_end - a.y_begin + a.tc_oh - 1) / a.tc_oh;
     const long long n = (long long)B * a.tiles_x * a.tiles_y;
-    if (n > INT_MAX) return cudaErrorInvalidValue;
+    if (n > INT_MAX / 128) return cudaErrorInvalidValue;
     a.n_tiles = (int)n;
-    if (n > 0) kern<<<(unsigned)n, kNT, smem, s>>>(a);
+    if (n == 0) return cudaSuccess;
+    TcArgs p;   // kernel parameter (copied at launch)
+    std::memset(&p, 0, sizeof p);
+    p.a = a;
+    p.use_tma = encode_u_tiles<K, NK>(&p.tm_u, a, B) ? 1 : 0;
+    const int grid = (int)std::min<long long>(n, di.sms > 0 ? di.sms : 148);
+#ifdef TNRD_TC_PROF
+    // per warp: mean wait fraction over the CTAs (stderr), one line per launch
+    static unsigned long long *prof = nullptr;
+    if (!prof) cudaMalloc(&prof, sizeof(unsigned long long) * 64 * 1024);
+    cudaMemsetAsync(prof, 0, sizeof(unsigned long long) * 64 * 1024, s);
+    p.prof = prof;
+    kern<<<grid, kTNT, smem, s>>>(p);
+    std::vector<unsigned long long> hp(64 * (size_t)grid);
+    cudaMemcpyAsync(hp.data(), prof, sizeof(unsigned long long) * hp.size(), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "TCPROF wait%% per warp:");
+    for (int w = 0; w < kTNT / 32; ++w) {
+        double wt = 0, tt = 0;
+        for (int c = 0; c < grid; ++c) { wt += (double)hp[(c * 32 + w) * 2]; tt += (double)hp[(c * 32 + w) * 2 + 1]; }
+        fprintf(stderr, " %.1f", tt > 0 ? 100.0 * wt / tt : 0.0);
+    }
+    fprintf(stderr, "\n");
     return cudaGetLastError();
+#else
+    kern<<<grid, kTNT, smem, s>>>(p);
+    return cudaGetLastError();
+#endif
 }
 
 

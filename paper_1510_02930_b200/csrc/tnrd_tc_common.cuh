@@ -1,10 +1,12 @@
-// tcgen05 / TMEM / mbarrier helpers and the packed-pair phi shared by the tensor-core
-// stage kernels (tnrd_tc.cu: per-tile engine and its gradient banks; tnrd_stream.cu:
-// the persistent streaming engine).  Internal, header-only.
+// tcgen05 / TMEM / mbarrier / TMA helpers and the packed-pair phi shared by the
+// tensor-core kernels (tnrd_tc.cu: the persistent stage kernel and the gradient's
+// banks).  Internal, header-only.
 #pragma once
 
 #include "tnrd_internal.h"
 #include "tnrd_device.cuh"
+
+#include <cuda.h>
 
 #include <climits>
 #include <stdint.h>
@@ -84,6 +86,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
                      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
                      : "memory");
     }
+}
+// non-blocking test of an mbarrier phase; warp-uniform (lane 0's result) when `warp`
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity, bool warp) {
+    uint32_t done;
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done)
+                 : "r"(smem_u32(bar)), "r"(parity)
+                 : "memory");
+    if (warp) done = __shfl_sync(0xffffffffu, done, 0);
+    return done != 0;
 }
 // floor / ceil of |x| < 2^22 as an int without the XU pipe (F2I): a directed-
 // rounding add of 1.5 * 2^23 leaves the integer in the low mantissa bits
@@ -228,6 +241,41 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+
+// ---- TMA (cp.async.bulk.tensor): tensor maps are encoded on the host through the
+// driver entry point (no -lcuda link), passed as __grid_constant__ kernel parameters.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// box at (x, y, z) of a 3-D tensor map -> shared memory, completion on `bar`;
+// out-of-range elements are zero filled (they still count toward the bytes)
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm, int x, int y, int z, uint64_t *bar) {
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+                 "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+                 "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeTiled encoder() {
+    static EncodeTiled fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiled>(f);
+        cudaGetLastError();
+    }
+    return fn;
+}
+
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 }  // namespace
 }  // namespace tnrd

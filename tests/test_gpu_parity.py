@@ -566,38 +566,6 @@ def test_host_entry_point_pipelined_chunks_bitwise(torch_cuda, P):
     assert np.array_equal(u_pin.numpy(), u_dev)
 
 
-# ------------------------------------------------------------------ streaming engine (opt-in experiment)
-@pytest.fixture()
-def stream_engine():
-    """TNRD_STREAM=1: the persistent TMA / tcgen05.cp streaming kernel."""
-    old = os.environ.get("TNRD_STREAM")
-    os.environ["TNRD_STREAM"] = "1"
-    yield
-    if old is None:
-        del os.environ["TNRD_STREAM"]
-    else:
-        os.environ["TNRD_STREAM"] = old
-
-
-@pytest.mark.parametrize("bc", [0, 1])
-@pytest.mark.parametrize("shape", [(1, 30, 40), (2, 64, 128), (1, 200, 300), (3, 7, 64)])
-def test_streaming_engine_parity(torch_cuda, P, stream_engine, shape, bc):
-    rng = np.random.default_rng(sum(shape) + bc)
-    f = rng.poisson(rng.uniform(0, 4, shape)).astype(np.float32)
-    model = make_model(rng, 2, 48, 7, 63, float(max(f.max(), 1.0)))
-    u = _gpu_denoise(P, torch_cuda, model, f, boundary=bc)
-    for b in range(shape[0]):
-        _assert_parity(u[b], oracle.denoise(f[b], model, boundary=bc), 4.0, what=f"stream {shape} bc{bc} b{b}")
-
-
-def test_streaming_engine_c3_table_and_slabs(torch_cuda, P, stream_engine):
-    torch = torch_cuda
-    p = make_problem(3)
-    u_ref = oracle.denoise(p.f[0], p.model)
-    u = _gpu_denoise(P, torch, p.model, p.f, peak=p.peaks)[0]
-    _assert_parity(u, u_ref, float(p.peaks[0]), p.clean[0], "stream C3")
-    ut = _gpu_denoise(P, torch, p.model, p.f, peak=p.peaks, phi_mode=P.PHI_TABLE)[0]
-    _assert_parity(ut, u_ref, float(p.peaks[0]), p.clean[0], "stream C3 table")
     eng = P.TNRD(p.model)
     f = torch.from_numpy(p.f[0]).cuda()
     full = eng.denoise(f)
