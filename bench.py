@@ -309,6 +309,11 @@ def main():
                     help="stage engine (tnrd_set_engine): auto = tensor cores where they apply")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--launch-events", default="after", choices=["after", "inline"],
+                    help="per-launch CUDA events: 'after' = on up to 3 profiled steps right after the timed "
+                         "region (default: an event between two stage kernels would serialise the "
+                         "programmatic dependent launch that overlaps one stage's set-up with the previous "
+                         "stage's tail), 'inline' = around every launch inside the timed region")
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU only: the multi-rank plumbing (launch, shards, barriers, max over ranks) "
                          "over gloo without any GPU work")
@@ -378,7 +383,7 @@ def main():
         step()
     barrier()
     n_launch0 = P.tnrd_launch_count(eng.h)
-    P.tnrd_set_profiling(eng.h, True)
+    P.tnrd_set_profiling(eng.h, args.launch_events == "inline")
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
@@ -391,6 +396,13 @@ def main():
     launches = P.tnrd_launch_count(eng.h) - n_launch0
     launch_ms = P.tnrd_get_launch_times(eng.h)
     P.tnrd_set_profiling(eng.h, False)
+    if args.launch_events == "after":   # per-launch times from profiled steps right after the timed region
+        P.tnrd_set_profiling(eng.h, True)
+        for _ in range(min(args.steps, 3)):
+            step()
+        torch.cuda.synchronize()
+        launch_ms = P.tnrd_get_launch_times(eng.h)
+        P.tnrd_set_profiling(eng.h, False)
     clocks = clk.summary()
     t = torch.tensor([ms, float(launches), float(np.mean(launch_ms)) if len(launch_ms) else 0.0], device=dev)
     if world > 1:
@@ -445,12 +457,17 @@ def main():
             except Exception:
                 traffic = None
         secs = mean_launch_ms / 1e3 if mean_launch_ms > 0 else None
+        launch_timing = ("CUDA events around every stage launch on the launching stream, " +
+                         ("inside the timed region" if args.launch_events == "inline" else
+                          f"over {min(args.steps, 3)} profiled steps right after the timed region (events between "
+                          "stage kernels would serialise the programmatic dependent launch the timed steps use)"))
         if not tensor:
             achieved = flop_launch / secs / 1e12 if secs else None
             roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                         "kernel": "stage_kernel (FP32 engine, one fused TNRD stage)",
                         "flop_per_px_stage": f_px, "flop_per_launch": flop_launch, "mean_launch_ms": mean_launch_ms,
+                        "launch_timing": launch_timing,
                         "peak_source": f"derived: {n_sm} SM x 128 FP32 lanes x 2 x {max_mhz:.0f} MHz "
                                        "(MEASURED_PEAKS.json has no FP32 figure)"}
         else:
@@ -470,7 +487,7 @@ def main():
                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                         "kernel": "tc_stage_kernel (tensor-core engine, one fused TNRD stage)",
                         "flop_per_px_stage": f_alu, "flop_per_launch": f_alu * px_rank,
-                        "mean_launch_ms": mean_launch_ms,
+                        "mean_launch_ms": mean_launch_ms, "launch_timing": launch_timing,
                         "peak_source": f"derived: {n_sm} SM x 128 FP32 lanes x 2 x {max_mhz:.0f} MHz "
                                        "(MEASURED_PEAKS.json has no FP32 figure)",
                         "fp32_equivalent_frac": (flop_launch / secs / 1e12 / peak) if secs else None,

@@ -115,10 +115,27 @@ struct tnrd_handle {
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;   // tnrd_denoise_host copy streams
     std::vector<cudaEvent_t> chunk_ev;               // 2 per pipelined chunk
     int ev_used = 0;
+    // CUDA graphs of the T-stage loop (tnrd_denoise), keyed by every launch argument;
+    // captured on a private stream, replayed on the caller's
+    struct Graph {
+        const float *f, *u, *scratch;
+        int B, H, W, tc_oh, tile, profile;
+        long long ld;
+        cudaGraph_t graph = nullptr;             // kept: its nodes address the exec's event records
+        cudaGraphExec_t exec = nullptr;
+        std::vector<cudaGraphNode_t> ev_nodes;   // profiling: event-record nodes in launch order
+        unsigned long long used = 0;
+    };
+    std::vector<Graph> graphs;
+    unsigned long long graph_clock = 0;
+    cudaStream_t s_cap = nullptr;
+    int use_graphs = -1;          // -1: from TNRD_GRAPH (default on)
     std::string err;
 };
 
 namespace {
+
+void drop_graphs(tnrd_handle *h);
 
 tnrd_status fail(tnrd_handle *h, tnrd_status s, const char *fmt, ...) {
     char buf[512];
@@ -235,6 +252,7 @@ tnrd_status launch_one(tnrd_handle *h, int t, const Plan &plan, StageArgs &a, in
     a.boundary = h->d.boundary;
     a.reaction = h->d.reaction;
     a.lambda = h->lambda[t];
+    unsigned ev_flags = cudaEventRecordDefault;
     if (h->profile) {
         if ((size_t)h->ev_used + 2 > h->ev.size()) {
             for (int k = 0; k < 64; ++k) {
@@ -243,13 +261,17 @@ tnrd_status launch_one(tnrd_handle *h, int t, const Plan &plan, StageArgs &a, in
                 h->ev.push_back(e);
             }
         }
-        TNRD_CUDA(h, cudaEventRecord(h->ev[h->ev_used], s));
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        TNRD_CUDA(h, cudaStreamIsCapturing(s, &cs));
+        // captured: event-record nodes (run_graph swaps their events per replay)
+        ev_flags = cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+        TNRD_CUDA(h, cudaEventRecordWithFlags(h->ev[h->ev_used], s, ev_flags));
     }
     cudaError_t e = plan.tc_oh > 0 ? tnrd::launch_stage_tc(h->d.ksize, a, B, s)
                                    : tnrd::launch_stage(h->d.ksize, plan.tile, a, B, s);
     if (e != cudaSuccess) return cuda_fail(h, e, "stage kernel launch");
     if (h->profile) {
-        TNRD_CUDA(h, cudaEventRecord(h->ev[h->ev_used + 1], s));
+        TNRD_CUDA(h, cudaEventRecordWithFlags(h->ev[h->ev_used + 1], s, ev_flags));
         h->ev_used += 2;
     }
     h->launches++;
@@ -475,6 +497,93 @@ void pack_tc_stage(const tnrd_desc &d, const float *filters, const float *phi_ho
 
 }  // namespace
 
+namespace {
+// The T stage launches of one tnrd_denoise call as a CUDA graph: captured once per
+// argument set on the handle's private stream (relaxed mode: the launchers query
+// attributes), replayed on the caller's stream.  Stage parameters, engine and
+// buffers are part of the key or invalidate the cache (tnrd_set_stage_params,
+// tnrd_set_engine).  With profiling on, the per-launch events are event-record nodes
+// whose events are swapped for fresh ones before every replay.
+template <class F>
+tnrd_status run_graph(tnrd_handle *h, const float *f, const float *u, int B, int H, int W, long long ld,
+                      const Plan &plan, cudaStream_t s, const F &stages) {
+    using G = tnrd_handle::Graph;
+    const int prof = h->profile ? 1 : 0;
+    G *g = nullptr;
+    for (G &c : h->graphs)
+        if (c.f == f && c.u == u && c.scratch == h->scratch && c.B == B && c.H == H && c.W == W && c.ld == ld &&
+            c.tc_oh == plan.tc_oh && c.tile == plan.tile && c.profile == prof) { g = &c; break; }
+    const int T = h->d.T;
+    if (!g) {
+        if (!h->s_cap) TNRD_CUDA(h, cudaStreamCreateWithFlags(&h->s_cap, cudaStreamNonBlocking));
+        const int ev0 = h->ev_used;
+        const unsigned long long l0 = h->launches;
+        TNRD_CUDA(h, cudaStreamBeginCapture(h->s_cap, cudaStreamCaptureModeRelaxed));
+        tnrd_status st = stages(h->s_cap);
+        cudaGraph_t graph = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(h->s_cap, &graph);
+        h->launches = l0;
+        if (st != TNRD_OK) { if (graph) cudaGraphDestroy(graph); return st; }
+        if (ce != cudaSuccess) return cuda_fail(h, ce, "graph capture");
+        G ng;
+        ng.f = f; ng.u = u; ng.scratch = h->scratch; ng.B = B; ng.H = H; ng.W = W; ng.ld = ld;
+        ng.tc_oh = plan.tc_oh; ng.tile = plan.tile; ng.profile = prof;
+        if (prof) {   // event-record nodes in the order of the events they record
+            size_t n = 0;
+            cudaGraphGetNodes(graph, nullptr, &n);
+            std::vector<cudaGraphNode_t> nodes(n);
+            cudaGraphGetNodes(graph, nodes.data(), &n);
+            ng.ev_nodes.assign(2 * (size_t)T, nullptr);
+            for (cudaGraphNode_t nd : nodes) {
+                cudaGraphNodeType ty;
+                cudaGraphNodeGetType(nd, &ty);
+                if (ty != cudaGraphNodeTypeEventRecord) continue;
+                cudaEvent_t e;
+                cudaGraphEventRecordNodeGetEvent(nd, &e);
+                for (int j = 0; j < 2 * T; ++j)
+                    if (h->ev[ev0 + j] == e) ng.ev_nodes[j] = nd;
+            }
+            h->ev_used = ev0;
+        }
+        const cudaError_t ie = cudaGraphInstantiate(&ng.exec, graph, 0);
+        if (ie != cudaSuccess) { cudaGraphDestroy(graph); return cuda_fail(h, ie, "graph instantiate"); }
+        ng.graph = graph;
+        if (h->graphs.size() >= 16) {   // evict the least recently used
+            size_t lru = 0;
+            for (size_t k = 1; k < h->graphs.size(); ++k)
+                if (h->graphs[k].used < h->graphs[lru].used) lru = k;
+            cudaGraphExecDestroy(h->graphs[lru].exec);
+            cudaGraphDestroy(h->graphs[lru].graph);
+            h->graphs.erase(h->graphs.begin() + (long)lru);
+        }
+        h->graphs.push_back(std::move(ng));
+        g = &h->graphs.back();
+    }
+    g->used = ++h->graph_clock;
+    if (prof) {
+        while ((size_t)h->ev_used + 2 * T > h->ev.size()) {
+            cudaEvent_t e;
+            TNRD_CUDA(h, cudaEventCreate(&e));
+            h->ev.push_back(e);
+        }
+        for (int j = 0; j < 2 * T; ++j)
+            if (g->ev_nodes[j]) TNRD_CUDA(h, cudaGraphExecEventRecordNodeSetEvent(g->exec, g->ev_nodes[j], h->ev[h->ev_used + j]));
+        h->ev_used += 2 * T;
+    }
+    TNRD_CUDA(h, cudaGraphLaunch(g->exec, s));
+    h->launches += T;
+    return TNRD_OK;
+}
+
+void drop_graphs(tnrd_handle *h) {
+    for (auto &c : h->graphs) {
+        cudaGraphExecDestroy(c.exec);
+        cudaGraphDestroy(c.graph);
+    }
+    h->graphs.clear();
+}
+}  // namespace
+
 extern "C" {
 
 int tnrd_abi_version(void) { return TNRD_ABI_VERSION; }
@@ -665,6 +774,7 @@ tnrd_status tnrd_set_stage_params(tnrd_handle *h, int t, const float *filters, c
     h->mode[t] = mode;
     h->lambda[t] = lambda;
     h->is_set[t] = 1;
+    drop_graphs(h);   // launch arguments (lambda, phi mode, engine eligibility) may have changed
     return TNRD_OK;
 }
 
@@ -679,6 +789,7 @@ tnrd_status tnrd_set_engine(tnrd_handle *h, int engine) {
     if (!h) return fail(nullptr, TNRD_EINVAL, "null handle");
     if (engine < TNRD_ENGINE_AUTO || engine > TNRD_ENGINE_TENSOR) return fail(h, TNRD_EINVAL, "bad engine %d", engine);
     h->engine = engine;
+    drop_graphs(h);
     return TNRD_OK;
 }
 
@@ -712,20 +823,28 @@ tnrd_status tnrd_denoise(tnrd_handle *h, const float *f, float *u, int B, int H,
     const tnrd::Image in_f{f, ld, (long long)H * ld, 0};
     const tnrd::Image in_s{h->scratch, W, (long long)H * W, 0};
     const tnrd::Image in_u{u, ld, (long long)H * ld, 0};
-    for (int t = 0; t < T; ++t) {
-        // ping-pong so that the last stage writes u: stage t writes u iff (T-1-t) is even
-        const bool to_u = ((T - 1 - t) % 2) == 0;
-        StageArgs a{};
-        a.u_in = t == 0 ? in_f : (to_u ? in_s : in_u);
-        a.f = in_f;
-        if (to_u) { a.u_out = u; a.out_ld = ld; a.out_img_stride = (long long)H * ld; }
-        else { a.u_out = h->scratch; a.out_ld = W; a.out_img_stride = (long long)H * W; }
-        a.out_row_base = 0;
-        a.H = H; a.W = W; a.y_begin = 0; a.y_end = H; a.avail_lo = 0; a.avail_hi = H;
-        st = launch_one(h, t, plan, a, B, s);
-        if (st != TNRD_OK) return st;
+    const auto stages = [&](cudaStream_t cs) -> tnrd_status {
+        for (int t = 0; t < T; ++t) {
+            // ping-pong so that the last stage writes u: stage t writes u iff (T-1-t) is even
+            const bool to_u = ((T - 1 - t) % 2) == 0;
+            StageArgs a{};
+            a.u_in = t == 0 ? in_f : (to_u ? in_s : in_u);
+            a.f = in_f;
+            if (to_u) { a.u_out = u; a.out_ld = ld; a.out_img_stride = (long long)H * ld; }
+            else { a.u_out = h->scratch; a.out_ld = W; a.out_img_stride = (long long)H * W; }
+            a.out_row_base = 0;
+            a.H = H; a.W = W; a.y_begin = 0; a.y_end = H; a.avail_lo = 0; a.avail_hi = H;
+            tnrd_status r = launch_one(h, t, plan, a, B, cs);
+            if (r != TNRD_OK) return r;
+        }
+        return TNRD_OK;
+    };
+    if (h->use_graphs < 0) {
+        const char *env = getenv("TNRD_GRAPH");
+        h->use_graphs = !(env && env[0] == '0');
     }
-    return TNRD_OK;
+    if (!h->use_graphs) return stages(s);
+    return run_graph(h, f, u, B, H, W, ld, plan, s, stages);
 }
 
 tnrd_status tnrd_denoise_host(tnrd_handle *h, const float *f_host, float *u_host, int B, int H, int W,
@@ -786,6 +905,8 @@ tnrd_status tnrd_destroy(tnrd_handle *h) {
     {
         DeviceGuard g(h->d.device);
         cudaDeviceSynchronize();
+        drop_graphs(h);
+        if (h->s_cap) cudaStreamDestroy(h->s_cap);
         cudaFree(h->d_params);
         cudaFree(h->d_tc);
         cudaFree(h->d_table);

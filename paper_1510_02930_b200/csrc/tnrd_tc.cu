@@ -202,6 +202,9 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // operands visible to the MMA (async proxy)
+    // programmatic dependent launch: the set-up above overlaps the previous stage's
+    // tail; images (u_in, f, u_out) are touched only after that grid has completed
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -656,8 +659,17 @@ cudaError_t launch_tc(StageArgs &a, int B, cudaStream_t s) {
     fprintf(stderr, "\n");
     return cudaGetLastError();
 #else
-    kern<<<grid, kTNT, smem, s>>>(p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kTNT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
 #endif
 }
 

@@ -574,3 +574,45 @@ def test_host_entry_point_pipelined_chunks_bitwise(torch_cuda, P):
     torch.cuda.synchronize()
     assert torch.equal(full, us)
     eng.close()
+
+
+# ------------------------------------------------------------------ CUDA-graph replay
+def test_graph_replay_bitwise_equal_to_eager_and_invalidated(torch_cuda, P):
+    """tnrd_denoise replays a captured graph of its T launches: repeated calls (and the
+    profiled variant with event nodes) equal eager launches (TNRD_GRAPH=0) bitwise, and
+    new stage parameters (here a new lambda_0) take effect on the next call."""
+    torch = torch_cuda
+    p = make_problem(2)
+    f = torch.from_numpy(np.ascontiguousarray(p.f)).cuda()
+    os.environ["TNRD_GRAPH"] = "0"
+    try:
+        eager = P.TNRD(p.model)
+        u_eager = eager.denoise(f)
+        torch.cuda.synchronize()
+    finally:
+        del os.environ["TNRD_GRAPH"]
+    eng = P.TNRD(p.model)
+    outs = [eng.denoise(f).clone() for _ in range(3)]
+    P.tnrd_set_profiling(eng.h, True)
+    outs.append(eng.denoise(f).clone())
+    outs.append(eng.denoise(f).clone())
+    torch.cuda.synchronize()
+    times = P.tnrd_get_launch_times(eng.h)
+    P.tnrd_set_profiling(eng.h, False)
+    assert len(times) == 2 * p.model.filters.shape[0] and all(t > 0 for t in times)
+    for o in outs:
+        assert torch.equal(o, u_eager)
+    assert eng.launches == 5 * p.model.filters.shape[0]
+    # new lambda_0: the cached graph must not replay the old launch arguments
+    m = p.model
+    P.tnrd_set_stage_params(eng.h, 0, m.filters[0], m.rbf_w[0], m.rbf_mu0[0], m.rbf_step[0], m.rbf_gamma[0],
+                            2.0 * float(m.lam[0]))
+    P.tnrd_set_stage_params(eager.h, 0, m.filters[0], m.rbf_w[0], m.rbf_mu0[0], m.rbf_step[0], m.rbf_gamma[0],
+                            2.0 * float(m.lam[0]))
+    u2 = eng.denoise(f)
+    u2_eager = eager.denoise(f)
+    torch.cuda.synchronize()
+    assert not torch.equal(u2, u_eager)
+    assert torch.equal(u2, u2_eager)
+    eng.close()
+    eager.close()

@@ -9,7 +9,7 @@ timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gp
 python -c "
 import json; d=json.loads(open('gpurun_out/bench_$tag.json').read().strip().splitlines()[-1])
 print('BENCH', d['value'], 'MPix/s', 'launch_ms', d['roofline']['mean_launch_ms'], 'frac', d['roofline']['frac'])" || tail -5 gpurun_out/bench_$tag.err
-timeout 300 python bench.py --config 3 --steps 20 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_$tag.json 2>/dev/null
+timeout 300 python bench.py --config 3 --steps 1000 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_$tag.json 2>/dev/null
 python -c "
 import json; d=json.loads(open('gpurun_out/bench_c3_$tag.json').read().strip().splitlines()[-1])
 print('C3', d['value'], 'MPix/s', 'launch_ms', d['roofline']['mean_launch_ms'], 'frac', d['roofline']['frac'])"
