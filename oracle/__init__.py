@@ -73,6 +73,10 @@ def lib() -> ctypes.CDLL:
             L.oracle_exp_fixed.restype = ctypes.c_double
             L.oracle_reaction.argtypes = [ctypes.c_double] * 4 + [i]
             L.oracle_reaction.restype = ctypes.c_double
+            L.oracle_scale_to_peak.argtypes = [ctypes.c_long, dp, ctypes.c_double, dp]
+            L.oracle_scale_to_peak.restype = i
+            L.oracle_ssim.argtypes = [i, i, dp, dp, ctypes.c_double]
+            L.oracle_ssim.restype = ctypes.c_double
             _lib = L
     return _lib
 
@@ -226,6 +230,27 @@ def psnr(u, clean, peak: float) -> float:
     """10 log10(peak^2 / MSE), unclamped (S l.374 after the 255/peak rescale)."""
     mse = float(np.mean((np.asarray(u, np.float64) - np.asarray(clean, np.float64)) ** 2))
     return float("inf") if mse == 0 else 10.0 * np.log10(peak * peak / mse)
+
+
+def scale_to_peak(x, peak: float) -> np.ndarray:
+    """x * peak / max(x) (S l.351-358); ValueError for an all-zero or negative image."""
+    x = _d(x)
+    out = np.empty_like(x)
+    if lib().oracle_scale_to_peak(x.size, _p(x), float(peak), _p(out)) != 0:
+        raise ValueError("scale_to_peak: all-zero or negative image")
+    return out
+
+
+def ssim(u, clean, peak: float) -> float:
+    """Mean SSIM over the valid 11x11 Gaussian (sigma 1.5) windows after the 255/peak
+    rescale (S l.381-389; reading M2)."""
+    u, c = _d(u), _d(clean)
+    if u.shape != c.shape or u.ndim != 2:
+        raise ValueError("ssim: two images of the same [H][W] shape")
+    r = lib().oracle_ssim(u.shape[0], u.shape[1], _p(u), _p(c), float(peak))
+    if r == -1.0:
+        raise ValueError("ssim: image smaller than the 11x11 window")
+    return float(r)
 
 
 def num_threads() -> int:

@@ -356,3 +356,63 @@ EXPORT void oracle_sample_poisson(int B, int H, int W, const double *u, uint64_t
 #pragma omp parallel for schedule(static)
     for (long i = 0; i < (long)B * H * W; ++i) f[i] = oracle_poisson_draw(u[i], (uint64_t)i, seed);
 }
+
+/* ---------------------------------------------------------------------------
+ * Steps either side of the path: peak scaling and SSIM.
+ * ------------------------------------------------------------------------- */
+
+/* Peak scaling (S l.351-358, "scale_to_peak"; P l.113-116: the noise level "is
+ * generally defined as the peak value (the maximal value)" of the clean image):
+ * out = x * (peak / max(x)), and exactly peak where x == max(x) (S l.354's post-
+ * condition max(u) == peak, which the rounded product need not meet).  Returns -1
+ * (out untouched) if max(x) <= 0 (S l.355: all-zero image is an error) or any
+ * x < 0, else 0. */
+EXPORT int oracle_scale_to_peak(long n, const double *x, double peak, double *out) {
+    double m = 0.0;
+    for (long i = 0; i < n; ++i) {
+        if (x[i] < 0.0) return -1;
+        if (x[i] > m) m = x[i];
+    }
+    if (m <= 0.0) return -1;
+    const double r = peak / m;
+    for (long i = 0; i < n; ++i) out[i] = x[i] == m ? peak : x[i] * r;
+    return 0;
+}
+
+/* SSIM (S l.381-389; P l.444-445 cites the structural similarity index): both
+ * images rescaled by 255/peak (S l.374), then the mean over every 11 x 11 window
+ * that lies inside the image ("valid" windows, reading M2 in DESIGN.md §2) of
+ *   ((2 mu_x mu_y + C1)(2 s_xy + C2)) / ((mu_x^2 + mu_y^2 + C1)(s_x^2 + s_y^2 + C2)),
+ * mu, s^2, s_xy the window's Gaussian-weighted (sigma = 1.5, weights normalised to
+ * sum 1) means, variances and covariance, C1 = (0.01 L)^2, C2 = (0.03 L)^2, L = 255.
+ * Returns -1 if H or W < 11. */
+EXPORT double oracle_ssim(int H, int W, const double *x, const double *y, double peak) {
+    enum { WIN = 11, HALF = 5 };
+    if (H < WIN || W < WIN) return -1.0;
+    double wgt[WIN][WIN], wsum = 0.0;
+    for (int a = 0; a < WIN; ++a)
+        for (int b = 0; b < WIN; ++b) {
+            const double da = a - HALF, db = b - HALF;
+            wgt[a][b] = exp(-(da * da + db * db) / (2.0 * 1.5 * 1.5));
+            wsum += wgt[a][b];
+        }
+    const double s = 255.0 / peak, C1 = (0.01 * 255.0) * (0.01 * 255.0), C2 = (0.03 * 255.0) * (0.03 * 255.0);
+    double total = 0.0;
+    for (int i = 0; i + WIN <= H; ++i)
+        for (int j = 0; j + WIN <= W; ++j) {
+            double mx = 0, my = 0, xx = 0, yy = 0, xy = 0;
+            for (int a = 0; a < WIN; ++a)
+                for (int b = 0; b < WIN; ++b) {
+                    const double w = wgt[a][b] / wsum;
+                    const double xv = s * x[(long)(i + a) * W + j + b], yv = s * y[(long)(i + a) * W + j + b];
+                    mx += w * xv;
+                    my += w * yv;
+                    xx += w * xv * xv;
+                    yy += w * yv * yv;
+                    xy += w * xv * yv;
+                }
+            const double vx = xx - mx * mx, vy = yy - my * my, cxy = xy - mx * my;
+            total += ((2 * mx * my + C1) * (2 * cxy + C2)) / ((mx * mx + my * my + C1) * (vx + vy + C2));
+        }
+    return total / ((double)(H - WIN + 1) * (W - WIN + 1));
+}

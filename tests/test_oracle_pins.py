@@ -564,3 +564,82 @@ def test_poisson_sampler_zero_mean_determinism_and_pmf():
     for k in range(9):
         p = scipy.stats.poisson.pmf(k, 2.5)
         assert abs(np.mean(a == k) - p) < 5 * np.sqrt(p * (1 - p) / n)
+
+
+# ------------------------------------------------------------------ P18 / P19: peak scaling and SSIM
+def test_scale_to_peak_spec_examples_and_errors():
+    """S l.351-358: post max(u) == peak; examples constant 255 -> constant 4,
+    peak == max -> identity, {0, 255} with peak 1 -> {0, 1}; all-zero image -> error."""
+    assert np.array_equal(oracle.scale_to_peak(np.full((5, 6), 255.0), 4.0), np.full((5, 6), 4.0))
+    x = np.random.default_rng(3).uniform(0, 200, (7, 9))
+    x[2, 3] = 250.0
+    assert np.array_equal(oracle.scale_to_peak(x, 250.0), x)
+    two = np.array([[0.0, 255.0], [255.0, 0.0]])
+    assert np.array_equal(oracle.scale_to_peak(two, 1.0), two / 255.0)
+    with pytest.raises(ValueError):
+        oracle.scale_to_peak(np.zeros((4, 4)), 1.0)
+    with pytest.raises(ValueError):
+        oracle.scale_to_peak(np.array([[1.0, -1.0]]), 1.0)
+
+
+def test_scale_to_peak_max_and_ratios():
+    """max(out) == peak (to the last double ulp) and ratios between pixels are kept."""
+    x = np.random.default_rng(5).gamma(2.0, 30.0, (33, 47))
+    for peak in (0.1, 1.0, 4.0, 40.0):
+        out = oracle.scale_to_peak(x, peak)
+        assert out.max() == peak
+        i, j = np.unravel_index(np.argmin(x), x.shape)
+        assert np.allclose(out / out[i, j], x / x[i, j], rtol=1e-14)
+
+
+def _ssim_window_moments(x, y):
+    """Gaussian-weighted window means over the valid 11x11 windows, by scipy
+    (scipy.signal.correlate2d), independent of the oracle's loops."""
+    g = np.exp(-((np.arange(11) - 5.0) ** 2) / (2 * 1.5 ** 2))
+    w = np.outer(g, g)
+    w /= w.sum()
+    corr = lambda a: scipy.signal.correlate2d(a, w, mode="valid")
+    return corr(x), corr(y), corr(x * x), corr(y * y), corr(x * y)
+
+
+def test_ssim_identity_symmetry_and_range():
+    """SSIM(x, x) = 1; symmetric in its arguments; in [-1, 1]; reference vs 255 -
+    reference below 1 (S l.386-388); images smaller than the window are an error."""
+    rng = np.random.default_rng(8)
+    x = rng.uniform(0, 4, (40, 52))
+    y = np.clip(x + rng.normal(0, 0.5, x.shape), 0, None)
+    assert abs(oracle.ssim(x, x, 4.0) - 1.0) < 1e-12
+    assert abs(oracle.ssim(x, y, 4.0) - oracle.ssim(y, x, 4.0)) < 1e-12
+    assert -1.0 <= oracle.ssim(x, y, 4.0) < 1.0
+    ref = rng.uniform(0, 255, (30, 30))
+    assert oracle.ssim(255.0 - ref, ref, 255.0) < 1.0
+    with pytest.raises(ValueError):
+        oracle.ssim(np.ones((10, 30)), np.ones((10, 30)), 1.0)
+
+
+def test_ssim_constant_shift_closed_form():
+    """y = x + c: s_y = s_x and s_xy = s_x^2, so the contrast-structure factor is 1 and
+    SSIM = mean (2 mu (mu + c) + C1) / (mu^2 + (mu + c)^2 + C1) (pins the luminance
+    term and C1).  S l.389's checkerboard-plus-10 example, on the 255 scale."""
+    yy, xx = np.mgrid[0:64, 0:64]
+    board = np.where(((yy // 8) + (xx // 8)) % 2 == 0, 40.0, 200.0)
+    for x, c in ((board, 10.0), (np.random.default_rng(2).uniform(0, 255, (37, 45)), -17.5)):
+        mu, _, _, _, _ = _ssim_window_moments(x, x)
+        C1 = (0.01 * 255) ** 2
+        want = np.mean((2 * mu * (mu + c) + C1) / (mu ** 2 + (mu + c) ** 2 + C1))
+        assert abs(oracle.ssim(x + c, x, 255.0) - want) < 1e-10
+
+
+def test_ssim_scaling_closed_form():
+    """y = a x: mu_y = a mu_x, s_y^2 = a^2 s_x^2, s_xy = a s_x^2, so SSIM = mean of
+    (2 a mu^2 + C1) / ((1 + a^2) mu^2 + C1) * (2 a s^2 + C2) / ((1 + a^2) s^2 + C2)
+    (pins the variance / covariance terms and C2); also the 255/peak rescale."""
+    x = np.random.default_rng(4).gamma(2.0, 0.8, (31, 43))
+    a, peak = 0.7, 4.0
+    xs = x * 255.0 / peak
+    mu, _, xx2, _, _ = _ssim_window_moments(xs, xs)
+    var = xx2 - mu ** 2
+    C1, C2 = (0.01 * 255) ** 2, (0.03 * 255) ** 2
+    want = np.mean((2 * a * mu ** 2 + C1) / ((1 + a * a) * mu ** 2 + C1) *
+                   (2 * a * var + C2) / ((1 + a * a) * var + C2))
+    assert abs(oracle.ssim(a * x, x, peak) - want) < 1e-10
