@@ -242,6 +242,25 @@ TNRD_API tnrd_status tnrd_sample_poisson(const float *u_dev, float *f_dev, int B
 TNRD_API tnrd_status tnrd_psnr(const float *u_dev, const float *clean_dev, int B, int H, int W, long long ld,
                                const float *peak, double *psnr_out, void *cuda_stream);
 
+/* Peak scaling (S l.351-358; P l.113-116, "the noise level ... is generally defined
+ * as the peak value (the maximal value)"): out_b = x_b * (peak_b / max(x_b)) in fp32,
+ * and exactly peak_b where x_b == max(x_b), so max(out_b) == peak_b.
+ *   x_dev, out_dev  device [B][H][ld] (may alias); peak host [B], > 0
+ * EINVAL: bad sizes, B > 65535, a peak <= 0, a negative / NaN input or an all-zero
+ * image (S l.355; out is then undefined).  Synchronous. */
+TNRD_API tnrd_status tnrd_scale_to_peak(const float *x_dev, float *out_dev, int B, int H, int W, long long ld,
+                                        const float *peak, void *cuda_stream);
+
+/* SSIM per image (S l.381-389; P l.444-445; reading M2 in DESIGN.md): both images
+ * rescaled by 255/peak_b, the mean over every 11 x 11 window inside the image of
+ * ((2 mu_u mu_c + C1)(2 s_uc + C2)) / ((mu_u^2 + mu_c^2 + C1)(s_u^2 + s_c^2 + C2)),
+ * Gaussian-weighted window moments (sigma = 1.5, weights summing to 1), C1 = (0.01 *
+ * 255)^2, C2 = (0.03 * 255)^2.  Moments in double; window sums in a fixed order.
+ *   u_dev, clean_dev device [B][H][ld]; peak host [B]; ssim_out host [B]
+ * EINVAL: H or W < 11, ld < W, B outside [1, 65535], a peak <= 0.  Synchronous. */
+TNRD_API tnrd_status tnrd_ssim(const float *u_dev, const float *clean_dev, int B, int H, int W, long long ld,
+                               const float *peak, double *ssim_out, void *cuda_stream);
+
 /* ---------------- multi-GPU: row slabs of one large image ----------------
  * Rank rho of N owns rows [row0, row0 + rows) of an H_global x W image.
  * Before every stage each rank exchanges 2r = ksize-1 rows of u_t with each

@@ -84,6 +84,8 @@ def _load() -> ctypes.CDLL:
         "tnrd_loss_grad": ([vp, vp, vp, i, i, i, ll, fp, fp, fp, ctypes.POINTER(ctypes.c_double), vp], i),
         "tnrd_sample_poisson": ([vp, vp, i, i, i, ll, ctypes.c_ulonglong, vp], i),
         "tnrd_psnr": ([vp, vp, i, i, i, ll, fp, ctypes.POINTER(ctypes.c_double), vp], i),
+        "tnrd_scale_to_peak": ([vp, vp, i, i, i, ll, fp, vp], i),
+        "tnrd_ssim": ([vp, vp, i, i, i, ll, fp, ctypes.POINTER(ctypes.c_double), vp], i),
         "tnrd_set_engine": ([vp, i], i),
         "tnrd_engine_for": ([vp, i, i, i], i),
         "tnrd_set_grad_chunk": ([vp, i], i),
@@ -102,7 +104,7 @@ EXPORTED = (
     "tnrd_nccl_unique_id", "tnrd_comm_init", "tnrd_denoise_slab", "tnrd_denoise_slabs_loopback",
     "tnrd_denoise_slabs_nccl_self",
     "tnrd_set_profiling", "tnrd_get_launch_times", "tnrd_debug_phi", "tnrd_debug_prox", "tnrd_loss_grad",
-    "tnrd_sample_poisson", "tnrd_psnr", "tnrd_set_engine", "tnrd_engine_for", "tnrd_set_grad_chunk",
+    "tnrd_sample_poisson", "tnrd_psnr", "tnrd_scale_to_peak", "tnrd_ssim", "tnrd_set_engine", "tnrd_engine_for", "tnrd_set_grad_chunk",
 )
 
 
@@ -313,6 +315,36 @@ def tnrd_psnr(u, clean, peak, stream=None) -> np.ndarray:
     _check(_lib.tnrd_psnr(_dev_ptr(u3), _dev_ptr(c3), B, H, W, u3.stride(1), _f32p(pk),
                           out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream_ptr(stream)))
     return out
+
+
+def tnrd_scale_to_peak(x, peak, out=None, stream=None):
+    """out = x * (peak / max(x)) per image, exactly peak at the max (S l.351-358)."""
+    x3 = x if x.dim() == 3 else x.unsqueeze(0)
+    if out is None:
+        out = torch_empty_like(x3)
+    o3 = out if out.dim() == 3 else out.unsqueeze(0)
+    B, H, W = x3.shape
+    if o3.shape != x3.shape or o3.stride(1) != x3.stride(1):
+        raise ValueError("out must match x")
+    pk = _host_f32(np.broadcast_to(np.asarray(peak, np.float32), (B,)))
+    _check(_lib.tnrd_scale_to_peak(_dev_ptr(x3), _dev_ptr(o3), B, H, W, x3.stride(1), _f32p(pk), _stream_ptr(stream)))
+    return out
+
+
+def tnrd_ssim(u, clean, peak, stream=None) -> np.ndarray:
+    """Mean SSIM per image over the valid 11x11 Gaussian windows (S l.381-389, reading M2)."""
+    u3, c3 = (u, clean) if u.dim() == 3 else (u.unsqueeze(0), clean.unsqueeze(0))
+    B, H, W = u3.shape
+    pk = _host_f32(np.broadcast_to(np.asarray(peak, np.float32), (B,)))
+    out = np.zeros(B, np.float64)
+    _check(_lib.tnrd_ssim(_dev_ptr(u3), _dev_ptr(c3), B, H, W, u3.stride(1), _f32p(pk),
+                          out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream_ptr(stream)))
+    return out
+
+
+def torch_empty_like(x):
+    import torch
+    return torch.empty_like(x)
 
 
 # ------------------------------------------------------------------ convenience wrapper

@@ -1141,6 +1141,75 @@ tnrd_status tnrd_psnr(const float *u, const float *c, int B, int H, int W, long 
     return TNRD_OK;
 }
 
+tnrd_status tnrd_scale_to_peak(const float *x, float *out, int B, int H, int W, long long ld, const float *peak,
+                               void *stream) {
+    if (!x || !out || !peak) return fail(nullptr, TNRD_EINVAL, "null pointer");
+    if (B < 1 || H < 1 || W < 1 || ld < W) return fail(nullptr, TNRD_EINVAL, "bad size");
+    if (B > 65535) return fail(nullptr, TNRD_EINVAL, "B must be <= 65535 (grid.y)");
+    for (int b = 0; b < B; ++b)
+        if (!std::isfinite(peak[b]) || peak[b] <= 0.f) return fail(nullptr, TNRD_EINVAL, "peak[%d] must be > 0", b);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    // scratch: mx [B] (unsigned), bad (int), peak [B] (float)
+    char *scr = nullptr;
+    const size_t n_mx = sizeof(unsigned) * (size_t)B, n_bad = 16, n_pk = sizeof(float) * (size_t)B;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&scr), n_mx + n_bad + n_pk, s);
+    if (e != cudaSuccess) return fail(nullptr, TNRD_ENOMEM, "cudaMallocAsync: %s", cudaGetErrorString(e));
+    unsigned *mx = reinterpret_cast<unsigned *>(scr);
+    int *bad = reinterpret_cast<int *>(scr + n_mx);
+    float *pk = reinterpret_cast<float *>(scr + n_mx + n_bad);
+    std::vector<unsigned> hm((size_t)B);
+    int hbad = 0;
+    e = cudaMemsetAsync(bad, 0, sizeof(int), s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(pk, peak, n_pk, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = tnrd::data_scale_to_peak(x, out, B, H, W, ld, pk, mx, bad, sms, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hm.data(), mx, n_mx, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(scr, s);
+    if (e != cudaSuccess) return fail(nullptr, TNRD_ECUDA, "scale_to_peak: %s", cudaGetErrorString(e));
+    if (hbad) return fail(nullptr, TNRD_EINVAL, "scale_to_peak: negative or NaN input (out is undefined)");
+    for (int b = 0; b < B; ++b)
+        if (hm[b] == 0) return fail(nullptr, TNRD_EINVAL, "scale_to_peak: image %d is all zero (out is undefined)", b);
+    return TNRD_OK;
+}
+
+tnrd_status tnrd_ssim(const float *u, const float *c, int B, int H, int W, long long ld, const float *peak,
+                      double *out, void *stream) {
+    if (!u || !c || !peak || !out) return fail(nullptr, TNRD_EINVAL, "null pointer");
+    if (B < 1 || H < 11 || W < 11 || ld < W) return fail(nullptr, TNRD_EINVAL, "bad size (H, W >= 11)");
+    if (B > 65535) return fail(nullptr, TNRD_EINVAL, "B must be <= 65535 (grid.y)");
+    for (int b = 0; b < B; ++b)
+        if (!std::isfinite(peak[b]) || peak[b] <= 0.f) return fail(nullptr, TNRD_EINVAL, "peak[%d] must be > 0", b);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const long long windows = (long long)(H - 10) * (W - 10);
+    const int nb = tnrd::data_ssim_blocks(windows, sms);
+    std::vector<double> hs((size_t)B);
+    for (int b = 0; b < B; ++b) hs[b] = 255.0 / (double)peak[b];
+    double *buf = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&buf), sizeof(double) * (size_t)B * (nb + 1), s);
+    if (e != cudaSuccess) return fail(nullptr, TNRD_ENOMEM, "cudaMallocAsync: %s", cudaGetErrorString(e));
+    double *scale = buf, *part = buf + B;
+    std::vector<double> hp((size_t)B * nb);
+    e = cudaMemcpyAsync(scale, hs.data(), sizeof(double) * (size_t)B, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = tnrd::data_ssim(u, c, B, H, W, ld, scale, part, nb, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hp.data(), part, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(buf, s);
+    if (e != cudaSuccess) return fail(nullptr, TNRD_ECUDA, "ssim: %s", cudaGetErrorString(e));
+    for (int b = 0; b < B; ++b) {
+        double sum = 0.0;
+        for (int j = 0; j < nb; ++j) sum += hp[(size_t)b * nb + j];
+        out[b] = sum / (double)windows;
+    }
+    return TNRD_OK;
+}
+
 // ------------------------------------------------------------------ slabs
 tnrd_status tnrd_nccl_unique_id(void *id128) {
     if (!id128) return fail(nullptr, TNRD_EINVAL, "null id");

@@ -182,5 +182,13 @@ cudaError_t data_sample_poisson(const float *u, float *f, int B, int H, int W, l
 int data_sq_err_blocks(long long per_image, int num_sms);
 cudaError_t data_sq_err(const float *u, const float *c, int B, int H, int W, long long ld, double *partial,
                         int blocks, cudaStream_t s);
+// x -> x * (peak_b / max_b(x)) per image (exactly peak_b at the max); mx [B] scratch,
+// *bad set if an input is negative or NaN.
+cudaError_t data_scale_to_peak(const float *x, float *out, int B, int H, int W, long long ld, const float *peak_dev,
+                               unsigned *mx, int *bad, int num_sms, cudaStream_t s);
+// SSIM partial sums over the valid 11 x 11 windows: partial[b * blocks + k]
+int data_ssim_blocks(long long windows, int num_sms);
+cudaError_t data_ssim(const float *x, const float *y, int B, int H, int W, long long ld, const double *scale_dev,
+                      double *partial, int blocks, cudaStream_t s);
 
 }  // namespace tnrd
