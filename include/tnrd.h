@@ -286,6 +286,15 @@ TNRD_API tnrd_status tnrd_denoise_slab(tnrd_handle *h, const float *f_slab_dev, 
                               int H_global, int W, int row0, int rows, long long ld, float peak,
                               void *cuda_stream);
 
+/* Wait for the work enqueued on cuda_stream (e.g. tnrd_denoise_slab) while polling
+ * the communicator's asynchronous error every 200 us (ncclCommGetAsyncError).  A
+ * NCCL error, or no completion within timeout_ms (< 0: no limit), aborts the
+ * communicator (ncclCommAbort: pending NCCL kernels return) and returns ENCCL; the
+ * handle then needs tnrd_comm_init again.  ECUDA for a failed stream.  OK when the
+ * stream has drained without error.  Failure detection for the slab path (SURVEY
+ * §5); every tnrd_denoise_slab also polls once per exchange without blocking. */
+TNRD_API tnrd_status tnrd_comm_wait(tnrd_handle *h, void *cuda_stream, int timeout_ms);
+
 /* Single-device emulation of the slab path: the image f_dev [H][ld] is split
  * into nslabs row slabs processed with the same slab kernels and halo buffers,
  * the halo exchange done with device-to-device copies instead of NCCL.  Used

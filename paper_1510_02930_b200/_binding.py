@@ -85,6 +85,7 @@ def _load() -> ctypes.CDLL:
         "tnrd_sample_poisson": ([vp, vp, i, i, i, ll, ctypes.c_ulonglong, vp], i),
         "tnrd_psnr": ([vp, vp, i, i, i, ll, fp, ctypes.POINTER(ctypes.c_double), vp], i),
         "tnrd_scale_to_peak": ([vp, vp, i, i, i, ll, fp, vp], i),
+        "tnrd_comm_wait": ([vp, vp, i], i),
         "tnrd_ssim": ([vp, vp, i, i, i, ll, fp, ctypes.POINTER(ctypes.c_double), vp], i),
         "tnrd_set_engine": ([vp, i], i),
         "tnrd_engine_for": ([vp, i, i, i], i),
@@ -104,7 +105,7 @@ EXPORTED = (
     "tnrd_nccl_unique_id", "tnrd_comm_init", "tnrd_denoise_slab", "tnrd_denoise_slabs_loopback",
     "tnrd_denoise_slabs_nccl_self",
     "tnrd_set_profiling", "tnrd_get_launch_times", "tnrd_debug_phi", "tnrd_debug_prox", "tnrd_loss_grad",
-    "tnrd_sample_poisson", "tnrd_psnr", "tnrd_scale_to_peak", "tnrd_ssim", "tnrd_set_engine", "tnrd_engine_for", "tnrd_set_grad_chunk",
+    "tnrd_sample_poisson", "tnrd_psnr", "tnrd_scale_to_peak", "tnrd_ssim", "tnrd_comm_wait", "tnrd_set_engine", "tnrd_engine_for", "tnrd_set_grad_chunk",
 )
 
 
@@ -340,6 +341,12 @@ def tnrd_ssim(u, clean, peak, stream=None) -> np.ndarray:
     _check(_lib.tnrd_ssim(_dev_ptr(u3), _dev_ptr(c3), B, H, W, u3.stride(1), _f32p(pk),
                           out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream_ptr(stream)))
     return out
+
+
+def tnrd_comm_wait(h: int, stream=None, timeout_ms: int = -1) -> None:
+    """Drain `stream` while polling the communicator's asynchronous error (ENCCL on error
+    or timeout; the communicator is then aborted)."""
+    _check(_lib.tnrd_comm_wait(h, _stream_ptr(stream), int(timeout_ms)), h)
 
 
 def torch_empty_like(x):

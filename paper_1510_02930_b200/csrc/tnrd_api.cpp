@@ -11,7 +11,9 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -39,6 +41,8 @@ struct NcclApi {
     ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -63,6 +67,8 @@ NcclApi &nccl() {
     TNRD_SYM(Recv, "ncclRecv");
     TNRD_SYM(GroupStart, "ncclGroupStart");
     TNRD_SYM(GroupEnd, "ncclGroupEnd");
+    TNRD_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
+    TNRD_SYM(CommAbort, "ncclCommAbort");
     TNRD_SYM(GetErrorString, "ncclGetErrorString");
 #undef TNRD_SYM
     api.loaded = true;
@@ -312,6 +318,21 @@ tnrd_status run_slab(tnrd_handle *h, const float *f_slab, long long f_ld, float 
     return launch_one(h, stage, plan, a, 1, s);
 }
 
+// Non-blocking poll of the communicator's asynchronous error (a failed or vanished
+// peer, a NCCL-internal error): on error the communicator is aborted, so enqueued
+// NCCL kernels return instead of waiting forever, and the handle reports ENCCL.
+tnrd_status comm_async_check(tnrd_handle *h) {
+    if (!h->comm) return TNRD_OK;
+    NcclApi &api = nccl();
+    ncclResult_t ae = ncclSuccess;
+    const ncclResult_t r = api.CommGetAsyncError(h->comm, &ae);
+    if (r == ncclSuccess && (ae == ncclSuccess || ae == ncclInProgress)) return TNRD_OK;
+    const ncclResult_t bad = r != ncclSuccess ? r : ae;
+    api.CommAbort(h->comm);
+    h->comm = nullptr;
+    return fail(h, TNRD_ENCCL, "NCCL asynchronous error (communicator aborted): %s", api.GetErrorString(bad));
+}
+
 struct NcclExchange : SlabExchange {
     tnrd_handle *h; int rows, W; cudaStream_t s;
     NcclExchange(tnrd_handle *h_, int rows_, int W_, cudaStream_t s_) : h(h_), rows(rows_), W(W_), s(s_) {}
@@ -332,7 +353,7 @@ struct NcclExchange : SlabExchange {
         ncclResult_t r2 = api.GroupEnd();
         if (r != ncclSuccess || r2 != ncclSuccess)
             return fail(h, TNRD_ENCCL, "halo exchange: %s", api.GetErrorString(r != ncclSuccess ? r : r2));
-        return TNRD_OK;
+        return comm_async_check(h);   // a peer's failure surfaces here (non-blocking poll)
     }
 };
 
@@ -1397,6 +1418,31 @@ tnrd_status tnrd_denoise_slab(tnrd_handle *h, const float *f_slab, float *u_slab
         return run_slabs(h, sl, H, W, none, s);
     }
     return run_slabs(h, sl, H, W, ex, s);
+}
+
+tnrd_status tnrd_comm_wait(tnrd_handle *h, void *stream, int timeout_ms) {
+    if (!h) return fail(nullptr, TNRD_EINVAL, "null handle");
+    DeviceGuard g(h->d.device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        const cudaError_t q = cudaStreamQuery(s);
+        if (q == cudaSuccess) return comm_async_check(h);
+        if (q != cudaErrorNotReady) return cuda_fail(h, q, "stream");
+        tnrd_status st = comm_async_check(h);
+        if (st != TNRD_OK) return st;
+        const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0);
+        if (timeout_ms >= 0 && ms.count() > timeout_ms) {
+            if (h->comm) {
+                nccl().CommAbort(h->comm);
+                h->comm = nullptr;
+                return fail(h, TNRD_ENCCL, "timed out after %d ms waiting for the halo exchanges (communicator aborted)",
+                            timeout_ms);
+            }
+            return fail(h, TNRD_ECUDA, "timed out after %d ms", timeout_ms);
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
 }
 
 tnrd_status tnrd_denoise_slabs_loopback(tnrd_handle *h, const float *f, float *u, int H, int W, long long ld,

@@ -91,10 +91,18 @@ struct alignas(64) TcArgs {
     int use_tma;   // 0: u tiles by per-element loads (rows not 16-byte aligned / no driver entry point)
     unsigned long long *prof;   // TNRD_TC_PROF builds: per CTA and warp {wait cycles, total cycles}
 };
-#ifdef TNRD_TC_PROF
-#define TCP_WAIT(bar, par) { const long long t0_ = clock64(); mbar_wait(bar, par); tcp_wait += clock64() - t0_; }
+#ifdef TNRD_TC_WAITNAP
+// experiment: phi / build-gather waits as test_wait + __nanosleep(TNRD_TC_WAITNAP ns) polls
+__device__ __forceinline__ void mbar_wait_pw(uint64_t *bar, uint32_t parity) {
+    while (!mbar_test(bar, parity, false)) __nanosleep(TNRD_TC_WAITNAP);
+}
 #else
-#define TCP_WAIT(bar, par) mbar_wait(bar, par)
+__device__ __forceinline__ void mbar_wait_pw(uint64_t *bar, uint32_t parity) { mbar_wait(bar, parity); }
+#endif
+#ifdef TNRD_TC_PROF
+#define TCP_WAIT(bar, par) { const long long t0_ = clock64(); mbar_wait_pw(bar, par); tcp_wait += clock64() - t0_; }
+#else
+#define TCP_WAIT(bar, par) mbar_wait_pw(bar, par)
 #endif
 
 // Shared memory (floats): operand block | u tiles [2][UH][UP] (128-byte aligned, TMA

@@ -199,11 +199,21 @@ __device__ __forceinline__ void phi_fpairs(const float *__restrict__ s_pp, int p
             tsg2[p] = pk(h0.z, h0.w);
             yra[p] = h2.z;
             yrb[p] = h2.w;
+#ifdef TNRD_TC_OLDRANGE
             const f2 lo2 = fma2(pk(warp_min(va), warp_min(vb)), h1.x, h1.y);
             const f2 hi2 = fma2(pk(warp_max(va), warp_max(vb)), h1.x, pk(h2.x, h2.y));
             // ceil / floor are monotone: min / max first, one conversion each
             const int u0 = max(0, ceil_i(fminf(lo(lo2), hi(lo2))));
             const int u1 = min(nb - 1, floor_i(fmaxf(lo(hi2), hi(hi2))));
+#else
+            // A > 0 and fma rounding is monotone, so min_lanes fma(v, A, B0) ==
+            // fma(min_lanes v, A, B0) bit for bit: combine the pair per lane first and
+            // reduce once per bound (2 warp reductions per pair instead of 4)
+            const f2 lo2 = fma2(vv[p], h1.x, h1.y);
+            const f2 hi2 = fma2(vv[p], h1.x, pk(h2.x, h2.y));
+            const int u0 = max(0, ceil_i(warp_min(fminf(lo(lo2), hi(lo2)))));
+            const int u1 = min(nb - 1, floor_i(warp_max(fmaxf(lo(hi2), hi(hi2)))));
+#endif
             up[p] = reinterpret_cast<const char *>(hp + kTcPairHdr) + u0 * (4 * kTcPairUnit);
             nmax = max(nmax, u1 - u0 + 1);
             w[g + p] = 0ull;

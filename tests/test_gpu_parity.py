@@ -345,7 +345,7 @@ def test_nccl_self_exchange_slabs_bitwise_equal_full(torch_cuda, P, nslabs):
     full = eng.denoise(f)
     u = torch.empty_like(f)
     P.tnrd_denoise_slabs_nccl_self(eng.h, f, u, nslabs)
-    torch.cuda.synchronize()
+    P.tnrd_comm_wait(eng.h, timeout_ms=60000)   # drains the stream, polls the async error
     assert torch.equal(full, u)
     eng.close()
 
