@@ -91,18 +91,26 @@ struct alignas(64) TcArgs {
     int use_tma;   // 0: u tiles by per-element loads (rows not 16-byte aligned / no driver entry point)
     unsigned long long *prof;   // TNRD_TC_PROF builds: per CTA and warp {wait cycles, total cycles}
 };
-#ifdef TNRD_TC_WAITNAP
-// experiment: phi / build-gather waits as test_wait + __nanosleep(TNRD_TC_WAITNAP ns) polls
-__device__ __forceinline__ void mbar_wait_pw(uint64_t *bar, uint32_t parity) {
-    while (!mbar_test(bar, parity, false)) __nanosleep(TNRD_TC_WAITNAP);
-}
-#else
-__device__ __forceinline__ void mbar_wait_pw(uint64_t *bar, uint32_t parity) { mbar_wait(bar, parity); }
+// phi (V) and build/gather (Z) waits: test_wait + __nanosleep(NAP ns) polls (0: try_wait
+// with a suspend hint)
+#ifndef TNRD_TC_NAP_PHI
+#define TNRD_TC_NAP_PHI 256
 #endif
+#ifndef TNRD_TC_NAP_BG
+#define TNRD_TC_NAP_BG 0
+#endif
+template <int NAP>
+__device__ __forceinline__ void mbar_wait_nap(uint64_t *bar, uint32_t parity) {
+    if constexpr (NAP == 0) {
+        mbar_wait(bar, parity);
+    } else {
+        while (!mbar_test(bar, parity, false)) __nanosleep(NAP);
+    }
+}
 #ifdef TNRD_TC_PROF
-#define TCP_WAIT(bar, par) { const long long t0_ = clock64(); mbar_wait_pw(bar, par); tcp_wait += clock64() - t0_; }
+#define TCP_WAIT(NAP, bar, par) { const long long t0_ = clock64(); mbar_wait_nap<NAP>(bar, par); tcp_wait += clock64() - t0_; }
 #else
-#define TCP_WAIT(bar, par) mbar_wait_pw(bar, par)
+#define TCP_WAIT(NAP, bar, par) mbar_wait_nap<NAP>(bar, par)
 #endif
 
 // Shared memory (floats): operand block | u tiles [2][UH][UP] (128-byte aligned, TMA
@@ -231,7 +239,7 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
         Tile tT = tile_of(0);
         for (int g = 0; g < nblk; ++g) {
             const int s = g % kSlots;
-            TCP_WAIT(bar_v + s, (g / kSlots) & 1);
+            TCP_WAIT(TNRD_TC_NAP_PHI, bar_v + s, (g / kSlots) & 1);
             tc_fence_after();
             uint32_t vr[NFW];
             tmem_ld_nowait<NFW>(tl + VZ0 + VZW * s + h * NFW, vr);
@@ -387,7 +395,7 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
             const bool epi = ye >= 0 && x < OW && oye < a.y_end && oxe < W;
             float fv = 0.0f;
             if (epi) fv = __ldg(a.f.ptr + (long long)T.b * a.f.img_stride + (long long)(oye - a.f.row_base) * a.f.ld + oxe);
-            TCP_WAIT(bar_z + s, (g / kSlots) & 1);
+            TCP_WAIT(TNRD_TC_NAP_BG, bar_z + s, (g / kSlots) & 1);
             tc_fence_after();
             named_sync(BAR_BG, kNBG);  // every BG thread is done with gather(g - 1) and its epilogue
             if (i == 0 && n + 1 < ntl) request_u(n + 1);   // its buffer's last reader was tile n - 1
