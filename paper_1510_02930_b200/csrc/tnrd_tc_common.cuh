@@ -218,29 +218,31 @@ __device__ __forceinline__ void phi_fpairs(const float *__restrict__ s_pp, int p
             nmax = max(nmax, u1 - u0 + 1);
             w[g + p] = 0ull;
         }
+        // one unit of pair p: t, the cut, G and R (two ex2 each), the degree-7 Horner sum
+        const auto unit = [&](int p) {
+            const ulonglong2 *qp = reinterpret_cast<const ulonglong2 *>(up[p]);
+            up[p] += 4 * kTcPairUnit;
+            const ulonglong2 q0 = qp[0], q1 = qp[1], q2 = qp[2], q3 = qp[3];
+            const unsigned long long c7 = reinterpret_cast<const unsigned long long *>(qp + 4)[0];
+            // q0 = {ct, c0}, q1 = {c1, c2}, q2 = {c3, c4}, q3 = {c5, c6}  (pairs)
+            const f2 t = fma2(vv[p], as2[p], q0.x);
+            const f2 q = fma2(t, bc(-kCutBig), bc(-kCutBig * kCutT));
+            const f2 sq = fma2(t, t, pk(fmaxf(lo(q), 0.0f), fmaxf(hi(q), 0.0f)));
+            const f2 G = pk(ex2_ftz(-lo(sq)), ex2_ftz(-hi(sq)));
+            const f2 yr = mul2(t, tsg2[p]);
+            const f2 Rr = pk(ex2_ftz(fminf(lo(yr), yra[p])), ex2_ftz(fminf(hi(yr), yrb[p])));
+            f2 h = fma2(Rr, c7, q3.y);
+            h = fma2(h, Rr, q3.x);
+            h = fma2(h, Rr, q2.y);
+            h = fma2(h, Rr, q2.x);
+            h = fma2(h, Rr, q1.y);
+            h = fma2(h, Rr, q1.x);
+            h = fma2(h, Rr, q0.y);
+            w[g + p] = fma2(G, h, w[g + p]);
+        };
         for (int j = 0; j < nmax; ++j) {
 #pragma unroll
-            for (int p = 0; p < GP; ++p) {
-                const ulonglong2 *qp = reinterpret_cast<const ulonglong2 *>(up[p]);
-                up[p] += 4 * kTcPairUnit;
-                const ulonglong2 q0 = qp[0], q1 = qp[1], q2 = qp[2], q3 = qp[3];
-                const unsigned long long c7 = reinterpret_cast<const unsigned long long *>(qp + 4)[0];
-                // q0 = {ct, c0}, q1 = {c1, c2}, q2 = {c3, c4}, q3 = {c5, c6}  (pairs)
-                const f2 t = fma2(vv[p], as2[p], q0.x);
-                const f2 q = fma2(t, bc(-kCutBig), bc(-kCutBig * kCutT));
-                const f2 sq = fma2(t, t, pk(fmaxf(lo(q), 0.0f), fmaxf(hi(q), 0.0f)));
-                const f2 G = pk(ex2_ftz(-lo(sq)), ex2_ftz(-hi(sq)));
-                const f2 yr = mul2(t, tsg2[p]);
-                const f2 Rr = pk(ex2_ftz(fminf(lo(yr), yra[p])), ex2_ftz(fminf(hi(yr), yrb[p])));
-                f2 h = fma2(Rr, c7, q3.y);
-                h = fma2(h, Rr, q3.x);
-                h = fma2(h, Rr, q2.y);
-                h = fma2(h, Rr, q2.x);
-                h = fma2(h, Rr, q1.y);
-                h = fma2(h, Rr, q1.x);
-                h = fma2(h, Rr, q0.y);
-                w[g + p] = fma2(G, h, w[g + p]);
-            }
+            for (int p = 0; p < GP; ++p) unit(p);
         }
     }
 }
