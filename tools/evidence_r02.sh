@@ -8,6 +8,8 @@ tag=${1:-r02}
 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
 TNRD_PARITY_REPORT=gpurun_out/parity_$tag.json timeout 1800 python -m pytest tests -m gpu -q 2>&1 | tail -3
 timeout 600 python bench.py > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err; python tools/bench_line.py C4 < gpurun_out/bench_$tag.json
+timeout 300 python bench.py --config 1 --steps 1000 --no-cpu-baseline > gpurun_out/bench_c1_$tag.json 2>/dev/null; python tools/bench_line.py C1 < gpurun_out/bench_c1_$tag.json
+timeout 300 python bench.py --config 2 --steps 1000 --no-cpu-baseline > gpurun_out/bench_c2_$tag.json 2>/dev/null; python tools/bench_line.py C2 < gpurun_out/bench_c2_$tag.json
 timeout 300 python bench.py --config 3 --steps 1000 --no-cpu-baseline > gpurun_out/bench_c3_$tag.json 2>/dev/null; python tools/bench_line.py C3 < gpurun_out/bench_c3_$tag.json
 timeout 300 python bench.py --config 5 --steps 10 --no-cpu-baseline --no-e2e > gpurun_out/bench_c5_$tag.json 2>/dev/null; python tools/bench_line.py C5 < gpurun_out/bench_c5_$tag.json
 timeout 300 python bench.py --phi table --no-cpu-baseline > gpurun_out/bench_table_$tag.json 2>/dev/null; python tools/bench_line.py table < gpurun_out/bench_table_$tag.json
@@ -21,4 +23,8 @@ for c in 4 3 5; do
   tail -1 gpurun_out/${tag}_c${c}_ncu.log
 done
 ncu -i gpurun_out/${tag}_c4_stage.ncu-rep --page source --csv --print-source sass > gpurun_out/${tag}_c4_src.csv 2>/dev/null
-timeout 1800 python tools/oracle_timing.py > gpurun_out/oracle_timing_$tag.json 2> gpurun_out/oracle_timing_$tag.err; tail -6 gpurun_out/oracle_timing_$tag.err
+# the NCCL halo exchange on hardware: launch list of the 1-rank self send/recv slab test
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/nccl_self_launches_$tag.csv \
+   python -m pytest tests/test_gpu_parity.py -q -k "nccl_self_exchange and 2" > gpurun_out/nccl_self_$tag.log 2>&1; tail -1 gpurun_out/nccl_self_$tag.log
+grep -c ncclDevKernel gpurun_out/nccl_self_launches_$tag.csv
+[ -n "$ORACLE_TIMING" ] && timeout 1800 python tools/oracle_timing.py > gpurun_out/oracle_timing_$tag.json 2> gpurun_out/oracle_timing_$tag.err; tail -6 gpurun_out/oracle_timing_$tag.err
