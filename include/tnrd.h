@@ -163,7 +163,14 @@ TNRD_API tnrd_status tnrd_set_stage_params(tnrd_handle *h, int t, const float *f
  *   peak   host [B] or NULL: per-image peak (P l.113-116), metadata only -- Eq.13
  *          does not use it; it is validated (> 0, finite) when given.
  * Scratch (one ping-pong image batch) is owned by the handle and grown on demand
- * (synchronously, before enqueueing).  ESTATE if any stage is unset. */
+ * (synchronously, before enqueueing).  ESTATE if any stage is unset.
+ * Stream-ordered and asynchronous: the T stage launches are captured once per
+ * argument set (pointers, sizes, ld) as a CUDA graph on a handle-owned stream and
+ * replayed on cuda_stream (16 most recent kept; dropped by tnrd_set_stage_params /
+ * tnrd_set_engine; TNRD_GRAPH=0 in the environment launches eagerly).  Each stage
+ * kernel is a programmatic dependent launch: its set-up overlaps the previous
+ * stage's tail, its image accesses wait for that stage to complete
+ * (DESIGN.md §5.13). */
 TNRD_API tnrd_status tnrd_denoise(tnrd_handle *h, const float *f_dev, float *u_dev, int B, int H, int W,
                          long long ld, const float *peak, void *cuda_stream);
 

@@ -617,3 +617,25 @@ def test_graph_replay_bitwise_equal_to_eager_and_invalidated(torch_cuda, P):
     assert torch.equal(u2, u2_eager)
     eng.close()
     eager.close()
+
+
+def test_unaligned_rows_take_the_per_element_u_path_bitwise(torch_cuda, P):
+    """Rows whose pitch is not a multiple of 16 bytes cannot be TMA boxes: the
+    persistent kernel then loads u tiles element by element (reflect + clamp), the
+    operation the TMA box + mirror fix-up replaces.  Both give the same bits."""
+    torch = torch_cuda
+    p = make_problem(2)
+    H, W = p.f.shape[1:]
+    dense = torch.from_numpy(np.ascontiguousarray(p.f)).cuda()
+    eng = P.TNRD(p.model)
+    u_dense = eng.denoise(dense)
+    for pitch in (W + 3, W + 5):       # 4 * pitch % 16 != 0
+        buf = torch.zeros((1, H, pitch), device="cuda")
+        buf[:, :, :W] = dense
+        f_view = buf[:, :, :W]
+        u_buf = torch.full((1, H, pitch), float("nan"), device="cuda")
+        u_view = u_buf[:, :, :W]
+        eng.denoise(f_view, u_view)
+        torch.cuda.synchronize()
+        assert torch.equal(u_view, u_dense), pitch
+    eng.close()
