@@ -34,8 +34,13 @@
 // and add each output pixel's K tap rows of the block to d in a fixed order (a
 // ascending, b ascending), so d is deterministic and independent of tiling and
 // batching (R2: mirror-image terms at image edges, w = 0 outside the image).
-// Hand-offs are mbarriers; see tc_stage_kernel.  Macros TNRD_EXP_* and TNRD_TC_GP
-// are timing experiments / tuning knobs, never set in the product build.
+// (6) the same warps finish the two output rows the block completed (u - d, the
+// reaction, the store).  The kernel is persistent: one CTA per SM walks its tiles
+// with one M-block pipeline across tile boundaries, u tiles arrive by TMA, and the
+// forward / adjoint MMAs are issued by two warps.  Hand-offs are
+// mbarriers; see tc_stage_kernel.  Macros TNRD_EXP_*, TNRD_TC_PROF and TNRD_TC_{BG,
+// GP, PG, MMAW, 2MMA, NAP_*} are timing experiments / tuning knobs whose defaults
+// are the product.
 #include "tnrd_tc_common.cuh"
 
 #include <algorithm>
