@@ -39,8 +39,8 @@
 // with one M-block pipeline across tile boundaries, u tiles arrive by TMA, and the
 // forward / adjoint MMAs are issued by two warps.  Hand-offs are
 // mbarriers; see tc_stage_kernel.  Macros TNRD_EXP_*, TNRD_TC_PROF and TNRD_TC_{BG,
-// GP, PG, MMAW, 2MMA, NAP_*} are timing experiments / tuning knobs whose defaults
-// are the product.
+// GP, PG, MMAW, 2MMA, RELAY, PHI_HW, NAP_*} are timing experiments / tuning knobs
+// whose defaults are the product.
 #include "tnrd_tc_common.cuh"
 
 #include <algorithm>
@@ -56,15 +56,22 @@ namespace {
 #endif
 constexpr int kBG = TNRD_TC_BG;                 // build / gather warps (4 or 8: one or two per lane quarter)
 constexpr int kNBG = 32 * kBG;                  // build / gather threads
+#ifndef TNRD_TC_PHI_HW
+#define TNRD_TC_PHI_HW 1
+#endif
 #ifndef TNRD_TC_MMAW
-#define TNRD_TC_MMAW 0
+#define TNRD_TC_MMAW 1
 #endif
 #ifndef TNRD_TC_2MMA
 #define TNRD_TC_2MMA 1
 #endif
 constexpr bool kMmaWarp = TNRD_TC_MMAW;         // MMAs issued by the converged warp (elected lane)
 constexpr int kNMMA = TNRD_TC_2MMA ? 2 : 1;     // MMA issuer warps (2: forward and adjoint banks apart)
-constexpr int kTNT = (4 * kPG + kBG + kNMMA) * 32;  // phi warps, build / gather warps, MMA warp(s)
+#ifndef TNRD_TC_RELAY
+#define TNRD_TC_RELAY 1
+#endif
+constexpr int kRelay = TNRD_TC_RELAY;           // 1: a relay warp turns V_full into a hardware barrier for the phi warps
+constexpr int kTNT = (4 * kPG + kBG + kNMMA + (kRelay ? 1 : 0)) * 32;  // phi warps, build / gather warps, MMA warp(s), relay
 static_assert(kBG == 4 || kBG == 8, "build / gather warps");
 
 template <int K, int NK>
@@ -151,9 +158,15 @@ __host__ __device__ constexpr int tc_smem_floats(int oh, int par_floats) {
 //               (u - d, reaction, store).  u tiles are double buffered: tile n+1's
 //               is requested by TMA when tile n starts and waited for (plus the
 //               mirror fix-up of edge tiles) before its first im2col row.
-//   last warp   lane 0 issues the 3xTF32 MMAs: F(g) on A_full(g) -> V_full(g),
-//               Adj(g) on W_full(g) -> Z_full(g), in the order F(0..2), Adj(0),
-//               F(3), Adj(1), F(4), ...
+//   2 MMA warps (converged, one elected lane issues the 3xTF32 MMAs): one issues F(g)
+//               on A_full(g) -> V_full(g), the other Adj(g) on W_full(g) -> Z_full(g)
+//   relay warp  waits for V_full(g) (the mbarrier the MMA commit arrives on) and
+//               arrives on the hardware barrier BAR_V + slot the phi warps sleep in:
+//               16 polling phi warps cost 1.06 G spin instructions per C4 launch
+//               (13 % of all issued, ncu) - a bar.sync wait costs none
+// phi: the two half-warps of a phi warp swap half of their responses, so a thread
+// evaluates NFW/2 filters on two pixels with one set of constants (phi_halfwarp:
+// half the broadcast constant loads and range set-ups, bitwise the same w).
 template <int K, int NK, bool TABLE, bool R2, bool RN>
 __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant__ TcArgs p) {
     using G = TcGeo<K, NK>;
@@ -161,7 +174,7 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
     constexpr int NFW = G::NFW, NCH = G::NCH, NZC = G::NZC, SLOT = G::SLOT, PG = G::PG, DR = G::DR;
     constexpr int WBG = 4 * kPG, WMMA = WBG + kBG;   // first build / gather warp, MMA warp
     constexpr int VZ0 = kSlots * SLOT, VZW = NK > NZ ? NK : NZ;  // V / Z columns of slot s at VZ0 + VZW s
-    constexpr int BAR_BG = 1;
+    constexpr int BAR_BG = 1, BAR_V = 2;             // named barriers: build / gather group, V of slot s at BAR_V + s
     const StageArgs &a = p.a;
     extern __shared__ __align__(1024) float4 smem4[];
     float *s_par = reinterpret_cast<float *>(smem4);
@@ -244,7 +257,17 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
         Tile tT = tile_of(0);
         for (int g = 0; g < nblk; ++g) {
             const int s = g % kSlots;
-            TCP_WAIT(TNRD_TC_NAP_PHI, bar_v + s, (g / kSlots) & 1);
+            if constexpr (kRelay) {
+#ifdef TNRD_TC_PROF
+                const long long t0_ = clock64();
+#endif
+                asm volatile("bar.sync %0, %1;" ::"r"(BAR_V + s), "n"((4 * PG + 1) * 32) : "memory");
+#ifdef TNRD_TC_PROF
+                tcp_wait += clock64() - t0_;
+#endif
+            } else {
+                TCP_WAIT(TNRD_TC_NAP_PHI, bar_v + s, (g / kSlots) & 1);
+            }
             tc_fence_after();
             uint32_t vr[NFW];
             tmem_ld_nowait<NFW>(tl + VZ0 + VZW * s + h * NFW, vr);
@@ -273,7 +296,12 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
                     else w[e / 2] = pk(r, 0.0f);
                 }
             } else {
+#if TNRD_TC_PHI_HW
+                if constexpr (NFW % 4 == 0) phi_halfwarp<NFW>(s_pp + h * (NFW / 2) * pps, pps, vr, w, lane);
+                else phi_fpairs<NFW / 2>(s_pp + h * (NFW / 2) * pps, pps, vr, w);
+#else
                 phi_fpairs<NFW / 2>(s_pp + h * (NFW / 2) * pps, pps, vr, w);
+#endif
             }
 #endif
             // R2 (exact K^T): w is zero outside the image (the gather adds the mirror
@@ -502,6 +530,18 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
                 *dp = 0.0f;
             }
             if (++i == nmb) { i = 0; if (++n < ntl) T = tile_of(n); }
+        }
+    } else if (kRelay && warp == WMMA + kNMMA) {
+        // ======================= relay: V_full(g) (an mbarrier the MMA commit arrives on)
+        // becomes an arrival on the hardware barrier BAR_V + s the phi warps sleep in, so
+        // 16 warps do not poll.  A slot's barrier is reused only after every phi warp has
+        // left it: V(g + 3) needs A(g + 3), built after Z(g), i.e. after W_full(g).
+        for (int g = 0; g < nblk; ++g) {
+            const int s = g % kSlots;
+            mbar_wait(bar_v + s, (g / kSlots) & 1);
+            tc_fence_after();
+            tc_fence_before();
+            asm volatile("bar.arrive %0, %1;" ::"r"(BAR_V + s), "n"((4 * PG + 1) * 32) : "memory");
         }
     } else if (TABLE || kMmaWarp || lane == 0) {
         // ======================= MMA issuer: one thread with the exact phi; the

@@ -247,6 +247,100 @@ __device__ __forceinline__ void phi_fpairs(const float *__restrict__ s_pp, int p
     }
 }
 
+// The same phi with the warp's filters split between its half-warps: lanes L and
+// L + 16 (two pixels 16 columns apart in one row) swap half of their responses, so
+// lane L < 16 holds filters [0, NF/2) and lane L + 16 filters [NF/2, NF) of BOTH
+// pixels.  A thread then runs each of its NF/4 filter pairs on two pixels with one
+// set of constants: half the broadcast constant loads (a 128-bit shared-memory load
+// costs two wavefronts whether its lanes read one address or one per half-warp) and
+// half the range set-ups per warp; the influences of the partner's pixel go back by
+// a second swap.  Per value the arithmetic is phi_fpairs': the same units in the
+// same order; a half-warp's unit range is the union over its 32 values' pixels (the
+// same 32 pixels as before), and units outside a value's own range are exactly 0, so
+// w is bitwise unchanged.  Warp-collective (shuffles, warp reductions, votes).
+template <int NF>
+__device__ __forceinline__ void phi_halfwarp(const float *__restrict__ s_pp, int pps, const uint32_t (&vr)[NF],
+                                             f2 (&w)[NF / 2], int lane) {
+    static_assert(NF % 4 == 0, "two filter pairs per half-warp at least");
+    constexpr int HF = NF / 2, NP = NF / 4;   // filters, filter pairs per half-warp
+    const bool upper = lane >= 16;
+    uint32_t mine[HF], oth[HF];
+#pragma unroll
+    for (int k = 0; k < HF; ++k) {
+        mine[k] = upper ? vr[HF + k] : vr[k];
+        oth[k] = __shfl_xor_sync(0xffffffffu, upper ? vr[k] : vr[HF + k], 16);
+    }
+    const float *hp0 = s_pp + (upper ? NP * pps : 0);
+    const float inf = __int_as_float(0x7f800000);
+    f2 wm[NP], wo[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        const float *hp = hp0 + p * pps;
+        const float4 h0 = *reinterpret_cast<const float4 *>(hp);       // a_s, two_sg
+        const ulonglong2 h1 = *reinterpret_cast<const ulonglong2 *>(hp + 4);  // {A}, {B0}
+        const float4 h2 = *reinterpret_cast<const float4 *>(hp + 8);   // B1, yrmax
+        const int nb = __float_as_int(hp[12]);
+        const f2 va = pk(__uint_as_float(mine[2 * p]), __uint_as_float(mine[2 * p + 1]));
+        const f2 vb = pk(__uint_as_float(oth[2 * p]), __uint_as_float(oth[2 * p + 1]));
+        const f2 as2 = pk(h0.x, h0.y), tsg2 = pk(h0.z, h0.w);
+        const float yra = h2.z, yrb = h2.w;
+        // unit range of this half-warp's 32 values per filter: A > 0 and fma rounding
+        // is monotone, so the min / max commute with the fma (phi_fpairs)
+        const f2 la = fma2(va, h1.x, h1.y), lb = fma2(vb, h1.x, h1.y);
+        const f2 ha = fma2(va, h1.x, pk(h2.x, h2.y)), hb = fma2(vb, h1.x, pk(h2.x, h2.y));
+        const float l = fminf(fminf(lo(la), hi(la)), fminf(lo(lb), hi(lb)));
+        const float g = fmaxf(fmaxf(lo(ha), hi(ha)), fmaxf(lo(hb), hi(hb)));
+        const float lL = warp_min(upper ? inf : l), lU = warp_min(upper ? l : inf);
+        const float gL = warp_max(upper ? -inf : g), gU = warp_max(upper ? g : -inf);
+        const int u0r = max(0, ceil_i(upper ? lU : lL));
+        const int u1 = min(nb - 1, floor_i(upper ? gU : gL));
+        const int u0 = min(u0r, max(2 * nb - 2, 0));   // two units from u0 stay inside the 2 NB stored
+        const int n = u1 - u0r + 1;                    // own units; <= 0: none (u0 = u0r whenever n > 0)
+        const char *up = reinterpret_cast<const char *>(hp + kTcPairHdr) + u0 * (4 * kTcPairUnit);
+        f2 acca = 0ull, accb = 0ull;
+        const auto unit = [&]() {
+            const ulonglong2 *qp = reinterpret_cast<const ulonglong2 *>(up);
+            up += 4 * kTcPairUnit;
+            const ulonglong2 q0 = qp[0], q1 = qp[1], q2 = qp[2], q3 = qp[3];
+            const unsigned long long c7 = reinterpret_cast<const unsigned long long *>(qp + 4)[0];
+            const f2 ta = fma2(va, as2, q0.x), tb = fma2(vb, as2, q0.x);
+            const f2 qa = fma2(ta, bc(-kCutBig), bc(-kCutBig * kCutT)), qb = fma2(tb, bc(-kCutBig), bc(-kCutBig * kCutT));
+            const f2 sa = fma2(ta, ta, pk(fmaxf(lo(qa), 0.0f), fmaxf(hi(qa), 0.0f)));
+            const f2 sb = fma2(tb, tb, pk(fmaxf(lo(qb), 0.0f), fmaxf(hi(qb), 0.0f)));
+            const f2 Ga = pk(ex2_ftz(-lo(sa)), ex2_ftz(-hi(sa))), Gb = pk(ex2_ftz(-lo(sb)), ex2_ftz(-hi(sb)));
+            const f2 ya = mul2(ta, tsg2), yb = mul2(tb, tsg2);
+            const f2 Ra = pk(ex2_ftz(fminf(lo(ya), yra)), ex2_ftz(fminf(hi(ya), yrb)));
+            const f2 Rb = pk(ex2_ftz(fminf(lo(yb), yra)), ex2_ftz(fminf(hi(yb), yrb)));
+            f2 xa = fma2(Ra, c7, q3.y), xb = fma2(Rb, c7, q3.y);
+            xa = fma2(xa, Ra, q3.x); xb = fma2(xb, Rb, q3.x);
+            xa = fma2(xa, Ra, q2.y); xb = fma2(xb, Rb, q2.y);
+            xa = fma2(xa, Ra, q2.x); xb = fma2(xb, Rb, q2.x);
+            xa = fma2(xa, Ra, q1.y); xb = fma2(xb, Rb, q1.y);
+            xa = fma2(xa, Ra, q1.x); xb = fma2(xb, Rb, q1.x);
+            xa = fma2(xa, Ra, q0.y); xb = fma2(xb, Rb, q0.y);
+            acca = fma2(Ga, xa, acca);
+            accb = fma2(Gb, xb, accb);
+        };
+        unit();
+        unit();
+        // further units (the evaluation window of 32 adjacent pixels rarely spans
+        // more than two): only the lanes that own them, the others' pointers stay put
+#pragma unroll 1
+        for (int j = 2; __any_sync(0xffffffffu, j < n); ++j)
+            if (j < n) unit();
+        wm[p] = acca;
+        wo[p] = accb;
+    }
+    // the partner's influences go back; own pixel: filters [0, HF) from the lower
+    // lane of the pair, [HF, NF) from the upper one
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        const f2 r = __shfl_xor_sync(0xffffffffu, wo[p], 16);
+        w[p] = upper ? r : wm[p];
+        w[NP + p] = upper ? wm[p] : r;
+    }
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
