@@ -68,10 +68,15 @@ constexpr int kNBG = 32 * kBG;                  // build / gather threads
 constexpr bool kMmaWarp = TNRD_TC_MMAW;         // MMAs issued by the converged warp (elected lane)
 constexpr int kNMMA = TNRD_TC_2MMA ? 2 : 1;     // MMA issuer warps (2: forward and adjoint banks apart)
 #ifndef TNRD_TC_RELAY
-#define TNRD_TC_RELAY 1
+#define TNRD_TC_RELAY 2
 #endif
-constexpr int kRelay = TNRD_TC_RELAY;           // 1: a relay warp turns V_full into a hardware barrier for the phi warps
-constexpr int kTNT = (4 * kPG + kBG + kNMMA + (kRelay ? 1 : 0)) * 32;  // phi warps, build / gather warps, MMA warp(s), relay
+constexpr int kRelay = TNRD_TC_RELAY;           // a relay warp turns V_full into hardware barriers for the phi warps (2: one per lane quarter; 1: one; 0: the phi warps poll)
+#ifdef TNRD_TC_TRACE
+constexpr int kObs = 1;                         // trace builds: an observer warp stamps Z_full(g)
+#else
+constexpr int kObs = 0;
+#endif
+constexpr int kTNT = (4 * kPG + kBG + kNMMA + (kRelay ? 1 : 0) + kObs) * 32;  // phi warps, build / gather warps, MMA warp(s), relay
 static_assert(kBG == 4 || kBG == 8, "build / gather warps");
 
 template <int K, int NK>
@@ -119,14 +124,27 @@ __device__ __forceinline__ void mbar_wait_nap(uint64_t *bar, uint32_t parity) {
         while (!mbar_test(bar, parity, false)) __nanosleep(NAP);
     }
 }
+// TNRD_TC_TRACE builds (with TNRD_TC_PROF): CTA 0 stamps clock64 per block g and event e
+// into prof[16384 + 64 (g - 1000) + e], 1000 <= g < 1256 (e >= 8: build / gather warp (e - 8) / 6,
+// step (e - 8) % 6: has Z, Z moved, A built, second sync passed, gathered, epilogue done; e: 0 phi warp 0 has V, 1 its W arrived, 2 build/gather has
+// Z, 3 A(g + 3) arrived, 4 epilogue done, 5 relay saw V_full, 6 Adj issuer saw W_full,
+// 7 F issuer saw A_full); launch_tc writes them to gpurun_out/tc_trace.bin
+#ifdef TNRD_TC_TRACE
+// TNRD_TC_TRACE=1: only events 0, 1, 2 and 56 (light: the stamps themselves cost issue slots)
+#define TCT(g, e, cond) if ((TNRD_TC_TRACE > 1 || (e) <= 2 || (e) == 56) && blockIdx.x == 0 && (cond) && (g) >= 1000 && (g) < 1256) p.prof[16384 + 64 * ((g) - 1000) + (e)] = (unsigned long long)clock64()
+#else
+#define TCT(g, e, cond)
+#endif
 #ifdef TNRD_TC_PROF
 #define TCP_WAIT(NAP, bar, par) { const long long t0_ = clock64(); mbar_wait_nap<NAP>(bar, par); tcp_wait += clock64() - t0_; }
+#define TCP_SYNC(id, n) { const long long t0_ = clock64(); named_sync(id, n); tcp_wait += clock64() - t0_; }
 #else
 #define TCP_WAIT(NAP, bar, par) mbar_wait_nap<NAP>(bar, par)
+#define TCP_SYNC(id, n) named_sync(id, n)
 #endif
 
 // Shared memory (floats): operand block | u tiles [2][UH][UP] (128-byte aligned, TMA
-// destinations) | d ring [DR][OW] | Z of one M-block [KT][kZP] | mbarriers
+// destinations) | d ring [DR][OW] | Z of two M-blocks [2][KT][kZP] | mbarriers
 // (4 x kSlots + 2) | TMEM address.
 template <int K, int NK>
 __host__ __device__ constexpr int tc_u_floats(int oh) {
@@ -136,7 +154,7 @@ __host__ __device__ constexpr int tc_u_floats(int oh) {
 template <int K, int NK>
 __host__ __device__ constexpr int tc_smem_floats(int oh, int par_floats) {
     using G = TcGeo<K, NK>;
-    return round32(par_floats) + 2 * tc_u_floats<K, NK>(oh) + round4(G::DR * G::OW) + G::KT * kZP +
+    return round32(par_floats) + 2 * tc_u_floats<K, NK>(oh) + round4(G::DR * G::OW) + 2 * G::KT * kZP +
            2 * (4 * kSlots + 2) + 4;
 }
 
@@ -161,7 +179,7 @@ __host__ __device__ constexpr int tc_smem_floats(int oh, int par_floats) {
 //   2 MMA warps (converged, one elected lane issues the 3xTF32 MMAs): one issues F(g)
 //               on A_full(g) -> V_full(g), the other Adj(g) on W_full(g) -> Z_full(g)
 //   relay warp  waits for V_full(g) (the mbarrier the MMA commit arrives on) and
-//               arrives on the hardware barrier BAR_V + slot the phi warps sleep in:
+//               arrives on the hardware barriers (one per slot and lane quarter) the phi warps sleep in:
 //               16 polling phi warps cost 1.06 G spin instructions per C4 launch
 //               (13 % of all issued, ncu) - a bar.sync wait costs none
 // phi: the two half-warps of a phi warp swap half of their responses, so a thread
@@ -185,8 +203,8 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
     const int UF = tc_u_floats<K, NK>(OH);
     float *s_u0 = s_par + round32(a.tc_par_floats);  // u tile of local tile n: s_u0 + (n & 1) UF
     float *s_d = s_u0 + 2 * UF;                      // ring: output row y at (y % DR) OW
-    float *s_z = s_d + round4(DR * OW);              // [KT][kZP]
-    uint64_t *bar_a = reinterpret_cast<uint64_t *>(s_z + KT * kZP);   // A_full[kSlots]
+    float *s_z0 = s_d + round4(DR * OW);             // [2][KT][kZP]: Z of block g at (g & 1) KT kZP
+    uint64_t *bar_a = reinterpret_cast<uint64_t *>(s_z0 + 2 * KT * kZP);   // A_full[kSlots]
     uint64_t *bar_v = bar_a + kSlots, *bar_w = bar_v + kSlots, *bar_z = bar_w + kSlots;
     uint64_t *bar_u = bar_z + kSlots;                // u tile landed [2]
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(bar_u + 2);
@@ -261,7 +279,10 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
 #ifdef TNRD_TC_PROF
                 const long long t0_ = clock64();
 #endif
-                asm volatile("bar.sync %0, %1;" ::"r"(BAR_V + s), "n"((4 * PG + 1) * 32) : "memory");
+                if constexpr (kRelay == 2)   // one barrier per slot and lane quarter (the PG warps of one scheduler)
+                    asm volatile("bar.sync %0, %1;" ::"r"(BAR_V + 4 * s + quarter), "n"((PG + 1) * 32) : "memory");
+                else
+                    asm volatile("bar.sync %0, %1;" ::"r"(BAR_V + s), "n"((4 * PG + 1) * 32) : "memory");
 #ifdef TNRD_TC_PROF
                 tcp_wait += clock64() - t0_;
 #endif
@@ -269,6 +290,7 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
                 TCP_WAIT(TNRD_TC_NAP_PHI, bar_v + s, (g / kSlots) & 1);
             }
             tc_fence_after();
+            TCT(g, 0, tid == 0);
             uint32_t vr[NFW];
             tmem_ld_nowait<NFW>(tl + VZ0 + VZW * s + h * NFW, vr);
             tmem_wait_ld(vr);
@@ -326,6 +348,7 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_w + s);
+            TCT(g, 1, tid == 0);
         }
     } else if (warp < WBG) {
         // phi warps of an unused group (N_k not divisible): idle until the end
@@ -381,19 +404,24 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
         };
         int bn = 0, bi = 0;            // tile / block of the next build (builds run in g order)
         Tile bT = tile_of(0);
-        const auto build = [&](int g) {
-            // im2col row (hi, lo) of pixel m of block g: v-region (j, c) uses its mirror
-            // in the image (R1), clamped into the tile for pixels no output needs
-            const int s = g % kSlots;
+        int bcol = 0;                  // per tile: float offset of this thread's im2col column in the u tiles
+        const auto build = [&](int s) {
+            // im2col row (hi, lo) of pixel m of the next block (TMEM slot s): v-region (j, c)
+            // uses its mirror in the image (R1), clamped into the tile for pixels no
+            // output needs.  The column part of the address is per tile, the row part
+            // per block
             const int n = bn, i = bi;
-            if (i == 0) ensure_u(n);
-            const Tile T = bT;
+            if (i == 0) {
+                ensure_u(n);
+                const int c = m & 63;
+                const int gx = reflect(bT.x0 - R + c, W);
+                const int pc = min(max(gx - bT.x0 + R, 0), kTcVW - 1);
+                bcol = (n & 1) * UF + lead_of(bT.x0) + 2 * R * UP + pc + 2 * R;
+            }
+            const int yv = bT.y0 - R;  // first v row of the tile
+            const int pj = min(max(reflect(yv + 2 * i + (m >> 6), H) - yv, 0), VH - 1);
+            const float *up = s_u0 + bcol + pj * UP;   // tap (ta, tb) reads up[-ta*UP - tb]
             if (++bi == nmb) { bi = 0; if (++bn < ntl) bT = tile_of(bn); }
-            const int j = 2 * i + (m >> 6), c = m & 63;
-            const int gy = reflect(T.y0 - R + j, H), gx = reflect(T.x0 - R + c, W);
-            const int pj = min(max(gy - T.y0 + R, 0), VH - 1);
-            const int pc = min(max(gx - T.x0 + R, 0), kTcVW - 1);
-            const float *up = s_u0 + (n & 1) * UF + lead_of(T.x0) + (pj + 2 * R) * UP + pc + 2 * R;  // tap (ta, tb) reads up[-ta*UP - tb]
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch) {
                 if (kBG == 8 && (ch < (NCH + 1) / 2) != (half == 0)) continue;   // chunks split by half
@@ -416,22 +444,40 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
             if (lane == 0) mbar_arrive(bar_a + s);
         };
         if (nblk > 0) request_u(0);
-        for (int g = 0; g < kSlots && g < nblk; ++g) build(g);
+        for (int g = 0; g < kSlots && g < nblk; ++g) build(g);   // slot g
         const int x = gt & 63;
+        // gather row group of this thread (rows rg, rg + kNBG/64, ... of the block's K + 1;
+        // groups 0 and 1 also run the epilogue).  With two warps per lane quarter the
+        // second half - whose share of the im2col / Z chunks is the smaller one (the
+        // last chunk is mostly padding) - takes groups 0 and 1, so the epilogue lands
+        // on the less loaded warps
+        const int rg = kBG == 8 ? ((gt >> 6) + 2) & 3 : gt >> 6;
         int n = 0, i = 0;              // tile / block of g
         Tile T = tile_of(0);
+        // per tile: element index of this thread's column in tile row 0 of f and of the output
+        long long fi_t = 0, oi_t = 0;
+        const auto tile_bases = [&]() {
+            fi_t = (long long)T.b * a.f.img_stride + (long long)(T.y0 - a.f.row_base) * a.f.ld + (T.x0 + x);
+            oi_t = (long long)T.b * a.out_img_stride + (long long)(T.y0 - a.out_row_base) * a.out_ld + (T.x0 + x);
+        };
+        tile_bases();
         for (int g = 0; g < nblk; ++g) {
             const int s = g % kSlots;
-            // the epilogue pixel of this block (threads gt < 128: output row 2i - (K-1) +
-            // gt/64, column x): its f is fetched now, used after the gather
-            const int ye = gt < 128 ? 2 * i - (K - 1) + (gt >> 6) : -1, oye = T.y0 + ye, oxe = T.x0 + x;
+            // the epilogue pixel of this block (row groups 0 and 1: output row 2i - (K-1) +
+            // rg, column x): its f is fetched now, used after the gather
+            const int ye = rg < 2 ? 2 * i - (K - 1) + rg : -1, oye = T.y0 + ye, oxe = T.x0 + x;
             const bool epi = ye >= 0 && x < OW && oye < a.y_end && oxe < W;
             float fv = 0.0f;
-            if (epi) fv = __ldg(a.f.ptr + (long long)T.b * a.f.img_stride + (long long)(oye - a.f.row_base) * a.f.ld + oxe);
+            if (epi) fv = __ldg(a.f.ptr + (fi_t + ye * a.f.ld));
             TCP_WAIT(TNRD_TC_NAP_BG, bar_z + s, (g / kSlots) & 1);
             tc_fence_after();
-            named_sync(BAR_BG, kNBG);  // every BG thread is done with gather(g - 1) and its epilogue
-            if (i == 0 && n + 1 < ntl) request_u(n + 1);   // its buffer's last reader was tile n - 1
+            TCT(g, 57 + (gt >> 5), lane == 0 && gt < 224);
+            TCT(g, 2, gt == 0);
+            TCT(g, 8 + 6 * (gt >> 5) + 0, lane == 0);
+            // Z(g) -> s_z[g & 1] (two buffers: the gather of block g - 1 may still be reading
+            // the other one; buffer g & 1 was last read by gather(g - 2), which every thread
+            // finished before the barrier of iteration g - 1)
+            float *s_z = s_z0 + (g & 1) * (KT * kZP);
 #pragma unroll
             for (int ch = 0; ch < NZC; ++ch) {
                 if (ch * 8 >= KT) continue;
@@ -444,17 +490,25 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
                     if (ch * 8 + e < KT) s_z[(ch * 8 + e) * kZP + m] = __uint_as_float(z[e]);
             }
             tc_fence_before();
-            if (g + kSlots < nblk) build(g + kSlots);  // slot s is free: W(g) consumed, Z(g) read
-            named_sync(BAR_BG, kNBG);
+            TCT(g, 8 + 6 * (gt >> 5) + 1, lane == 0);
+            if (g + kSlots < nblk) build(s);           // block g + 3 into slot s, free: W(g) consumed, Z(g) read
+            TCT(g, 3, gt == 0);
+            TCT(g, 8 + 6 * (gt >> 5) + 2, lane == 0);
+            TCP_SYNC(BAR_BG, kNBG);    // Z(g) is in shared memory; every thread is done with iteration g - 1
+            TCT(g, 8 + 6 * (gt >> 5) + 3, lane == 0);
+            if (i == 0 && n + 1 < ntl) request_u(n + 1);   // its buffer's last reader was tile n - 1
             // d(y, x) += sum_b Z[(y + a, x + b)][a K + b] over rows 2i, 2i + 1 (v row y + a):
-            // thread gt takes column x and the rows r = gt/64 (mod kNBG/64) of the block's
+            // thread gt takes column x and the rows r = rg (mod kNBG/64) of the block's
             // K + 1; the epilogue rows (r = 0, 1) are last written by their epilogue thread
             const int j0 = 2 * i;
             const bool r2_edge = R2 && (T.y0 - R < 0 || T.y0 + OH + R > H || T.x0 - R < 0 || T.x0 + OW + R > W);
             if (!R2 || !r2_edge) {
-                for (int r = gt >> 6; r < K + 1; r += kNBG / 64) {  // output rows j0 - (K-1) .. j0 + 1
+                constexpr int NRG = kNBG / 64;
+#pragma unroll
+                for (int k = 0; k < (K + NRG) / NRG; ++k) {    // output rows j0 - (K-1) .. j0 + 1
+                    const int r = rg + NRG * k;
                     const int y = j0 - (K - 1) + r;
-                    if (x >= OW || y < 0 || y >= OH) continue;
+                    if (r > K || x >= OW || y < 0 || y >= OH) continue;
                     float *dp = s_d + (y % DR) * OW + x;
                     float d = *dp;
 #pragma unroll
@@ -485,7 +539,7 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
                     }
                     return S;
                 };
-                for (int r = gt >> 6; r < K + 1; r += kNBG / 64) {
+                for (int r = rg; r < K + 1; r += kNBG / 64) {
                     const int y = j0 - (K - 1) + r;
                     if (x >= OW || y < 0 || y >= OH) continue;
                     const int gy = T.y0 + y, gx = T.x0 + x;
@@ -512,6 +566,7 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
                     *dp = d;
                 }
             }
+            TCT(g, 8 + 6 * (gt >> 5) + 4, lane == 0);
             // epilogue: output row ye is complete (its last v row, ye + K - 1, is in this
             // block): ut = u - d, u+ = reaction(ut); the ring row is cleared for reuse
             if (ye >= 0 && x < OW) {
@@ -523,13 +578,15 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
 #endif
                     const float u = s_u0[(n & 1) * UF + lead_of(T.x0) + (ye + 2 * R) * UP + x + 2 * R];
                     const float ut = u - *dp;
-                    const long long oi = (long long)T.b * a.out_img_stride + (long long)(oye - a.out_row_base) * a.out_ld + oxe;
+                    const long long oi = oi_t + ye * a.out_ld;
                     a.u_out[oi] = reaction_step(a.reaction, u, ut, a.lambda, fv);
                     if (a.ut_out) a.ut_out[oi] = ut;
                 }
                 *dp = 0.0f;
             }
-            if (++i == nmb) { i = 0; if (++n < ntl) T = tile_of(n); }
+            TCT(g, 4, gt == 0);
+            TCT(g, 8 + 6 * (gt >> 5) + 5, lane == 0);
+            if (++i == nmb) { i = 0; if (++n < ntl) { T = tile_of(n); tile_bases(); } }
         }
     } else if (kRelay && warp == WMMA + kNMMA) {
         // ======================= relay: V_full(g) (an mbarrier the MMA commit arrives on)
@@ -539,9 +596,21 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
         for (int g = 0; g < nblk; ++g) {
             const int s = g % kSlots;
             mbar_wait(bar_v + s, (g / kSlots) & 1);
+            TCT(g, 5, lane == 0);
             tc_fence_after();
             tc_fence_before();
-            asm volatile("bar.arrive %0, %1;" ::"r"(BAR_V + s), "n"((4 * PG + 1) * 32) : "memory");
+            if constexpr (kRelay == 2) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    asm volatile("bar.arrive %0, %1;" ::"r"(BAR_V + 4 * s + q), "n"((PG + 1) * 32) : "memory");
+            } else {
+                asm volatile("bar.arrive %0, %1;" ::"r"(BAR_V + s), "n"((4 * PG + 1) * 32) : "memory");
+            }
+        }
+    } else if (kObs && warp == WMMA + kNMMA + (kRelay ? 1 : 0)) {
+        for (int g = 0; g < nblk; ++g) {
+            mbar_wait(bar_z + g % kSlots, (g / kSlots) & 1);
+            TCT(g, 56, lane == 0);
         }
     } else if (TABLE || kMmaWarp || lane == 0) {
         // ======================= MMA issuer: one thread with the exact phi; the
@@ -605,9 +674,9 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
             // two issuers (warps on different SM sub-partitions): F(g) after A_full(g),
             // Adj(g) after W_full(g); each commit tracks its own thread's MMAs
             if (warp == WMMA) {
-                for (int g = 0; g < nblk; ++g) { mbar_wait(bar_a + g % kSlots, (g / kSlots) & 1); fwd(g); }
+                for (int g = 0; g < nblk; ++g) { mbar_wait(bar_a + g % kSlots, (g / kSlots) & 1); TCT(g, 7, lane == 0); fwd(g); }
             } else {
-                for (int g = 0; g < nblk; ++g) { mbar_wait(bar_w + g % kSlots, (g / kSlots) & 1); adj(g); }
+                for (int g = 0; g < nblk; ++g) { mbar_wait(bar_w + g % kSlots, (g / kSlots) & 1); TCT(g, 6, lane == 0); adj(g); }
             }
         } else {
             int gf = 0, ga = 0;
@@ -718,6 +787,13 @@ cudaError_t launch_tc(StageArgs &a, int B, cudaStream_t s) {
         fprintf(stderr, " %.1f", tt > 0 ? 100.0 * wt / tt : 0.0);
     }
     fprintf(stderr, "\n");
+#ifdef TNRD_TC_TRACE
+    {
+        std::vector<unsigned long long> tr(64 * 256);
+        cudaMemcpy(tr.data(), prof + 16384, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost);
+        if (FILE *fh = fopen("gpurun_out/tc_trace.bin", "wb")) { fwrite(tr.data(), sizeof(unsigned long long), tr.size(), fh); fclose(fh); }
+    }
+#endif
     return cudaGetLastError();
 #else
     cudaLaunchConfig_t cfg = {};
