@@ -144,7 +144,8 @@ __device__ __forceinline__ void mbar_wait_nap(uint64_t *bar, uint32_t parity) {
 #endif
 
 // Shared memory (floats): operand block | u tiles [2][UH][UP] (128-byte aligned, TMA
-// destinations) | d ring [DR][OW] | Z of two M-blocks [2][KT][kZP] | mbarriers
+// destinations) | d ring [DR][OW] | Z of two M-blocks [2][KT][kZP] (one with the
+// tabulated phi, whose table lives in L1: the unified L1 / shared memory is 256 KB) | mbarriers
 // (4 x kSlots + 2) | TMEM address.
 template <int K, int NK>
 __host__ __device__ constexpr int tc_u_floats(int oh) {
@@ -152,9 +153,9 @@ __host__ __device__ constexpr int tc_u_floats(int oh) {
     return round32((oh + 4 * G::R) * G::UP);
 }
 template <int K, int NK>
-__host__ __device__ constexpr int tc_smem_floats(int oh, int par_floats) {
+__host__ __device__ constexpr int tc_smem_floats(int oh, int par_floats, int zb = 2) {
     using G = TcGeo<K, NK>;
-    return round32(par_floats) + 2 * tc_u_floats<K, NK>(oh) + round4(G::DR * G::OW) + 2 * G::KT * kZP +
+    return round32(par_floats) + 2 * tc_u_floats<K, NK>(oh) + round4(G::DR * G::OW) + zb * G::KT * kZP +
            2 * (4 * kSlots + 2) + 4;
 }
 
@@ -203,8 +204,9 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
     const int UF = tc_u_floats<K, NK>(OH);
     float *s_u0 = s_par + round32(a.tc_par_floats);  // u tile of local tile n: s_u0 + (n & 1) UF
     float *s_d = s_u0 + 2 * UF;                      // ring: output row y at (y % DR) OW
-    float *s_z0 = s_d + round4(DR * OW);             // [2][KT][kZP]: Z of block g at (g & 1) KT kZP
-    uint64_t *bar_a = reinterpret_cast<uint64_t *>(s_z0 + 2 * KT * kZP);   // A_full[kSlots]
+    constexpr int ZB = TABLE ? 1 : 2;                // Z buffers (tabulated phi: one, the table wants the L1)
+    float *s_z0 = s_d + round4(DR * OW);             // [ZB][KT][kZP]: Z of block g at (g % ZB) KT kZP
+    uint64_t *bar_a = reinterpret_cast<uint64_t *>(s_z0 + ZB * KT * kZP);   // A_full[kSlots]
     uint64_t *bar_v = bar_a + kSlots, *bar_w = bar_v + kSlots, *bar_z = bar_w + kSlots;
     uint64_t *bar_u = bar_z + kSlots;                // u tile landed [2]
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(bar_u + 2);
@@ -477,7 +479,8 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
             // Z(g) -> s_z[g & 1] (two buffers: the gather of block g - 1 may still be reading
             // the other one; buffer g & 1 was last read by gather(g - 2), which every thread
             // finished before the barrier of iteration g - 1)
-            float *s_z = s_z0 + (g & 1) * (KT * kZP);
+            float *s_z = s_z0 + (ZB == 2 ? (g & 1) * (KT * kZP) : 0);
+            if constexpr (ZB == 1) TCP_SYNC(BAR_BG, kNBG);   // one buffer: gather(g - 1) must be over
 #pragma unroll
             for (int ch = 0; ch < NZC; ++ch) {
                 if (ch * 8 >= KT) continue;
@@ -752,10 +755,11 @@ cudaError_t launch_tc(StageArgs &a, int B, cudaStream_t s) {
     // the u tile of tile n + 1 is requested when tile n starts: a tile needs >= 4 M-blocks
     a.tc_oh = std::max(a.tc_oh, 8 - 2 * G::R);
     const DevInfo di = dev_info();
-    size_t smem = sizeof(float) * (size_t)tc_smem_floats<K, NK>(a.tc_oh, a.tc_par_floats);
+    const int zb = a.mode == MODE_TABLE ? 1 : 2;      // Z buffers (ZB of the kernel)
+    size_t smem = sizeof(float) * (size_t)tc_smem_floats<K, NK>(a.tc_oh, a.tc_par_floats, zb);
     while (smem > (size_t)di.optin && a.tc_oh > 8) {  // fewer rows per tile until it fits
         a.tc_oh -= 8;
-        smem = sizeof(float) * (size_t)tc_smem_floats<K, NK>(a.tc_oh, a.tc_par_floats);
+        smem = sizeof(float) * (size_t)tc_smem_floats<K, NK>(a.tc_oh, a.tc_par_floats, zb);
     }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
