@@ -68,9 +68,9 @@ constexpr int kNBG = 32 * kBG;                  // build / gather threads
 constexpr bool kMmaWarp = TNRD_TC_MMAW;         // MMAs issued by the converged warp (elected lane)
 constexpr int kNMMA = TNRD_TC_2MMA ? 2 : 1;     // MMA issuer warps (2: forward and adjoint banks apart)
 #ifndef TNRD_TC_RELAY
-#define TNRD_TC_RELAY 2
+#define TNRD_TC_RELAY 3
 #endif
-constexpr int kRelay = TNRD_TC_RELAY;           // a relay warp turns V_full into hardware barriers for the phi warps (2: one per lane quarter; 1: one; 0: the phi warps poll)
+constexpr int kRelay = TNRD_TC_RELAY;           // a relay warp turns V_full into hardware barriers for the phi warps (3: one per filter group; 2: one per lane quarter; 1: one; 0: the phi warps poll)
 #ifdef TNRD_TC_TRACE
 constexpr int kObs = 1;                         // trace builds: an observer warp stamps Z_full(g)
 #else
@@ -180,7 +180,9 @@ __host__ __device__ constexpr int tc_smem_floats(int oh, int par_floats, int zb 
 //   2 MMA warps (converged, one elected lane issues the 3xTF32 MMAs): one issues F(g)
 //               on A_full(g) -> V_full(g), the other Adj(g) on W_full(g) -> Z_full(g)
 //   relay warp  waits for V_full(g) (the mbarrier the MMA commit arrives on) and
-//               arrives on the hardware barriers (one per slot and lane quarter) the phi warps sleep in:
+//               arrives on the hardware barriers (one per slot and filter group: the 4 phi warps
+//               of a scheduler belong to 4 different barriers, so they are not forced into
+//               the same phase) the phi warps sleep in:
 //               16 polling phi warps cost 1.06 G spin instructions per C4 launch
 //               (13 % of all issued, ncu) - a bar.sync wait costs none
 // phi: the two half-warps of a phi warp swap half of their responses, so a thread
@@ -281,7 +283,9 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
 #ifdef TNRD_TC_PROF
                 const long long t0_ = clock64();
 #endif
-                if constexpr (kRelay == 2)   // one barrier per slot and lane quarter (the PG warps of one scheduler)
+                if constexpr (kRelay == 3)   // one barrier per slot and filter group: its 4 warps sit on 4 schedulers
+                    asm volatile("bar.sync %0, %1;" ::"r"(BAR_V + PG * s + h), "n"(5 * 32) : "memory");
+                else if constexpr (kRelay == 2)   // one barrier per slot and lane quarter (the PG warps of one scheduler)
                     asm volatile("bar.sync %0, %1;" ::"r"(BAR_V + 4 * s + quarter), "n"((PG + 1) * 32) : "memory");
                 else
                     asm volatile("bar.sync %0, %1;" ::"r"(BAR_V + s), "n"((4 * PG + 1) * 32) : "memory");
@@ -602,7 +606,11 @@ __global__ void __launch_bounds__(kTNT, 1) tc_stage_kernel(const __grid_constant
             TCT(g, 5, lane == 0);
             tc_fence_after();
             tc_fence_before();
-            if constexpr (kRelay == 2) {
+            if constexpr (kRelay == 3) {
+#pragma unroll
+                for (int q = 0; q < PG; ++q)
+                    asm volatile("bar.arrive %0, %1;" ::"r"(BAR_V + PG * s + q), "n"(5 * 32) : "memory");
+            } else if constexpr (kRelay == 2) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
                     asm volatile("bar.arrive %0, %1;" ::"r"(BAR_V + 4 * s + q), "n"((PG + 1) * 32) : "memory");
