@@ -60,7 +60,7 @@ constexpr int kNBG = 32 * kBG;                  // build / gather threads
 #define TNRD_TC_PHI_HW 1
 #endif
 #ifndef TNRD_TC_MMAW
-#define TNRD_TC_MMAW 1
+#define TNRD_TC_MMAW 0
 #endif
 #ifndef TNRD_TC_2MMA
 #define TNRD_TC_2MMA 1
@@ -177,8 +177,9 @@ __host__ __device__ constexpr int tc_smem_floats(int oh, int par_floats, int zb 
 //               (u - d, reaction, store).  u tiles are double buffered: tile n+1's
 //               is requested by TMA when tile n starts and waited for (plus the
 //               mirror fix-up of edge tiles) before its first im2col row.
-//   2 MMA warps (converged, one elected lane issues the 3xTF32 MMAs): one issues F(g)
-//               on A_full(g) -> V_full(g), the other Adj(g) on W_full(g) -> Z_full(g)
+//   2 MMA warps (lane 0 issues the 3xTF32 MMAs; the converged warp with an elected lane
+//               for the tabulated phi): one issues F(g) on A_full(g) -> V_full(g), the
+//               other Adj(g) on W_full(g) -> Z_full(g)
 //   relay warp  waits for V_full(g) (the mbarrier the MMA commit arrives on) and
 //               arrives on the hardware barriers (one per slot and filter group: the 4 phi warps
 //               of a scheduler belong to 4 different barriers, so they are not forced into
